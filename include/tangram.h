@@ -1,0 +1,289 @@
+/*
+ * tangram.h — C-ABI of the B200-native Tangram model-loading hot path.
+ *
+ * Drop-in boundary for the reference's C++ pool / loader API
+ * (/root/reference/proj/include/warmsim).  Every entry point names the
+ * reference member it replaces; argument meaning, ordering rules and error
+ * behaviour are the reference's.  Plain pointers and sizes only; the library
+ * is libtangram.so (paper_2512_01357_b200/libtangram.so), no torch types.
+ *
+ * Return codes: 0 = ok; 1..10 = warmsim::Error ordinal + 1
+ * (types.hpp:155-166: InsufficientMemory=1, PoolExhausted=2, Infeasible=3,
+ * Pinned=4, NotFound=5, OverlapMove=6, DestinationOccupied=7,
+ * OrderingError=8, InstanceTooLarge=9, InvalidArgument=10); >= 100 are
+ * runtime errors of this implementation (TG_ERR_*).  A failed tg_load_model
+ * leaves the pool unchanged (reuse_store.hpp:117-119); a failed batch KV
+ * allocation leaves engine and pool unchanged (kv_engine.hpp:104-106).
+ * Thread-safety: single writer per pool, like the reference
+ * (reuse_store.hpp:4-6).
+ */
+#ifndef TANGRAM_H
+#define TANGRAM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TG_OK 0
+#define TG_ERR_CUDA 100
+#define TG_ERR_NO_DEVICE 101      /* data-plane call on a control-plane-only pool / no GPU */
+#define TG_ERR_NO_SOURCE 102      /* a miss has no registered host (or peer) source */
+#define TG_ERR_BUFFER 103         /* caller buffer too small; *needed says how big */
+#define TG_ERR_BAD_ARG 104        /* null handle / malformed argument */
+#define TG_ERR_VERIFY 105         /* reused bytes fail their fingerprint and cannot be repaired */
+#define TG_ERR_INTERNAL 106
+
+#define TG_POOL_NO_DEVICE (-1)    /* device argument: control plane only, moves no bytes */
+
+/* tg_load_policy.flags */
+#define TG_LOAD_VERIFY_REUSE 1u    /* fingerprint reused tensors, compare to the recorded digest */
+#define TG_LOAD_FINGERPRINT_NEW 2u /* fingerprint placed tensors, record the digest */
+#define TG_LOAD_PEER 4u            /* pull misses resident on a peer pool over NVLink */
+#define TG_LOAD_DEFAULT 3u
+
+typedef struct tg_pool tg_pool;
+typedef struct tg_stats tg_stats;
+typedef struct tg_kv tg_kv;
+typedef struct tg_rng tg_rng;
+typedef struct tg_model tg_model;
+typedef struct tg_snapshot tg_snapshot;
+
+typedef struct { uint64_t hi, lo; } tg_tensor_id; /* warmsim::TensorId (types.hpp:46-60) */
+typedef struct { uint64_t hi, lo; } tg_digest;    /* tgfp1 content fingerprint */
+
+/* warmsim::GpuSpec (model.hpp:39-45) */
+typedef struct {
+    const char* gpu_id;
+    uint64_t pool_size;
+    double pcie_bandwidth;
+    double intra_copy_bandwidth;
+    double store_bandwidth;
+} tg_gpu_spec;
+
+/* warmsim::TensorSpec (model.hpp:17-22); model_id defaults to the model's */
+typedef struct {
+    tg_tensor_id id;
+    const char* name;
+    uint64_t size;
+    const char* model_id; /* nullable */
+} tg_tensor_spec;
+
+/* warmsim::ModelSpec (model.hpp:30-37); tensors ordered by name */
+typedef struct {
+    const char* model_id;
+    const tg_tensor_spec* tensors;
+    uint32_t n_tensors;
+    uint64_t total_size;
+    double latency_sensitivity;
+    int32_t location; /* 0 model_cache, 1 model_store */
+    uint64_t bytes_per_token;
+} tg_model_spec;
+
+/* warmsim::LoadPolicy (reuse_store.hpp:43-48) + data-plane flags */
+typedef struct {
+    int32_t merge;          /* 0 PartitionedGain, 1 GlobalMerge (packing.hpp:125) */
+    int32_t strictness;     /* 0 Functional, 1 LiteralGuard (packing.hpp:92) */
+    int32_t random_eviction;
+    tg_rng* rng;            /* required for random eviction */
+    uint32_t flags;         /* TG_LOAD_* ; 0 means TG_LOAD_DEFAULT */
+} tg_load_policy;
+
+/* warmsim::LoadOutcome (reuse_store.hpp:34-41) summary + measured data plane */
+typedef struct {
+    uint32_t n_hits, n_misses, n_evictions, n_relocations, n_placements, n_waves;
+    uint64_t fallback_evictions;
+    uint64_t bytes_transferred, bytes_merged;
+    double eviction_cost_total;
+    uint64_t total_merge_cost, pgp_merge_cost, initial_merge_cost;
+    double total_eviction_cost;
+    /* data plane (device pools) */
+    uint64_t pcie_bytes, peer_bytes, fingerprint_bytes, repaired_bytes;
+    uint32_t verify_mismatches, expected_mismatches;
+    double plan_us, total_ms, relocate_ms, h2d_ms, peer_ms, fp_kernel_ms, fp_reuse_ms;
+} tg_load_outcome;
+
+/* warmsim::EvictionCandidate (packing.hpp:32-38); model_id valid until the next call on the pool */
+typedef struct {
+    tg_tensor_id tensor;
+    uint64_t size;
+    double cost;
+    double last_access;
+    const char* model_id;
+} tg_eviction;
+
+/* warmsim::Relocation (packing.hpp:216-221) + its WAR wave */
+typedef struct {
+    tg_tensor_id tensor;
+    uint64_t from, to, size;
+    uint32_t wave;
+} tg_relocation;
+
+/* warmsim::Placement (packing.hpp:223-226) + byte source */
+typedef struct {
+    tg_tensor_id tensor;
+    uint64_t offset, size;
+    uint32_t source; /* 0 host/PCIe, 1 peer/NVLink */
+} tg_placement;
+
+/* warmsim::Region (region_pool.hpp:22-28) */
+typedef struct {
+    uint64_t offset, size;
+    int32_t kind; /* 0 free, 1 tensor, 2 kv_block */
+    tg_tensor_id tensor;
+    uint64_t block_id;
+} tg_region;
+
+/* ReuseStore accessors (reuse_store.hpp:56-74) */
+typedef struct {
+    uint64_t pool_size, free_bytes, kv_bytes, pinned_tensor_bytes, pinned_bytes, reusable_bytes;
+    uint64_t bytes_merged_total, bytes_transferred_total, evictions_total;
+    uint64_t region_count, extent_count, tensor_count, largest_free;
+    int32_t device;
+    void* arena;
+} tg_pool_info;
+
+typedef struct {
+    uint64_t offset, size;
+    double last_access;
+    int32_t pinned, has_digest;
+    tg_digest digest;
+    void* device_ptr;
+} tg_tensor_info;
+
+/* warmsim::KvAllocStats (kv_engine.hpp:33-39) + engine state */
+typedef struct {
+    uint64_t pool_invocations, alloc_batches, blocks_from_free_list, blocks_from_pool, reclaim_events;
+    uint64_t free_list_size, active_requests, next_pbn, block_bytes;
+} tg_kv_stats;
+
+/* ---- library ------------------------------------------------------------- */
+int tg_version(void);
+const char* tg_error_string(int code);
+const char* tg_last_error_detail(void); /* thread-local detail of the last failure */
+int tg_device_count(int* n);
+
+/* ---- ids, catalog (types.hpp:131-146, catalog.hpp:37-90) ------------------- */
+int tg_murmur3_x64_128(const void* data, uint64_t len, uint64_t seed, tg_digest* out);
+int tg_tensor_key(const char* model_id, const char* name, const int64_t* shape, int32_t ndim, int32_t dtype,
+                  tg_tensor_id* out);
+int tg_model_make(const char* model_id, uint64_t total_size, int32_t layers, uint64_t bytes_per_token,
+                  int32_t location, double latency_sensitivity, tg_model** out);
+int tg_model_default_catalog(uint32_t index, tg_model** out); /* index < tg_model_catalog_size() */
+uint32_t tg_model_catalog_size(void);
+void tg_model_destroy(tg_model* m);
+int tg_model_view(const tg_model* m, tg_model_spec* out); /* pointers valid while m lives */
+int tg_model_shard(const tg_model* m, uint32_t rank, uint32_t world, tg_model** out); /* §8(e) tensor shards */
+
+/* ---- request shares (ModelStatsTable, model.hpp:70-133) -------------------- */
+int tg_stats_create(double decay, tg_stats** out);
+void tg_stats_destroy(tg_stats* s);
+int tg_stats_record_request(tg_stats* s, const char* model_id, double t);
+int tg_stats_record_eviction(tg_stats* s, const char* model_id, double t);
+int tg_stats_set_load_bandwidth(tg_stats* s, const char* model_id, double bw);
+double tg_stats_miss_probability(const tg_stats* s, const char* model_id);
+
+int tg_rng_create(uint64_t seed, tg_rng** out); /* warmsim::Rng (rng.hpp:18-73) */
+void tg_rng_destroy(tg_rng* r);
+uint64_t tg_rng_uniform_below(tg_rng* r, uint64_t n);
+
+/* ---- pool (ReuseStore, reuse_store.hpp:50-345) ------------------------------ */
+int tg_pool_create(const tg_gpu_spec* gpu, int32_t device, tg_pool** out); /* ReuseStore(GpuSpec) :54 */
+void tg_pool_destroy(tg_pool* p);
+int tg_pool_info_get(const tg_pool* p, tg_pool_info* out);
+int tg_pool_stream(const tg_pool* p, void** cuda_stream); /* stream every pool operation is ordered on */
+int tg_set_model_alpha(tg_pool* p, const char* model_id, double alpha); /* :76 */
+
+/* load_model (:120-174).  On success the plan arrays of this load can be read
+ * with tg_last_* until the next mutating call on the pool. */
+int tg_load_model(tg_pool* p, const tg_model_spec* m, const tg_stats* s, double clock, const tg_load_policy* pol,
+                  tg_load_outcome* out);
+uint32_t tg_last_hits(const tg_pool* p, tg_tensor_id* buf, uint32_t cap);
+uint32_t tg_last_misses(const tg_pool* p, tg_tensor_id* buf, uint32_t cap);
+uint32_t tg_last_evictions(const tg_pool* p, tg_eviction* buf, uint32_t cap);
+uint32_t tg_last_relocations(const tg_pool* p, tg_relocation* buf, uint32_t cap);
+uint32_t tg_last_placements(const tg_pool* p, tg_placement* buf, uint32_t cap);
+uint32_t tg_last_digests(const tg_pool* p, tg_digest* buf, uint32_t cap); /* model order */
+
+int tg_end_instance(tg_pool* p, const char* model_id);                     /* :177 */
+int tg_evict_tensor(tg_pool* p, tg_tensor_id id);                          /* :186 */
+int tg_evict_model(tg_pool* p, const char* model_id);                      /* :197 */
+int tg_move_tensor(tg_pool* p, tg_tensor_id id, uint64_t new_offset);      /* :212 (+ K3 bytes) */
+int tg_alloc_kv_region(tg_pool* p, uint64_t size, uint64_t block_id, uint64_t* offset); /* :224 */
+int tg_free_kv_region(tg_pool* p, uint64_t offset);                        /* :230 */
+int tg_lookup(const tg_pool* p, const tg_model_spec* m, uint8_t* hit_mask, uint64_t* reuse_size); /* :81 */
+int tg_reuse_size(const tg_pool* p, const tg_model_spec* m, uint64_t* out); /* :92 */
+int tg_peer_reuse_size(const tg_pool* p, const tg_model_spec* m, uint64_t* out); /* §8(e) extension */
+int tg_eviction_candidates(tg_pool* p, const tg_stats* s, const char* exclude, tg_eviction* buf, uint32_t cap,
+                           uint32_t* n); /* :99 */
+int tg_validate(const tg_pool* p);                                         /* :238 */
+int tg_dump(const tg_pool* p, char* buf, uint64_t cap, uint64_t* needed);  /* :270 (JSON) */
+int tg_regions(const tg_pool* p, tg_region* buf, uint64_t cap, uint64_t* n); /* RegionList::snapshot */
+int tg_tensor_info_get(const tg_pool* p, tg_tensor_id id, tg_tensor_info* out);
+int tg_fingerprint_tensor(tg_pool* p, tg_tensor_id id, tg_digest* out);    /* K1 over resident bytes */
+int tg_pool_add_peer(tg_pool* p, tg_pool* peer);                           /* NVLink peer pool (K5) */
+int tg_pool_snapshot(tg_pool* p, tg_snapshot** out);
+int tg_pool_restore(tg_pool* p, const tg_snapshot* s);
+void tg_snapshot_destroy(tg_snapshot* s);
+
+/* ---- host checkpoint sources (data side-channel) -------------- */
+int tg_host_register(tg_tensor_id id, const void* ptr, uint64_t size, const tg_digest* expected /*nullable*/);
+int tg_host_unregister(tg_tensor_id id);
+int tg_host_clear(void);
+int tg_host_alloc(uint64_t size, void** out); /* pinned */
+int tg_host_free(void* p);
+
+/* ---- raw device helpers ------------------------------------------------------ */
+int tg_fingerprint_device(const void* dptr, uint64_t n, int32_t device, tg_digest* out); /* K1 */
+int tg_synth_fill_device(tg_tensor_id id, uint64_t begin, uint64_t len, void* dptr, int32_t device);
+int tg_synth_fill_host(tg_tensor_id id, uint64_t begin, uint64_t len, void* dst, int32_t threads);
+int tg_device_alloc(int32_t device, uint64_t size, void** out);
+int tg_device_free(int32_t device, void* p);
+int tg_memcpy(void* dst, const void* src, uint64_t n); /* cudaMemcpy default kind, synchronous */
+
+/* ---- KV engine (KvEngine, kv_engine.hpp:43-239) ------------------------------- */
+int tg_kv_create(const char* model_id, uint64_t block_size_tokens, uint64_t bytes_per_token, tg_kv** out); /* :47 */
+void tg_kv_destroy(tg_kv* kv);
+int tg_kv_clone(const tg_kv* kv, tg_kv** out);
+/* ensure_capacity (:75-102): granted PBNs into buf (nullable) */
+int tg_kv_ensure_capacity(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t request_id, uint64_t tokens,
+                          uint64_t* granted, uint64_t cap, uint64_t* n_granted);
+/* batch_allocate (:107-161): counts[i] = blocks granted to request i;
+ * pbns (nullable, cap entries) receives all granted PBNs in order. */
+int tg_kv_batch_allocate(tg_kv* kv, tg_pool* p, const tg_stats* s, const uint64_t* request_ids,
+                         const uint64_t* tokens, uint64_t n, uint64_t* counts, uint64_t* pbns, uint64_t cap,
+                         uint64_t* total);
+int tg_kv_release_request(tg_kv* kv, uint64_t request_id);              /* :165 */
+int tg_kv_teardown(tg_kv* kv, tg_pool* p);                              /* :174 */
+int tg_kv_urgent_reclaim(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t blocks); /* :183 */
+int tg_kv_table(const tg_kv* kv, uint64_t request_id, uint64_t* pbns, uint64_t cap, uint64_t* n,
+                uint64_t* token_count);                                 /* table() :55 (reads HBM) */
+int tg_kv_address_table(const tg_kv* kv, uint64_t* triples /*pbn,off,size*/, uint64_t cap, uint64_t* n); /* :63 */
+int tg_kv_stats_get(const tg_kv* kv, tg_kv_stats* out);
+int tg_kv_device_tables(const tg_kv* kv, void** tables, uint64_t* stride, void** addr); /* for paged attention */
+
+/* ---- scheduler (scheduler.hpp:41-120) ------------------------------------------ */
+typedef struct {
+    const char* gpu_id;
+    int32_t available;
+    uint64_t pool_size;
+    uint64_t free_bytes;
+    double pcie_bandwidth;
+    double store_bandwidth;
+    double nvlink_bandwidth; /* peer term; 0 disables it (reference behaviour) */
+} tg_gpu_snapshot;
+/* reuse[g * n_models + m] = S' of model m on GPU g; peer_reuse likewise (nullable).
+ * request_models[i] indexes models; assignment[i] = chosen GPU index or -1;
+ * estimates[i * n_gpus + g] = estimate or -1 when infeasible (nullable). */
+int tg_schedule(const uint32_t* request_models, uint32_t n_requests, const tg_gpu_snapshot* gpus, uint32_t n_gpus,
+                const tg_model_spec* models, uint32_t n_models, const uint64_t* reuse, const uint64_t* peer_reuse,
+                uint32_t batch_size, uint64_t block_size_tokens, int32_t* assignment, double* estimates);
+double tg_estimate_load_time(const tg_model_spec* m, uint64_t reuse_size, const tg_gpu_snapshot* g,
+                             uint64_t peer_reuse_size);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TANGRAM_H */

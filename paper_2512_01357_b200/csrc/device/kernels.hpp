@@ -1,0 +1,75 @@
+// Launch interfaces of the sm_100a kernels (plain C++ so host code can call
+// them without CUDA headers beyond cuda_runtime.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tg {
+
+// ---- K1: content fingerprint (tgfp1) -------------------------------------
+// Leaf = 4096 B, leaf_i digest = murmur3_x64_128(leaf bytes, seed = i);
+// tensor digest = murmur3(le64 ΣH ‖ le64 ΣL ‖ le64 n, seed 0).
+constexpr std::uint64_t kLeafBytes = 4096;
+constexpr std::uint32_t kLeavesPerTile = 32;
+
+struct FpTask {
+    const std::uint8_t* base;  // device pointer (any alignment)
+    std::uint64_t n;           // bytes
+    std::uint64_t tile0;       // first tile index of this task (prefix over tasks)
+};
+
+// sums: 2 u64 per task (must be zeroed), digests: 2 u64 per task.
+void fp_launch(const FpTask* d_tasks, std::uint32_t n_tasks, std::uint64_t total_tiles, std::uint64_t* d_sums,
+               std::uint64_t* d_digests, int sm_count, cudaStream_t s);
+
+// ---- K3: relocation wave (batched misaligned memcpy) ---------------------
+constexpr int kMaxMovesPerLaunch = 96;
+struct MoveDesc {
+    std::uint64_t src;  // device address
+    std::uint64_t dst;  // device address
+    std::uint64_t len;  // bytes
+};
+// All moves of one launch must be pairwise hazard-free (one WAR wave).
+void relocate_launch(const MoveDesc* moves, int n_moves, int sm_count, cudaStream_t s);
+
+// ---- K4: KV batch expansion ------------------------------------------------
+struct KvGrantDev {
+    std::uint64_t start;  // first global block index of this grant
+    std::uint64_t lbn0;
+    std::uint32_t slot;
+    std::uint32_t pad;
+};
+struct KvRunDev {
+    std::uint64_t start;  // first carved-block index (relative to pops) of this run
+    std::uint64_t off;
+    std::uint64_t first_pbn;
+};
+struct KvBatchArgs {
+    const KvGrantDev* grants;
+    std::uint32_t n_grants;
+    const KvRunDev* runs;
+    std::uint32_t n_runs;
+    std::uint64_t total;
+    std::uint64_t pops;
+    std::uint64_t free_before;
+    std::uint64_t block_bytes;
+    std::uint64_t* tables;  // [slots][stride]
+    std::uint64_t stride;
+    std::uint64_t* free_list;
+    std::uint64_t* addr;  // pbn -> offset
+    std::uint64_t* out;   // optional: granted pbns in order
+};
+void kv_batch_launch(const KvBatchArgs& a, cudaStream_t s);
+void kv_release_launch(const std::uint64_t* table_row, std::uint64_t blocks, std::uint64_t* free_list_dst,
+                       cudaStream_t s);
+
+// ---- synthetic checkpoint bytes -------------------------------
+void synth_launch(std::uint64_t hi, std::uint64_t lo, std::uint64_t begin, std::uint64_t len, std::uint8_t* dst,
+                  cudaStream_t s);
+
+// ---- K5: peer pull (SM copy over NVLink peer mappings) -----------------------
+// Reuses the relocation kernel: the source address is a peer arena pointer.
+
+}  // namespace tg

@@ -1,0 +1,469 @@
+#include "pool.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "../device/common.cuh"
+#include "../device/kernels.hpp"
+
+namespace tg {
+
+// ---- host source registry ----------------------------------------------------
+SourceRegistry& SourceRegistry::get() {
+    static SourceRegistry r;
+    return r;
+}
+void SourceRegistry::put(const Key& k, const HostSource& s) {
+    std::lock_guard<std::mutex> g(mu_);
+    map_[k] = s;
+}
+bool SourceRegistry::find(const Key& k, HostSource* out) const {
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = map_.find(k);
+    if (it == map_.end()) return false;
+    *out = it->second;
+    return true;
+}
+void SourceRegistry::erase(const Key& k) {
+    std::lock_guard<std::mutex> g(mu_);
+    map_.erase(k);
+}
+void SourceRegistry::clear() {
+    std::lock_guard<std::mutex> g(mu_);
+    map_.clear();
+}
+
+// ---- pool --------------------------------------------------------------------
+Pool::Pool(GpuDesc gpu, int device) : store_(std::move(gpu)), device_(device) {
+    if (device_ < 0) return;
+    DeviceScope ds(device_);
+    TG_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device_));
+    // +256 B slack: aligned 16-byte word reads at a tensor's last byte may
+    // touch the following word.
+    TG_CUDA(cudaMalloc(reinterpret_cast<void**>(&arena_), store_.pool_size() + 256));
+    for (cudaStream_t* s : {&s_main_, &s_copy_, &s_fp_, &s_peer_})
+        TG_CUDA(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+}
+
+Pool::~Pool() {
+    if (device_ < 0) return;
+    DeviceScope ds(device_);
+    cudaDeviceSynchronize();
+    for (cudaEvent_t e : events_) cudaEventDestroy(e);
+    for (cudaStream_t s : {s_main_, s_copy_, s_fp_, s_peer_})
+        if (s) cudaStreamDestroy(s);
+    if (arena_) cudaFree(arena_);
+    if (d_stage_) cudaFree(d_stage_);
+    if (h_stage_) cudaFreeHost(h_stage_);
+}
+
+void Pool::ensure_events(std::size_t n) {
+    while (events_.size() < n) {
+        cudaEvent_t e;
+        TG_CUDA(cudaEventCreate(&e));
+        events_.push_back(e);
+    }
+}
+
+void Pool::ensure_stage(std::size_t bytes) {
+    if (bytes <= stage_cap_) return;
+    std::size_t n = stage_cap_ ? stage_cap_ : 1 << 16;
+    while (n < bytes) n *= 2;
+    if (h_stage_) {
+        TG_CUDA(cudaStreamSynchronize(s_main_));
+        cudaFreeHost(h_stage_);
+        cudaFree(d_stage_);
+    }
+    TG_CUDA(cudaMallocHost(&h_stage_, n));
+    TG_CUDA(cudaMalloc(&d_stage_, n));
+    stage_cap_ = n;
+}
+
+namespace {
+
+bool overlaps(u64 a, u64 alen, u64 b, u64 blen) { return a < b + blen && b < a + alen; }
+
+double ms_between(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    TG_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+
+// Tile prefix for a list of (ptr, n) tasks; returns total tiles.
+u64 build_tasks(std::vector<FpTask>& tasks) {
+    u64 tiles = 0;
+    for (auto& t : tasks) {
+        t.tile0 = tiles;
+        const u64 leaves = (t.n + kLeafBytes - 1) / kLeafBytes;
+        tiles += (leaves + kLeavesPerTile - 1) / kLeavesPerTile;
+    }
+    return tiles;
+}
+
+}  // namespace
+
+St Pool::load_model(const ModelDesc& m, const RequestShares& stats, double clock, const LoadOptions& opt, u32 flags,
+                    LoadReport* rep) {
+    using clk = std::chrono::steady_clock;
+    *rep = LoadReport{};
+    std::unique_ptr<DeviceScope> ds;
+    if (has_device()) {
+        ds = std::make_unique<DeviceScope>(device_);
+        ensure_events(8);
+        TG_CUDA(cudaEventRecord(ev(0), s_main_));  // t0: entry
+    }
+    const auto h0 = clk::now();
+    auto dec = store_.decide(m, stats, opt);
+    rep->t.plan_us = std::chrono::duration<double, std::micro>(clk::now() - h0).count();
+    if (!dec) return dec.error();
+    LoadDecision& d = dec.value();
+
+    // Resolve a byte source for every miss before anything changes, so a
+    // missing source leaves the store untouched (like a failed plan).
+    const std::size_t np = d.plan.placements.size();
+    std::vector<HostSource> src(np);
+    std::vector<const std::uint8_t*> peer_src(np, nullptr);
+    rep->placement_src.assign(np, 0);
+    if (has_device()) {
+        for (std::size_t i = 0; i < np; ++i) {
+            const TensorDesc& t = d.miss_desc[d.plan.placements[i].tensor];
+            if (flags & kLoadPeer) {
+                for (Pool* p : peers_) {
+                    const Entry* e = p->store_.entry(t.id);
+                    if (e && e->size == t.size && e->has_digest) {
+                        peer_src[i] = p->arena_ + e->off;
+                        rep->placement_src[i] = 1;
+                        break;
+                    }
+                }
+            }
+            if (peer_src[i]) continue;
+            if (!SourceRegistry::get().find(t.id, &src[i]) || src[i].size != t.size)
+                throw DeviceError(kErrNoSource, "no host source registered for tensor " + t.id.hex() + " (" +
+                                                    t.model_id + "/" + t.name + ")");
+        }
+    }
+
+    // Relocation waves: wave(k) = 1 + max wave(j), j < k, dst_k ∩ src_j ≠ ∅.
+    const auto& rel = d.plan.relocations;
+    rep->reloc_wave.assign(rel.size(), 0);
+    u32 waves = 0;
+    for (std::size_t k = 0; k < rel.size(); ++k) {
+        u32 w = 0;
+        for (std::size_t j = 0; j < k; ++j)
+            if (overlaps(rel[k].to, rel[k].size, rel[j].from, rel[j].size)) w = std::max(w, rep->reloc_wave[j] + 1);
+        rep->reloc_wave[k] = w;
+        waves = std::max(waves, w + 1);
+    }
+    rep->waves = waves;
+    // A placement must wait for the last wave that reads bytes it overwrites.
+    std::vector<int> dep(np, -1);
+    for (std::size_t i = 0; i < np; ++i) {
+        const auto& pl = d.plan.placements[i];
+        const u64 sz = d.miss_desc[pl.tensor].size;
+        for (std::size_t j = 0; j < rel.size(); ++j)
+            if (overlaps(pl.off, sz, rel[j].from, rel[j].size)) dep[i] = std::max(dep[i], static_cast<int>(rep->reloc_wave[j]));
+    }
+
+    std::vector<Key> hit_keys;
+    for (u32 i : d.hits) hit_keys.push_back(m.tensors[i].id);
+    store_.commit(m, d, clock);
+    rep->decision = std::move(d);
+    LoadDecision& D = rep->decision;
+    if (!has_device()) return ok();
+
+    for (std::size_t i = 0; i < np; ++i) (rep->placement_src[i] ? rep->peer_bytes : rep->pcie_bytes) += D.miss_desc[D.plan.placements[i].tensor].size;
+
+    // ---- event layout -----------------------------------------------------------
+    // 0 t0 | 1 reloc start | 2 reloc end | 3 end | 4 h2d start | 5 h2d end | 6 peer start | 7 peer end
+    // 8.. wave ends (waves) | then per placement "bytes landed" | then fp start/end pairs
+    const std::size_t ev_wave = 8, ev_land = ev_wave + waves, ev_fp = ev_land + np;
+    const bool fp_new = flags & kLoadFingerprintNew, fp_reuse = (flags & kLoadVerifyReuse) && !hit_keys.empty();
+    const std::size_t n_fp_launch = (fp_new ? np : 0) + (fp_reuse ? 1 : 0);
+    ensure_events(ev_fp + 2 * n_fp_launch);
+
+    // ---- fingerprint task table (one H2D of descriptors) -------------------------
+    // tasks: [placements (one launch each)] [hits (one launch)]
+    std::vector<FpTask> tasks;
+    for (std::size_t i = 0; i < np && fp_new; ++i) {
+        const auto& pl = D.plan.placements[i];
+        tasks.push_back(FpTask{arena_ + pl.off, D.miss_desc[pl.tensor].size, 0});
+    }
+    std::vector<FpTask> hit_tasks;
+    if (fp_reuse)
+        for (const Key& k : hit_keys) {
+            const Entry* e = store_.entry(k);
+            hit_tasks.push_back(FpTask{arena_ + e->off, e->size, 0});
+        }
+    const u64 hit_tiles = build_tasks(hit_tasks);
+    std::vector<u64> new_tiles(tasks.size());
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+        std::vector<FpTask> one{tasks[i]};
+        new_tiles[i] = build_tasks(one);
+    }
+    const std::size_t n_tasks = tasks.size() + hit_tasks.size();
+    const std::size_t desc_bytes = n_tasks * sizeof(FpTask), sums_bytes = n_tasks * 2 * sizeof(u64);
+    ensure_stage(desc_bytes + 2 * sums_bytes + 64);
+    auto* h = static_cast<std::uint8_t*>(h_stage_);
+    auto* dptr = static_cast<std::uint8_t*>(d_stage_);
+    std::memcpy(h, tasks.data(), tasks.size() * sizeof(FpTask));
+    std::memcpy(h + tasks.size() * sizeof(FpTask), hit_tasks.data(), hit_tasks.size() * sizeof(FpTask));
+    const auto* d_tasks = reinterpret_cast<const FpTask*>(dptr);
+    auto* d_sums = reinterpret_cast<u64*>(dptr + desc_bytes);
+    auto* d_dig = reinterpret_cast<u64*>(dptr + desc_bytes + sums_bytes);
+    if (n_tasks) {
+        TG_CUDA(cudaMemcpyAsync(dptr, h, desc_bytes, cudaMemcpyHostToDevice, s_main_));
+        TG_CUDA(cudaMemsetAsync(d_sums, 0, sums_bytes, s_main_));
+    }
+
+    // ---- relocation waves on the main stream (K3) ---------------------------------
+    TG_CUDA(cudaEventRecord(ev(1), s_main_));
+    for (u32 w = 0; w < waves; ++w) {
+        std::vector<MoveDesc> mv;
+        for (std::size_t j = 0; j < rel.size(); ++j)
+            if (rep->reloc_wave[j] == w)
+                mv.push_back(MoveDesc{reinterpret_cast<u64>(arena_ + rel[j].from), reinterpret_cast<u64>(arena_ + rel[j].to),
+                                      rel[j].size});
+        relocate_launch(mv.data(), static_cast<int>(mv.size()), sm_count_, s_main_);
+        TG_CUDA(cudaGetLastError());
+        TG_CUDA(cudaEventRecord(ev(ev_wave + w), s_main_));
+    }
+    TG_CUDA(cudaEventRecord(ev(2), s_main_));
+
+    // ---- placements: host→device on the copy stream, peer pulls on the peer stream
+    // Independent placements first, then those gated on a relocation wave.
+    std::vector<std::size_t> order(np);
+    for (std::size_t i = 0; i < np; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) { return dep[a] < dep[b]; });
+    TG_CUDA(cudaStreamWaitEvent(s_copy_, ev(0)));  // descriptor H2D / memset ordered before
+    TG_CUDA(cudaStreamWaitEvent(s_peer_, ev(0)));
+    TG_CUDA(cudaEventRecord(ev(4), s_copy_));
+    TG_CUDA(cudaEventRecord(ev(6), s_peer_));
+    int waited_copy = -1, waited_peer = -1;
+    for (std::size_t i : order) {
+        const auto& pl = D.plan.placements[i];
+        const u64 sz = D.miss_desc[pl.tensor].size;
+        const bool peer = rep->placement_src[i] != 0;
+        cudaStream_t s = peer ? s_peer_ : s_copy_;
+        int& waited = peer ? waited_peer : waited_copy;
+        if (dep[i] > waited) {
+            TG_CUDA(cudaStreamWaitEvent(s, ev(ev_wave + dep[i])));
+            waited = dep[i];
+        }
+        if (peer) {
+            MoveDesc md{reinterpret_cast<u64>(peer_src[i]), reinterpret_cast<u64>(arena_ + pl.off), sz};
+            relocate_launch(&md, 1, sm_count_, s);
+            TG_CUDA(cudaGetLastError());
+        } else {
+            TG_CUDA(cudaMemcpyAsync(arena_ + pl.off, src[i].ptr, sz, cudaMemcpyHostToDevice, s));
+        }
+        TG_CUDA(cudaEventRecord(ev(ev_land + i), s));
+    }
+    TG_CUDA(cudaEventRecord(ev(5), s_copy_));
+    TG_CUDA(cudaEventRecord(ev(7), s_peer_));
+
+    // ---- K1 over placed tensors, trailing the copies ------------------------------
+    std::size_t fp_i = 0;
+    if (fp_new) {
+        TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(1)));  // descriptors uploaded, sums zeroed
+        for (std::size_t i : order) {
+            TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(ev_land + i)));
+            TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s_fp_));
+            fp_launch(d_tasks + i, 1, new_tiles[i], d_sums + 2 * i, d_dig + 2 * i, sm_count_, s_fp_);
+            TG_CUDA(cudaGetLastError());
+            TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s_fp_));
+            ++fp_i;
+        }
+    }
+    // ---- K1 over reused tensors at their final offsets (after the waves) ------------
+    std::size_t fp_reuse_slot = 0;
+    if (fp_reuse) {
+        fp_reuse_slot = fp_i;
+        const std::size_t base = tasks.size();
+        TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s_main_));
+        fp_launch(d_tasks + base, static_cast<u32>(hit_tasks.size()), hit_tiles, d_sums + 2 * base, d_dig + 2 * base,
+                  sm_count_, s_main_);
+        TG_CUDA(cudaGetLastError());
+        TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s_main_));
+        ++fp_i;
+    }
+    // ---- join, read digests, end ------------------------------------------------
+    TG_CUDA(cudaStreamWaitEvent(s_main_, ev(5)));
+    TG_CUDA(cudaStreamWaitEvent(s_main_, ev(7)));
+    if (fp_new && !tasks.empty()) {
+        TG_CUDA(cudaEventRecord(ev(3), s_fp_));
+        TG_CUDA(cudaStreamWaitEvent(s_main_, ev(3)));
+    }
+    TG_CUDA(cudaEventRecord(ev(3), s_main_));
+    auto* h_dig = reinterpret_cast<u64*>(h + desc_bytes + sums_bytes);
+    if (n_tasks) TG_CUDA(cudaMemcpyAsync(h_dig, d_dig, sums_bytes, cudaMemcpyDeviceToHost, s_main_));
+    TG_CUDA(cudaStreamSynchronize(s_main_));
+
+    rep->t.total_ms = ms_between(ev(0), ev(3));
+    rep->t.relocate_ms = waves ? ms_between(ev(1), ev(2)) : 0.0;
+    rep->t.h2d_ms = rep->pcie_bytes ? ms_between(ev(4), ev(5)) : 0.0;
+    rep->t.peer_ms = rep->peer_bytes ? ms_between(ev(6), ev(7)) : 0.0;
+    for (std::size_t f = 0; f < fp_i; ++f) {
+        const double t = ms_between(ev(ev_fp + 2 * f), ev(ev_fp + 2 * f + 1));
+        rep->t.fp_kernel_ms += t;
+        if (fp_reuse && f == fp_reuse_slot) rep->t.fp_reuse_ms = t;
+    }
+
+    // ---- record / verify digests ----------------------------------------------
+    rep->digests.assign(m.tensors.size(), Digest{});
+    std::unordered_map<Key, std::size_t, KeyHash> pos;
+    for (std::size_t i = 0; i < m.tensors.size(); ++i) pos.emplace(m.tensors[i].id, i);
+    for (std::size_t i = 0; i < tasks.size(); ++i) {
+        const TensorDesc& t = D.miss_desc[D.plan.placements[i].tensor];
+        const Digest g{h_dig[2 * i], h_dig[2 * i + 1]};
+        Entry* e = store_.entry(t.id);
+        e->digest = g;
+        e->has_digest = true;
+        rep->digests[pos[t.id]] = g;
+        rep->fingerprint_bytes += t.size;
+        if (!rep->placement_src[i] && src[i].has_expected && !(src[i].expected == g)) ++rep->expected_mismatches;
+    }
+    for (std::size_t i = 0; i < hit_tasks.size(); ++i) {
+        const Key& k = hit_keys[i];
+        const Digest g{h_dig[2 * (tasks.size() + i)], h_dig[2 * (tasks.size() + i) + 1]};
+        Entry* e = store_.entry(k);
+        rep->digests[pos[k]] = g;
+        rep->fingerprint_bytes += e->size;
+        if (e->has_digest && !(e->digest == g)) {
+            // Content drifted: the key says "reuse", the bytes disagree.  Re-send
+            // the tensor in place from its host source (same plan, fresh bytes).
+            ++rep->verify_mismatches;
+            HostSource hs;
+            if (!SourceRegistry::get().find(k, &hs) || hs.size != e->size)
+                throw DeviceError(kErrVerify, "reused tensor " + k.hex() + " fails verification and has no host source");
+            TG_CUDA(cudaMemcpyAsync(arena_ + e->off, hs.ptr, e->size, cudaMemcpyHostToDevice, s_main_));
+            TG_CUDA(cudaStreamSynchronize(s_main_));
+            rep->repaired_bytes += e->size;
+            e->digest = fingerprint_resident(k);
+        } else if (!e->has_digest) {
+            e->digest = g;
+            e->has_digest = true;
+        }
+    }
+    return ok();
+}
+
+St Pool::move_tensor(const Key& k, u64 to) {
+    const Entry* e = store_.entry(k);
+    const u64 from = e ? e->off : 0, size = e ? e->size : 0;
+    St st = store_.move_tensor(k, to);
+    if (!st || !has_device()) return st;
+    DeviceScope ds(device_);
+    MoveDesc md{reinterpret_cast<u64>(arena_ + from), reinterpret_cast<u64>(arena_ + to), size};
+    relocate_launch(&md, 1, sm_count_, s_main_);
+    TG_CUDA(cudaGetLastError());
+    TG_CUDA(cudaStreamSynchronize(s_main_));
+    return st;
+}
+
+Digest Pool::fingerprint_resident(const Key& k) {
+    const Entry* e = store_.entry(k);
+    if (!e) throw DeviceError(kErrNoSource, "tensor not resident");
+    if (!has_device()) throw DeviceError(kErrNoDevice, "pool has no device");
+    Digest d;
+    fingerprint_device(arena_ + e->off, e->size, device_, &d);
+    return d;
+}
+
+void Pool::add_peer(Pool* p) {
+    if (!has_device() || !p->has_device()) throw DeviceError(kErrNoDevice, "peer pools need devices");
+    if (p->device_ != device_) {
+        DeviceScope ds(device_);
+        int can = 0;
+        TG_CUDA(cudaDeviceCanAccessPeer(&can, device_, p->device_));
+        if (!can) throw DeviceError(kErrCuda, "no P2P path between devices");
+        cudaError_t e = cudaDeviceEnablePeerAccess(p->device_, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_check(e, "cudaDeviceEnablePeerAccess");
+        cudaGetLastError();
+    }
+    peers_.push_back(p);
+}
+
+u64 Pool::peer_reuse_size(const ModelDesc& m) const {
+    u64 s = 0;
+    for (const auto& t : m.tensors) {
+        if (store_.tensors().count(t.id)) continue;
+        for (Pool* p : peers_)
+            if (const auto it = p->store_.tensors().find(t.id); it != p->store_.tensors().end() && it->second.has_digest) {
+                s += t.size;
+                break;
+            }
+    }
+    return s;
+}
+
+struct Pool::Snapshot {
+    Store store;
+    std::uint8_t* bytes = nullptr;
+    u64 n = 0;
+};
+
+Pool::Snapshot* Pool::snapshot() {
+    auto* s = new Snapshot{store_, nullptr, 0};
+    if (has_device()) {
+        DeviceScope ds(device_);
+        s->n = store_.pool_size();
+        TG_CUDA(cudaMalloc(reinterpret_cast<void**>(&s->bytes), s->n));
+        TG_CUDA(cudaMemcpyAsync(s->bytes, arena_, s->n, cudaMemcpyDeviceToDevice, s_main_));
+        TG_CUDA(cudaStreamSynchronize(s_main_));
+    }
+    return s;
+}
+
+void Pool::restore(const Snapshot* s) {
+    store_ = s->store;
+    if (has_device() && s->bytes) {
+        DeviceScope ds(device_);
+        TG_CUDA(cudaMemcpyAsync(arena_, s->bytes, s->n, cudaMemcpyDeviceToDevice, s_main_));
+        TG_CUDA(cudaStreamSynchronize(s_main_));
+    }
+}
+
+void Pool::drop(Snapshot* s) {
+    if (!s) return;
+    if (s->bytes) cudaFree(s->bytes);
+    delete s;
+}
+
+std::unique_ptr<KvDevice> Pool::make_kv_device() {
+    if (!has_device()) return nullptr;
+    return tg::make_kv_device(device_, s_main_);
+}
+
+void fingerprint_device(const void* ptr, u64 n, int device, Digest* out) {
+    DeviceScope ds(device);
+    int sms = 148;
+    TG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    std::vector<FpTask> t{FpTask{static_cast<const std::uint8_t*>(ptr), n, 0}};
+    const u64 tiles = build_tasks(t);
+    cudaStream_t s;
+    TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    void* d = nullptr;
+    TG_CUDA(cudaMallocAsync(&d, sizeof(FpTask) + 4 * sizeof(u64), s));
+    TG_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(FpTask), cudaMemcpyHostToDevice, s));
+    auto* sums = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(d) + sizeof(FpTask));
+    TG_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(u64), s));
+    fp_launch(static_cast<const FpTask*>(d), 1, tiles, sums, sums + 2, sms, s);
+    TG_CUDA(cudaGetLastError());
+    u64 h[2];
+    TG_CUDA(cudaMemcpyAsync(h, sums + 2, sizeof h, cudaMemcpyDeviceToHost, s));
+    TG_CUDA(cudaFreeAsync(d, s));
+    TG_CUDA(cudaStreamSynchronize(s));
+    TG_CUDA(cudaStreamDestroy(s));
+    *out = Digest{h[0], h[1]};
+}
+
+void synth_fill_device(const Key& k, u64 begin, u64 len, void* dst, int device) {
+    DeviceScope ds(device);
+    synth_launch(k.hi, k.lo, begin, len, static_cast<std::uint8_t*>(dst), nullptr);
+    TG_CUDA(cudaGetLastError());
+    TG_CUDA(cudaStreamSynchronize(nullptr));
+}
+
+}  // namespace tg

@@ -1,0 +1,132 @@
+// One GPU's Tangram pool: the control plane (Store) bound to its B200 data
+// plane — a device-resident arena of pool_size bytes, a copy stream for
+// host→device placement, a compute stream for relocation waves and reuse
+// verification, and a fingerprint stream that trails the copies tensor by
+// tensor.  load_model() keeps ReuseStore::load_model's decisions
+// (reuse_store.hpp:120-174) and adds the bytes: relocations as WAR-ordered
+// waves of the K3 kernel, misses as H2D (or NVLink peer pulls through the
+// same kernel), and K1 content fingerprints of every placed and every reused
+// tensor.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kv.hpp"
+#include "store.hpp"
+
+namespace tg {
+
+constexpr int kErrNoDevice = 101;
+constexpr int kErrNoSource = 102;
+constexpr int kErrVerify = 105;
+
+// Host-side checkpoint bytes per tensor key, with an optional expected
+// content fingerprint (e.g. from a checkpoint manifest).
+struct HostSource {
+    const void* ptr = nullptr;
+    u64 size = 0;
+    bool has_expected = false;
+    Digest expected;
+};
+
+class SourceRegistry {
+public:
+    static SourceRegistry& get();
+    void put(const Key& k, const HostSource& s);
+    bool find(const Key& k, HostSource* out) const;
+    void erase(const Key& k);
+    void clear();
+
+private:
+    mutable std::mutex mu_;
+    std::unordered_map<Key, HostSource, KeyHash> map_;
+};
+
+// load flags (tg_load_policy.flags)
+constexpr u32 kLoadVerifyReuse = 1u;     // fingerprint reused tensors, compare to the recorded digest
+constexpr u32 kLoadFingerprintNew = 2u;  // fingerprint placed tensors and record the digest
+constexpr u32 kLoadPeer = 4u;            // pull misses from peer pools that hold them
+constexpr u32 kLoadDefault = kLoadVerifyReuse | kLoadFingerprintNew;
+
+struct LoadTimings {
+    double plan_us = 0;          // host planning (decide)
+    double total_ms = 0;         // device span: entry .. all bytes placed and verified
+    double relocate_ms = 0;      // relocation waves (K3)
+    double h2d_ms = 0;           // first .. last host→device copy
+    double peer_ms = 0;          // peer pulls
+    double fp_kernel_ms = 0;     // Σ K1 launch durations
+    double fp_reuse_ms = 0;      // K1 over reused tensors
+};
+
+struct LoadReport {
+    LoadDecision decision;           // hits / misses / plan (placements index miss_desc)
+    std::vector<u32> reloc_wave;     // WAR wave of each relocation
+    std::vector<std::uint8_t> placement_src;  // 0 = host (PCIe), 1 = peer (NVLink)
+    u32 waves = 0;
+    u64 pcie_bytes = 0, peer_bytes = 0, fingerprint_bytes = 0, repaired_bytes = 0;
+    u32 verify_mismatches = 0, expected_mismatches = 0;
+    std::vector<Digest> digests;     // per model tensor (model order), when fingerprinted
+    LoadTimings t;
+};
+
+class Pool {
+public:
+    // device < 0: control plane only (no arena; moves no bytes).
+    Pool(GpuDesc gpu, int device);
+    ~Pool();
+    Pool(const Pool&) = delete;
+    Pool& operator=(const Pool&) = delete;
+
+    Store& store() { return store_; }
+    const Store& store() const { return store_; }
+    int device() const { return device_; }
+    bool has_device() const { return device_ >= 0; }
+    std::uint8_t* arena() const { return arena_; }
+    cudaStream_t stream() const { return s_main_; }
+    int sm_count() const { return sm_count_; }
+
+    St load_model(const ModelDesc& m, const RequestShares& stats, double clock, const LoadOptions& opt, u32 flags,
+                  LoadReport* rep);
+    St move_tensor(const Key& k, u64 to);  // metadata + bytes
+
+    Digest fingerprint_resident(const Key& k);  // K1 over the resident bytes
+    void add_peer(Pool* p);
+    u64 peer_reuse_size(const ModelDesc& m) const;  // bytes of m's misses resident on a peer
+
+    // Whole-pool checkpoint (metadata + arena bytes) for rollback / benchmarks.
+    struct Snapshot;
+    Snapshot* snapshot();
+    void restore(const Snapshot* s);
+    static void drop(Snapshot* s);
+
+    std::unique_ptr<KvDevice> make_kv_device();
+
+private:
+    void ensure_events(std::size_t n);
+    cudaEvent_t ev(std::size_t i) { return events_[i]; }
+
+    Store store_;
+    int device_ = -1;
+    int sm_count_ = 148;
+    std::uint8_t* arena_ = nullptr;
+    cudaStream_t s_main_ = nullptr, s_copy_ = nullptr, s_fp_ = nullptr, s_peer_ = nullptr;
+    std::vector<cudaEvent_t> events_;
+    std::vector<Pool*> peers_;
+    // staging
+    void* h_stage_ = nullptr;
+    void* d_stage_ = nullptr;
+    std::size_t stage_cap_ = 0;
+    void ensure_stage(std::size_t bytes);
+};
+
+std::unique_ptr<KvDevice> make_kv_device(int device, cudaStream_t stream);
+void fingerprint_device(const void* ptr, u64 n, int device, Digest* out);
+void synth_fill_device(const Key& k, u64 begin, u64 len, void* dst, int device);
+
+}  // namespace tg

@@ -1,0 +1,145 @@
+// Control plane of one GPU's unified pool: the tensor index plus the
+// load / evict / move / KV-region lifecycle.  Decisions are bit-identical to
+// the reference ReuseStore (reuse_store.hpp:50-345); the byte movement each
+// decision implies is executed by the device data plane (pool.cpp), which is
+// why planning and applying are separate steps here.
+#pragma once
+
+#include <map>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "model.hpp"
+#include "planner.hpp"
+#include "regions.hpp"
+
+namespace tg {
+
+// Device-side failure (CUDA error, missing host source, ...).  Thrown by the
+// data plane and converted to an error code at the C-ABI boundary.
+struct DeviceError : std::runtime_error {
+    int code;
+    DeviceError(int c, const std::string& what) : std::runtime_error(what), code(c) {}
+};
+
+// mt19937_64 stream + rejection-sampled uniform_below; the same stream the
+// reference Rng produces (rng.hpp:18-73).
+class Rng {
+public:
+    explicit Rng(u64 seed) : gen_(seed) {}
+    u64 next() { return gen_(); }
+    u64 uniform_below(u64 n) {
+        const u64 limit = UINT64_MAX - UINT64_MAX % n;
+        u64 x;
+        do x = gen_();
+        while (x >= limit);
+        return x % n;
+    }
+
+private:
+    std::mt19937_64 gen_;
+};
+
+struct LoadOptions {
+    MergeMode merge = MergeMode::PartitionedGain;
+    Strictness strictness = Strictness::Functional;
+    bool random_eviction = false;
+    Rng* rng = nullptr;
+};
+
+struct Digest {
+    u64 hi = 0, lo = 0;
+    bool operator==(const Digest& o) const { return hi == o.hi && lo == o.lo; }
+};
+
+struct Entry {
+    u64 off = 0;
+    u64 size = 0;
+    std::string model;
+    double last_access = 0;
+    bool pinned = false;
+    bool has_digest = false;  // content fingerprint recorded by the data plane
+    Digest digest;
+};
+
+struct LoadDecision {
+    std::vector<u32> hits;    // indices into model.tensors, model order
+    std::vector<u32> misses;  // indices into model.tensors, model order
+    std::vector<Key> hit_keys;
+    std::vector<TensorDesc> miss_desc;
+    u64 bytes_transferred = 0;
+    Plan plan;                // placements index into miss_desc
+    PoolMap after;            // layout once the plan is applied
+};
+
+class Store {
+public:
+    Store() = default;
+    explicit Store(GpuDesc gpu) : gpu_(std::move(gpu)), map_(gpu_.pool_size) {}
+
+    const GpuDesc& gpu() const { return gpu_; }
+    u64 pool_size() const { return gpu_.pool_size; }
+    u64 free_bytes() const { return map_.free_total(); }
+    u64 kv_bytes() const { return kv_bytes_; }
+    u64 pinned_tensor_bytes() const { return pinned_tensor_bytes_; }
+    u64 pinned_bytes() const { return pinned_tensor_bytes_ + kv_bytes_; }
+    u64 reusable_bytes() const { return gpu_.pool_size - pinned_bytes(); }
+    u64 merged_total() const { return merged_total_; }
+    u64 transferred_total() const { return transferred_total_; }
+    u64 evictions_total() const { return evictions_total_; }
+    const PoolMap& map() const { return map_; }
+    const std::unordered_map<Key, Entry, KeyHash>& tensors() const { return tensors_; }
+    Entry* entry(const Key& k) {
+        auto it = tensors_.find(k);
+        return it == tensors_.end() ? nullptr : &it->second;
+    }
+    void set_alpha(const std::string& model, double a) { alpha_[model] = a; }
+
+    // lookup / reuse_size (reuse_store.hpp:81-97)
+    void lookup(const ModelDesc& m, std::vector<u32>* hits, std::vector<u32>* misses) const;
+    u64 reuse_size(const ModelDesc& m) const;
+    // eviction_candidates (reuse_store.hpp:99-115)
+    std::vector<Candidate> candidates(const RequestShares& stats, const std::string& exclude) const;
+
+    // load_model, split in two (reuse_store.hpp:120-174).  decide() performs
+    // the alpha update, the capacity check, lookup and planning without
+    // touching the layout; commit() applies the decision and pins.
+    Res<LoadDecision> decide(const ModelDesc& m, const RequestShares& stats, const LoadOptions& opt);
+    void commit(const ModelDesc& m, LoadDecision& d, double clock);
+
+    void end_instance(const std::string& model);
+    St evict_tensor(const Key& k);
+    void evict_model(const std::string& model);
+    St move_tensor(const Key& k, u64 to);
+    Res<u64> alloc_kv_region(u64 size, u64 block_id);
+    St free_kv_region(u64 off);
+
+    // KV block runs carved by the block allocator (kv.cpp).
+    void carve_kv_run(u64 off, u64 nblocks, u64 block_len, u64 first_block);
+    // Release every KV extent inside [off, off+bytes) (teardown of a run).
+    void release_kv_range(u64 off, u64 bytes);
+
+    St validate() const;
+    std::string dump_json() const;
+
+private:
+    double alpha_of(const std::string& m) const {
+        auto it = alpha_.find(m);
+        return it == alpha_.end() ? 1.0 : it->second;
+    }
+
+    GpuDesc gpu_;
+    PoolMap map_;
+    std::unordered_map<Key, Entry, KeyHash> tensors_;
+    std::map<std::string, double> alpha_;
+    u64 kv_bytes_ = 0;
+    u64 pinned_tensor_bytes_ = 0;
+    u64 merged_total_ = 0;
+    u64 transferred_total_ = 0;
+    u64 evictions_total_ = 0;
+};
+
+}  // namespace tg

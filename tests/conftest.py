@@ -1,0 +1,33 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+@pytest.fixture(scope="session")
+def ref():
+    from oracle import ref as R
+    if not R.available():
+        pytest.skip("reference oracle (oracle/_ref) not built")
+    return R
+
+
+@pytest.fixture(scope="session")
+def cpu():
+    from oracle import cpu as O
+    return O
+
+
+@pytest.fixture(scope="session")
+def tg():
+    import paper_2512_01357_b200 as T
+    return T

@@ -1,0 +1,93 @@
+"""K1 fingerprint and K3 relocation kernels against the CPU oracle.
+
+Parity bar: bit-exact (integer/byte work).  Oracle: oracle/cpu_oracle.c
+(murmur3 restated from types.hpp:77-124, tgfp1 content fingerprint,
+synthetic bytes) — itself pinned to the compiled reference in test_oracle.py.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev_fp(tg, dptr, n):
+    from paper_2512_01357_b200 import _native as N
+    d = N.DigestC()
+    rc = N.lib.tg_fingerprint_device(C.c_void_p(dptr), n, 0, C.byref(d))
+    assert rc == 0, N.lib.tg_last_error_detail()
+    return (d.hi, d.lo)
+
+
+@pytest.mark.parametrize("n", [0, 1, 15, 16, 17, 4095, 4096, 4097, 4096 * 32, 4096 * 32 + 5, 131072 * 3 + 77,
+                               (1 << 22) + 12345])
+@pytest.mark.parametrize("shift", [0, 1, 3, 4, 7, 8, 13, 15])
+def test_fingerprint_matches_cpu(tg, cpu, n, shift):
+    from paper_2512_01357_b200.checkpoint import DeviceBuffer
+    from paper_2512_01357_b200 import _native as N
+    rng = np.random.default_rng(n * 31 + shift)
+    data = rng.integers(0, 256, size=n, dtype=np.uint8)
+    buf = DeviceBuffer(n + 64)
+    N.lib.tg_memcpy(C.c_void_p(buf.ptr + shift), data.ctypes.data_as(C.c_void_p), n)
+    got = _dev_fp(tg, buf.ptr + shift, n)
+    want, _ = cpu.content_fingerprint(data, threads=4)
+    assert got == want
+
+
+def test_fingerprint_large_synthetic(tg, cpu):
+    from paper_2512_01357_b200.checkpoint import DeviceBuffer
+    from paper_2512_01357_b200 import _native as N
+    tid = tg.TensorId(0x1234, 0x5678)
+    n = 68_611_111  # odd catalog size (opt1.3B layer attn)
+    buf = DeviceBuffer(n + 64)
+    assert N.lib.tg_synth_fill_device(tid.c(), 0, n, C.c_void_p(buf.ptr + 3), 0) == 0
+    host = np.empty(n, dtype=np.uint8)
+    N.lib.tg_memcpy(host.ctypes.data_as(C.c_void_p), C.c_void_p(buf.ptr + 3), n)
+    assert np.array_equal(host[:1 << 20], cpu.synth(tid.hi, tid.lo, 1 << 20))
+    assert np.array_equal(host[-4099:], cpu.synth(tid.hi, tid.lo, 4099, begin=n - 4099))
+    assert _dev_fp(tg, buf.ptr + 3, n) == cpu.content_fingerprint(host, threads=8)[0]
+
+
+def _relocate_case(tg, moves, arena_n, seed):
+    """Apply moves (src_off, dst_off, len) through tg_move_tensor on a pool and
+    compare the arena with a numpy memmove replay."""
+    from paper_2512_01357_b200 import _native as N
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=arena_n), device=0)
+    arena = pool.info()["arena"]
+    rng = np.random.default_rng(seed)
+    data = rng.integers(0, 256, size=arena_n, dtype=np.uint8)
+    N.lib.tg_memcpy(C.c_void_p(arena), data.ctypes.data_as(C.c_void_p), arena_n)
+    return pool, arena, data
+
+
+def test_relocation_kernel_random_alignments(tg):
+    """Single moves of every alignment class through tg_move_tensor (K3)."""
+    from paper_2512_01357_b200 import _native as N
+    rng = np.random.default_rng(7)
+    arena_n = 8 << 20
+    for case in range(40):
+        size = int(rng.integers(1, 300_000)) if case % 4 else int(rng.integers(1, 40))
+        pool = tg.ReuseStore(tg.GpuSpec(pool_size=arena_n), device=0)
+        arena = pool.info()["arena"]
+        m = tg.ModelSpec("m", [tg.TensorSpec(tg.TensorId(1, case), "m", "t", size)], size)
+        from paper_2512_01357_b200.checkpoint import PinnedBuffer
+        src = PinnedBuffer(size)
+        src.array()[:] = rng.integers(0, 256, size=size, dtype=np.uint8)
+        N.lib.tg_host_register(tg.TensorId(1, case).c(), C.c_void_p(src.ptr), size, None)
+        st = tg.ModelStatsTable()
+        pre = int(rng.integers(0, 64))
+        # occupy [0, pre) with a kv region so the tensor lands at an odd offset
+        if pre:
+            assert pool.alloc_kv_region(pre, 1).ok()
+        o = pool.load_model(m, st, 0.0).value()
+        pool.end_instance("m")
+        off = o.plan.placements[0].offset
+        to = int(rng.integers(off + size, arena_n - size))
+        assert pool.move_tensor(tg.TensorId(1, case), to).ok()
+        out = np.empty(size, dtype=np.uint8)
+        N.lib.tg_memcpy(out.ctypes.data_as(C.c_void_p), C.c_void_p(arena + to), size)
+        assert np.array_equal(out, src.array()), (case, size, off, to)
+        assert pool.fingerprint_tensor(tg.TensorId(1, case)) == o.digests[0]
+        N.lib.tg_host_unregister(tg.TensorId(1, case).c())
+        pool.close()
