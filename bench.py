@@ -1,0 +1,487 @@
+#!/usr/bin/env python
+"""Tangram B200 load-path benchmark.
+
+Workload (BASELINE.json configs[1]): the OPT-6.7B -> OPT-13B
+model switch in a 32 GiB pool.  Loads opt13B, opt6.7B run as setup; the timed
+step is the third load (opt13B again): 28 of 41 tensors reused in place
+(79.4 % of 26 GB), 13 tensors (5.35 GB) placed, 18 evictions, 15 relocations
+(7.62 GB compacted in 3 WAR waves), every placed and every reused tensor
+content-fingerprinted.  Before each step the pool (metadata + 32 GiB arena) is
+restored from a snapshot outside the timed region.
+
+* ``value``  — effective load GB/s (model bytes / step latency) with the
+  missing tensors' bytes already resident in HBM (an HBM model cache; placed
+  by the K3 copy kernel): the device data plane alone.
+* ``e2e``    — same metric through the C-ABI with the missing tensors in
+  pinned HOST memory: H2D over PCIe inside the timed region.
+* ``--impl reference`` — the reference's CPU path for the same load: the
+  compiled reference's ReuseStore::load_model (oracle/_ref) plus the CPU data
+  plane of apply_plan restated in oracle/cpu_oracle.c (memmove relocations,
+  memcpy placements, tgfp1 fingerprints), all host threads.
+
+Metric per step = one load.  Latency is the CUDA-event span on the pool's
+stream around the synchronous tg_load_model call (host planning included);
+N GPUs run N independent pools (weak scaling), max over ranks.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GIB = 1 << 30
+POOL = 32 * GIB
+SEQ = ["opt13B", "opt6.7B", "opt13B"]
+METRIC = "effective load GB/s, OPT-6.7B->OPT-13B switch (load #3, 79.4% tensor reuse, 32 GiB pool)"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-threads", type=int, default=0)
+    p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks, no baseline)")
+    return p.parse_args()
+
+
+# ---- clocks ---------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---- helpers -----------------------------------------------------------------------------------
+def catalog(tg):
+    return {m.model_id: m for m in tg.default_catalog()}
+
+
+def fresh_stats(tg, upto):
+    s = tg.ModelStatsTable()
+    for i, mid in enumerate(SEQ[:upto]):
+        s.record_request(mid, 10.0 * i)
+        s.set_load_bandwidth(mid, 55e9)
+    return s
+
+
+def measured_h2d_peak(dev):
+    """Pinned H2D bandwidth of this GPU's link (cudaMemcpyAsync, best of 3)."""
+    import torch
+    n = 2 * GIB
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    best = 1e9
+    for _ in range(3):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        d.copy_(h, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b) / 1e3)
+    del h, d
+    return n / best / 1e9
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy r+w)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---- CPU path (reference arm and cpu_baseline) ------------------------------------------------
+def cpu_load_once(ref, cpu, rcat, arena, sources, threads):
+    """The reference's CPU path for load #3: ReuseStore::load_model (compiled
+    reference) + apply_plan's bytes on a host arena (oracle port), all threads.
+    Returns (seconds, outcome)."""
+    import numpy as np
+    st = ref.ReuseStore(POOL)
+    stats = ref.ModelStatsTable()
+    for i, mid in enumerate(SEQ[:2]):
+        stats.record_request(mid, 10.0 * i)
+        stats.set_load_bandwidth(mid, 55e9)
+        st.load_model(rcat[mid], stats, 10.0 * i)
+        st.end_instance(mid)
+    stats.record_request(SEQ[2], 20.0)
+    stats.set_load_bandwidth(SEQ[2], 55e9)
+    base = arena.ctypes.data
+    t0 = time.perf_counter()
+    o = st.load_model(rcat[SEQ[2]], stats, 20.0)
+    for r in o["plan"]["relocations"]:
+        cpu.copy(base + r["to"], base + r["from"], r["size"], threads)
+    for p in o["plan"]["placements"]:
+        cpu.copy(base + p["offset"], sources[p["tensor"]], p["size"], threads)
+    final = {t["tensor"]: t for t in st.dump()["tensor_map"]}
+    for t in rcat[SEQ[2]]["tensors"]:
+        e = final[t["id"]]
+        cpu.content_fingerprint(base + e["offset"], threads, n=e["size"])
+    return time.perf_counter() - t0, o
+
+
+def cpu_setup(ref, cpu, threads):
+    """Host arena + host sources of load #3's misses (oracle synth)."""
+    import numpy as np
+    rcat = {m["model_id"]: m for m in ref.default_catalog()}
+    arena = np.empty(POOL + 64, dtype=np.uint8)
+    arena.fill(0)  # pre-fault
+    # misses of load #3 = sources needed; find them with a dry control-plane run
+    st = ref.ReuseStore(POOL)
+    stats = ref.ModelStatsTable()
+    for i, mid in enumerate(SEQ[:2]):
+        stats.record_request(mid, 10.0 * i)
+        stats.set_load_bandwidth(mid, 55e9)
+        st.load_model(rcat[mid], stats, 10.0 * i)
+        st.end_instance(mid)
+    miss = set(st.lookup(rcat[SEQ[2]])["misses"])
+    sources, keep = {}, []
+    for t in rcat[SEQ[2]]["tensors"]:
+        if t["id"] in miss:
+            hi, lo = int(t["id"][:16], 16), int(t["id"][16:], 16)
+            buf = np.empty(t["size"], dtype=np.uint8)
+            cpu.synth_into(hi, lo, buf.ctypes.data, t["size"])
+            keep.append(buf)
+            sources[t["id"]] = buf.ctypes.data
+    return rcat, arena, sources, keep
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    from oracle import cpu, ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return 0
+    threads = args.cpu_threads or os.cpu_count()
+    rcat, arena, sources, keep = cpu_setup(ref, cpu, threads)
+    total = rcat[SEQ[2]]["total_size"]
+    for _ in range(args.warmup):
+        cpu_load_once(ref, cpu, rcat, arena, sources, threads)
+    times = []
+    for _ in range(args.steps):
+        s, o = cpu_load_once(ref, cpu, rcat, arena, sources, threads)
+        times.append(s)
+    sec = sum(times) / len(times)
+    value = total / sec / 1e9
+    sample = (f"load #3 of the C2 switch per step: reference ReuseStore::load_model (oracle/_ref) + CPU data plane "
+              f"port (oracle/cpu_oracle.c): {len(o['plan']['relocations'])} relocations "
+              f"({o['bytes_merged']} B memmove), {len(o['plan']['placements'])} placements "
+              f"({o['bytes_transferred']} B memcpy from host), tgfp1 over all 41 tensors ({total} B)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": "C2 OPT-6.7B->OPT-13B switch, load #3, 32 GiB pool (host arena)",
+                       "threads": threads},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ---- our arm ---------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2512_01357_b200 as tg
+    from paper_2512_01357_b200 import _native as N
+    from paper_2512_01357_b200.checkpoint import DeviceBuffer, PinnedBuffer
+    lib = N.lib
+
+    cat = catalog(tg)
+    models = [cat["opt13B"], cat["opt6.7B"]]
+    target = cat[SEQ[2]]
+
+    # HBM model cache: every tensor of both models synthesised in HBM (setup
+    # loads and the value path place from here).
+    cache = {}
+    for m in models:
+        for t in m.tensors:
+            if t.id not in cache:
+                b = DeviceBuffer(t.size, local)
+                N.check_runtime(lib.tg_synth_fill_device(t.id.c(), 0, t.size, C.c_void_p(b.ptr), local))
+                cache[t.id] = b
+
+    def register_device(ids):
+        for tid in ids:
+            N.check_runtime(lib.tg_host_register(tid.c(), C.c_void_p(cache[tid].ptr), cache[tid].n, None))
+
+    register_device(cache.keys())
+    pool = tg.ReuseStore(tg.GpuSpec(f"gpu{local}", POOL), device=local)
+    for i, mid in enumerate(SEQ[:2]):
+        st = fresh_stats(tg, i + 1)
+        pool.load_model(cat[mid], st, 10.0 * i).value()
+        pool.end_instance(mid)
+    snap = pool.snapshot()
+    hits, misses = pool.lookup(target)
+    miss_ids = [t.id for t in misses]
+
+    # pinned host copies of the misses (the e2e sources)
+    host = {}
+    for t in misses:
+        pb = PinnedBuffer(t.size)
+        N.check_runtime(lib.tg_memcpy(C.c_void_p(pb.ptr), C.c_void_p(cache[t.id].ptr), t.size))
+        host[t.id] = pb
+
+    def register_host(ids):
+        for tid in ids:
+            N.check_runtime(lib.tg_host_register(tid.c(), C.c_void_p(host[tid].ptr), host[tid].n, None))
+
+    stream = torch.cuda.ExternalStream(pool.stream(), device=local)
+
+    def step():
+        pool.restore(snap)
+        st = fresh_stats(tg, 3)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        o = pool.load_model(target, st, 20.0, details=False).value()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b), o
+
+    def phase(register):
+        register(miss_ids)
+        for _ in range(args.warmup):
+            step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = lib.tg_kernel_launches()
+        ms, outs = [], []
+        for _ in range(args.steps):
+            t, o = step()
+            ms.append(t)
+            outs.append(o)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        launches = (lib.tg_kernel_launches() - l0) // max(1, args.steps)
+        return ms, outs, launches
+
+    clocks = ClockSampler(local)
+    if not args.profile:
+        clocks.start()
+    ms_v, outs_v, launches = phase(register_device)
+    ms_e, outs_e, _ = phase(register_host)
+    clk = clocks.stop() if not args.profile else {}
+
+    def maxrank(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    mv = maxrank(sum(ms_v) / len(ms_v))
+    me = maxrank(sum(ms_e) / len(ms_e))
+    o_v, o_e = outs_v[-1], outs_e[-1]
+    total = target.total_size
+
+    # parity of the timed load (last e2e step): decisions vs the reference,
+    # placed bytes vs the CPU restatement, reused bytes vs recorded digests
+    parity = {"verify_mismatches": sum(o.verify_mismatches for o in outs_v + outs_e),
+              "repaired_bytes": sum(o.repaired_bytes for o in outs_v + outs_e)}
+    if rank == 0 and not args.profile:
+        parity.update(check_parity(tg, pool, target, host, cache, local))
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    hbm_peak, peak_src = peaks()
+    h2d_peak = measured_h2d_peak(local)
+    fp_bytes = sum(t.size for t in target.tensors if t.id not in set(miss_ids))
+    fp_ms = statistics.mean(o.timings["fp_reuse_ms"] for o in outs_v)
+    rel_ms = statistics.mean(o.timings["relocate_ms"] for o in outs_v)
+    h2d_ms = statistics.mean(o.timings["h2d_ms"] for o in outs_e)
+    fp_ach = fp_bytes / (fp_ms / 1e3) / 1e9
+    rel_ach = 2 * o_v.bytes_merged / (rel_ms / 1e3) / 1e9
+    h2d_ach = o_e.pcie_bytes / (h2d_ms / 1e3) / 1e9
+
+    cpu_base = None
+    if not args.no_cpu_baseline and world == 1 and not args.profile:
+        cpu_base = cpu_baseline(args)
+
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "fp_reuse_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("traffic_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC,
+        "value": world * total / (mv / 1e3) / 1e9,
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": mv,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic: reference catalog tensor lists, splitmix64 bytes keyed by TensorId",
+        "config": {
+            "workload": "C2 OPT-6.7B->OPT-13B switch, load #3 (opt13B) in a 32 GiB pool",
+            "model_bytes": total, "reuse_ratio": round(1 - o_v.bytes_transferred / total, 4),
+            "bytes_transferred": o_v.bytes_transferred, "bytes_merged": o_v.bytes_merged,
+            "relocations": 15, "waves": o_v.waves, "placements": len(miss_ids), "reused": len(hits),
+            "value_sources": "missing tensors resident in HBM (model cache), placed by K3",
+            "e2e_sources": "missing tensors in pinned host memory, cudaMemcpyAsync H2D",
+            "fingerprint": "tgfp1 over all 41 tensors (13 placed + 28 reused verified)",
+            "l2": "no flush: every step streams >= 20 GB, >> 126 MB L2; arena restored (D2D 32 GiB) between steps",
+            "timing": "CUDA events on the pool stream around each synchronous load; snapshot restore untimed; "
+                      "mean over steps, max over ranks",
+            "parallelism": f"{world} independent pools (one per GPU)",
+        },
+        "latency_ms": {"value_path": mv, "e2e": me, "plan_us": o_v.timings["plan_us"],
+                       "relocate_ms": rel_ms, "h2d_ms": h2d_ms, "fp_reuse_ms": fp_ms,
+                       "fp_kernel_ms_total": o_v.timings["fp_kernel_ms"]},
+        "e2e": {"value": world * total / (me / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": me,
+                "h2d_bytes_per_step": o_e.pcie_bytes, "d2h_bytes_per_step": 16 * len(target.tensors)},
+        "roofline": {"bound": "hbm", "kernel": "K1 fp_leaves_kernel (reuse verification launch)",
+                     "achieved": fp_ach, "peak": hbm_peak, "unit": "GB/s", "frac": fp_ach / hbm_peak,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": fp_bytes, "peak_source": peak_src},
+        "roofline_relocate": {"bound": "hbm", "kernel": "K3 relocate_kernel (3 waves)", "achieved": rel_ach,
+                              "peak": hbm_peak, "unit": "GB/s", "frac": rel_ach / hbm_peak,
+                              "algorithmic_bytes_per_load": 2 * o_v.bytes_merged},
+        "roofline_h2d": {"bound": "pcie", "achieved": h2d_ach, "peak": h2d_peak, "unit": "GB/s",
+                         "frac": h2d_ach / h2d_peak, "peak_source": "measured pinned H2D 2 GiB in this run"},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "parity": parity,
+    }
+    if cpu_base:
+        line["cpu_baseline"] = cpu_base
+    print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def check_parity(tg, pool, target, host, cache, dev):
+    """Decisions/dump vs the compiled reference (if present) and placed bytes
+    vs the CPU restatement of tgfp1."""
+    out = {}
+    from oracle import cpu
+    info = {t.id: pool.tensor_info(t.id) for t in target.tensors}
+    ok = True
+    for tid, pb in host.items():
+        want, _ = cpu.content_fingerprint(pb.ptr, 16, n=pb.n)
+        ok &= info[tid]["digest"] == want
+    out["placed_digests_match_cpu_oracle"] = bool(ok)
+    try:
+        from oracle import ref
+        if ref.available():
+            rcat = {m["model_id"]: m for m in ref.default_catalog()}
+            st = ref.ReuseStore(POOL, gpu_id=f"gpu{dev}")
+            stats = ref.ModelStatsTable()
+            for i, mid in enumerate(SEQ):
+                stats.record_request(mid, 10.0 * i)
+                stats.set_load_bandwidth(mid, 55e9)
+                st.load_model(rcat[mid], stats, 10.0 * i)
+                if i < 2:
+                    st.end_instance(mid)
+            out["dump_equals_reference"] = st.dump() == pool.dump()
+    except Exception as e:  # pragma: no cover
+        out["dump_equals_reference"] = f"unavailable: {e}"
+    return out
+
+
+def cpu_baseline(args):
+    from oracle import cpu, ref
+    if not ref.available():
+        return None
+    threads = args.cpu_threads or os.cpu_count()
+    rcat, arena, sources, keep = cpu_setup(ref, cpu, threads)
+    cpu_load_once(ref, cpu, rcat, arena, sources, threads)
+    times = [cpu_load_once(ref, cpu, rcat, arena, sources, threads)[0] for _ in range(2)]
+    sec = min(times)
+    total = rcat[SEQ[2]]["total_size"]
+    return {"value": total / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+            "ms_per_step": sec * 1e3,
+            "sample": "2 timed replays of load #3 on a 32 GiB host arena: reference ReuseStore::load_model "
+                      "(oracle/_ref) + CPU data plane port (memmove relocations, memcpy placements, tgfp1 of all "
+                      "41 tensors)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

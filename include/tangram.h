@@ -100,7 +100,7 @@ typedef struct {
     uint64_t total_merge_cost, pgp_merge_cost, initial_merge_cost;
     double total_eviction_cost;
     /* data plane (device pools) */
-    uint64_t pcie_bytes, peer_bytes, fingerprint_bytes, repaired_bytes;
+    uint64_t pcie_bytes, peer_bytes, device_src_bytes, fingerprint_bytes, repaired_bytes;
     uint32_t verify_mismatches, expected_mismatches;
     double plan_us, total_ms, relocate_ms, h2d_ms, peer_ms, fp_kernel_ms, fp_reuse_ms;
 } tg_load_outcome;
@@ -125,7 +125,7 @@ typedef struct {
 typedef struct {
     tg_tensor_id tensor;
     uint64_t offset, size;
-    uint32_t source; /* 0 host/PCIe, 1 peer/NVLink */
+    uint32_t source; /* 0 host/PCIe, 1 peer pool/NVLink, 2 device-resident source (HBM) */
 } tg_placement;
 
 /* warmsim::Region (region_pool.hpp:22-28) */
@@ -164,6 +164,7 @@ int tg_version(void);
 const char* tg_error_string(int code);
 const char* tg_last_error_detail(void); /* thread-local detail of the last failure */
 int tg_device_count(int* n);
+uint64_t tg_kernel_launches(void); /* kernels launched by this library so far */
 
 /* ---- ids, catalog (types.hpp:131-146, catalog.hpp:37-90) ------------------- */
 int tg_murmur3_x64_128(const void* data, uint64_t len, uint64_t seed, tg_digest* out);
@@ -228,7 +229,10 @@ int tg_pool_snapshot(tg_pool* p, tg_snapshot** out);
 int tg_pool_restore(tg_pool* p, const tg_snapshot* s);
 void tg_snapshot_destroy(tg_snapshot* s);
 
-/* ---- host checkpoint sources (data side-channel) -------------- */
+/* ---- host checkpoint sources (data side-channel) --------------
+ * ptr may be pinned host memory (placed over PCIe by the copy engine) or
+ * device memory, e.g. an HBM-resident model cache (placed by the K3 copy
+ * kernel; source kind 2 in tg_placement). */
 int tg_host_register(tg_tensor_id id, const void* ptr, uint64_t size, const tg_digest* expected /*nullable*/);
 int tg_host_unregister(tg_tensor_id id);
 int tg_host_clear(void);
@@ -263,6 +267,22 @@ int tg_kv_table(const tg_kv* kv, uint64_t request_id, uint64_t* pbns, uint64_t c
 int tg_kv_address_table(const tg_kv* kv, uint64_t* triples /*pbn,off,size*/, uint64_t cap, uint64_t* n); /* :63 */
 int tg_kv_stats_get(const tg_kv* kv, tg_kv_stats* out);
 int tg_kv_device_tables(const tg_kv* kv, void** tables, uint64_t* stride, void** addr); /* for paged attention */
+
+/* ---- planner (plan_allocation, packing.hpp:311-483) ----------------------------
+ * Pure two-stage plan over an address-ordered region tiling.  new_tensors are
+ * placed in the given order after a stable size-descending sort; candidates
+ * are sorted by (cost, -size, last_access, id) unless keep_candidate_order. */
+typedef struct tg_plan tg_plan;
+int tg_plan_allocation(const tg_region* regions, uint64_t n_regions, const tg_tensor_spec* new_tensors,
+                       uint32_t n_new, const tg_eviction* candidates, uint32_t n_candidates,
+                       const tg_tensor_id* immovable, uint32_t n_immovable, int32_t strictness, int32_t merge,
+                       int32_t keep_candidate_order, tg_plan** out);
+uint32_t tg_plan_evictions(const tg_plan* p, tg_eviction* buf, uint32_t cap);
+uint32_t tg_plan_relocations(const tg_plan* p, tg_relocation* buf, uint32_t cap);
+uint32_t tg_plan_placements(const tg_plan* p, tg_placement* buf, uint32_t cap);
+int tg_plan_costs(const tg_plan* p, double* total_eviction_cost, uint64_t* total_merge_cost, uint64_t* pgp_merge_cost,
+                  uint64_t* initial_merge_cost, uint64_t* fallback_evictions);
+void tg_plan_destroy(tg_plan* p);
 
 /* ---- scheduler (scheduler.hpp:41-120) ------------------------------------------ */
 typedef struct {

@@ -473,7 +473,15 @@ const char* ref_brute_force_oracle(const char* instance_json) {
 // ---- scheduler --------------------------------------------------------------
 // in: {"requests":[model ids], "snapshots":[{gpu_id,available,pool_size,free_bytes,
 //      reuse:{model:bytes}, pcie, store}], "models":[model json], "batch_size", "block_size_tokens"}
+static const char* ref_schedule_impl(const char* in_json);
 const char* ref_schedule(const char* in_json) {
+    try {
+        return ref_schedule_impl(in_json);
+    } catch (const std::exception& e) {
+        return emit(json{{"exception", e.what()}});
+    }
+}
+static const char* ref_schedule_impl(const char* in_json) {
     const json j = json::parse(in_json);
     std::vector<std::string> reqs = j.at("requests").get<std::vector<std::string>>();
     std::vector<GpuSnapshot> snaps;
@@ -483,7 +491,8 @@ const char* ref_schedule(const char* in_json) {
         g.available = s.value("available", true);
         g.pool_size = s.at("pool_size").get<Bytes>();
         g.free_bytes = s.value("free_bytes", Bytes{0});
-        for (const auto& [k, v] : s.value("reuse", json::object()).items()) g.reuse_size_by_model[k] = v.get<Bytes>();
+        const json reuse = s.value("reuse", json::object());
+        for (const auto& [k, v] : reuse.items()) g.reuse_size_by_model[k] = v.get<Bytes>();
         g.pcie_bandwidth = s.at("pcie").get<double>();
         g.store_bandwidth = s.at("store").get<double>();
         snaps.push_back(g);

@@ -6,6 +6,7 @@ affinity scheduler) driving sm_100a kernels for content fingerprints,
 relocation/compaction, KV block tables and NVLink peer pulls.  This package is
 the thin Python mirror of the reference's C++ API used by tests and bench.py.
 """
+from . import pool
 from .pool import (AllocationPlan, Error, GpuSnapshot, GpuSpec, KvEngine, LoadOutcome, LoadPolicy, MergePolicy,
                    ModelLocation, ModelSpec, ModelStatsTable, PackingStrictness, Result, ReuseStore, Rng,
                    TensorId, TensorSpec, default_catalog, estimate_load_time, make_model, murmur3_x64_128,

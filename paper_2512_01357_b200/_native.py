@@ -52,7 +52,7 @@ class LoadOutcomeC(C.Structure):
                 ("bytes_transferred", u64), ("bytes_merged", u64), ("eviction_cost_total", dbl),
                 ("total_merge_cost", u64), ("pgp_merge_cost", u64), ("initial_merge_cost", u64),
                 ("total_eviction_cost", dbl),
-                ("pcie_bytes", u64), ("peer_bytes", u64), ("fingerprint_bytes", u64), ("repaired_bytes", u64),
+                ("pcie_bytes", u64), ("peer_bytes", u64), ("device_src_bytes", u64), ("fingerprint_bytes", u64), ("repaired_bytes", u64),
                 ("verify_mismatches", u32), ("expected_mismatches", u32),
                 ("plan_us", dbl), ("total_ms", dbl), ("relocate_ms", dbl), ("h2d_ms", dbl), ("peer_ms", dbl),
                 ("fp_kernel_ms", dbl), ("fp_reuse_ms", dbl)]
@@ -103,6 +103,7 @@ _SIGS = {
     "tg_error_string": (cp, [C.c_int]),
     "tg_last_error_detail": (cp, []),
     "tg_device_count": (C.c_int, [P(C.c_int)]),
+    "tg_kernel_launches": (u64, []),
     "tg_murmur3_x64_128": (C.c_int, [vp, u64, u64, P(DigestC)]),
     "tg_tensor_key": (C.c_int, [cp, cp, P(i64), i32, i32, P(TensorIdC)]),
     "tg_model_make": (C.c_int, [cp, u64, i32, u64, i32, dbl, P(vp)]),
@@ -174,6 +175,13 @@ _SIGS = {
     "tg_kv_address_table": (C.c_int, [vp, P(u64), u64, P(u64)]),
     "tg_kv_stats_get": (C.c_int, [vp, P(KvStatsC)]),
     "tg_kv_device_tables": (C.c_int, [vp, P(vp), P(u64), P(vp)]),
+    "tg_plan_allocation": (C.c_int, [P(RegionC), u64, P(TensorSpecC), u32, P(EvictionC), u32, P(TensorIdC), u32,
+                                     i32, i32, i32, P(vp)]),
+    "tg_plan_evictions": (u32, [vp, P(EvictionC), u32]),
+    "tg_plan_relocations": (u32, [vp, P(RelocationC), u32]),
+    "tg_plan_placements": (u32, [vp, P(PlacementC), u32]),
+    "tg_plan_costs": (C.c_int, [vp, P(dbl), P(u64), P(u64), P(u64), P(u64)]),
+    "tg_plan_destroy": (None, [vp]),
     "tg_schedule": (C.c_int, [P(u32), u32, P(GpuSnapshotC), u32, P(ModelSpecC), u32, P(u64), P(u64), u32, u64,
                               P(i32), P(dbl)]),
     "tg_estimate_load_time": (dbl, [P(ModelSpecC), u64, P(GpuSnapshotC), u64]),

@@ -158,8 +158,10 @@ void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums,
         const u64 cap = static_cast<u64>(sm_count) * 4;
         const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
         fp_leaves_kernel<<<blocks, 256, 0, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
+        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     }
     fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 }  // namespace tg

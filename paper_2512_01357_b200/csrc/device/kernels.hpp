@@ -4,9 +4,13 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 namespace tg {
+
+// Number of kernels this library has launched (bench.py's gpu_launches).
+extern std::atomic<std::uint64_t> g_kernel_launches;
 
 // ---- K1: content fingerprint (tgfp1) -------------------------------------
 // Leaf = 4096 B, leaf_i digest = murmur3_x64_128(leaf bytes, seed = i);

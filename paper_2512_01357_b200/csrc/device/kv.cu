@@ -260,12 +260,14 @@ void kv_batch_launch(const KvBatchArgs& a, cudaStream_t s) {
     if (a.total == 0) return;
     const unsigned blocks = static_cast<unsigned>((a.total + 255) / 256);
     kv_batch_kernel<<<blocks, 256, 0, s>>>(a);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void kv_release_launch(const u64* table_row, u64 blocks, u64* free_list_dst, cudaStream_t s) {
     if (blocks == 0) return;
     const unsigned grid = static_cast<unsigned>((blocks + 255) / 256 < 1024 ? (blocks + 255) / 256 : 1024);
     kv_copy_kernel<<<grid, 256, 0, s>>>(table_row, blocks, free_list_dst);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 std::unique_ptr<KvDevice> make_kv_device(int device, cudaStream_t stream) {

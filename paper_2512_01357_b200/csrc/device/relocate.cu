@@ -141,6 +141,7 @@ void relocate_launch(const MoveDesc* moves, int n_moves, int sm_count, cudaStrea
         const u32 want = (total + 7) / 8;
         const u32 cap = static_cast<u32>(sm_count) * 4;
         relocate_kernel<<<want < cap ? want : cap, 256, 0, s>>>(a);
+        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     }
 }
 

@@ -44,6 +44,9 @@ void synth_launch(u64 hi, u64 lo, u64 begin, u64 len, std::uint8_t* dst, cudaStr
     if (len == 0) return;
     const u64 seed = hi ^ ((lo << 17) | (lo >> 47));
     synth_kernel<<<148 * 8, 256, 0, s>>>(seed, begin, len, dst);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
+
+std::atomic<std::uint64_t> g_kernel_launches{0};
 
 }  // namespace tg

@@ -12,6 +12,7 @@
 
 #include "../../../include/tangram.h"
 #include "../device/common.cuh"
+#include "../device/kernels.hpp"
 #include "kv.hpp"
 #include "pool.hpp"
 #include "sched.hpp"
@@ -131,6 +132,8 @@ const char* tg_error_string(int code) {
 }
 
 const char* tg_last_error_detail(void) { return g_detail.c_str(); }
+
+uint64_t tg_kernel_launches(void) { return g_kernel_launches.load(); }
 
 int tg_device_count(int* n) {
     cudaError_t e = cudaGetDeviceCount(n);
@@ -309,6 +312,7 @@ int tg_load_model(tg_pool* p, const tg_model_spec* ms, const tg_stats* s, double
             out->total_eviction_cost = pl.total_eviction_cost;
             out->pcie_bytes = r.pcie_bytes;
             out->peer_bytes = r.peer_bytes;
+            out->device_src_bytes = r.device_src_bytes;
             out->fingerprint_bytes = r.fingerprint_bytes;
             out->repaired_bytes = r.repaired_bytes;
             out->verify_mismatches = r.verify_mismatches;
@@ -500,7 +504,10 @@ void tg_snapshot_destroy(tg_snapshot* s) {
 // ---- host sources ------------------------------------------------------------------
 int tg_host_register(tg_tensor_id id, const void* ptr, uint64_t size, const tg_digest* expected) {
     if (!ptr && size) return TG_ERR_BAD_ARG;
-    HostSource s{ptr, size, expected != nullptr, expected ? Digest{expected->hi, expected->lo} : Digest{}};
+    HostSource s{ptr, size, expected != nullptr, expected ? Digest{expected->hi, expected->lo} : Digest{}, false};
+    cudaPointerAttributes a{};
+    if (ptr && cudaPointerGetAttributes(&a, ptr) == cudaSuccess) s.on_device = a.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
     SourceRegistry::get().put(key_of(id), s);
     return 0;
 }
@@ -701,6 +708,84 @@ int tg_kv_device_tables(const tg_kv* kv, void** tables, uint64_t* stride, void**
     *addr = d->addr_ptr();
     return 0;
 }
+
+// ---- planner ------------------------------------------------------------------------------------
+struct tg_plan {
+    Plan plan;
+    std::vector<TensorDesc> tensors;
+};
+
+int tg_plan_allocation(const tg_region* regions, uint64_t n_regions, const tg_tensor_spec* new_tensors,
+                       uint32_t n_new, const tg_eviction* candidates, uint32_t n_cand, const tg_tensor_id* immovable,
+                       uint32_t n_imm, int32_t strictness, int32_t merge, int32_t keep_order, tg_plan** out) {
+    return guard([&] {
+        if (!out || (n_regions && !regions)) return TG_ERR_BAD_ARG;
+        std::vector<Region> regs;
+        u64 pool = 0;
+        for (uint64_t i = 0; i < n_regions; ++i) {
+            const tg_region& r = regions[i];
+            regs.push_back(Region{r.offset, r.size, static_cast<Kind>(r.kind), key_of(r.tensor), r.block_id});
+            pool = std::max<u64>(pool, r.offset + r.size);
+        }
+        const PoolMap map = PoolMap::from_regions(pool, regs);
+        auto p = std::make_unique<tg_plan>();
+        for (uint32_t i = 0; i < n_new; ++i)
+            p->tensors.push_back(TensorDesc{key_of(new_tensors[i].id),
+                                            new_tensors[i].model_id ? new_tensors[i].model_id : "",
+                                            new_tensors[i].name ? new_tensors[i].name : "", new_tensors[i].size});
+        PlanInput in;
+        in.pool = &map;
+        in.tensors = &p->tensors;
+        for (uint32_t i = 0; i < n_cand; ++i)
+            in.candidates.push_back(Candidate{key_of(candidates[i].tensor), candidates[i].size, candidates[i].cost,
+                                              candidates[i].last_access,
+                                              candidates[i].model_id ? candidates[i].model_id : ""});
+        for (uint32_t i = 0; i < n_imm; ++i) in.immovable.insert(key_of(immovable[i]));
+        in.strictness = strictness ? Strictness::LiteralGuard : Strictness::Functional;
+        in.merge = merge ? MergeMode::GlobalMerge : MergeMode::PartitionedGain;
+        in.keep_candidate_order = keep_order != 0;
+        PoolMap work;
+        auto res = make_plan(in, &work);
+        if (!res) return code_of(res.error());
+        p->plan = std::move(res.value());
+        *out = p.release();
+        return 0;
+    });
+}
+
+uint32_t tg_plan_evictions(const tg_plan* p, tg_eviction* buf, uint32_t cap) {
+    const auto& ev = p->plan.evictions;
+    for (uint32_t i = 0; buf && i < ev.size() && i < cap; ++i)
+        buf[i] = tg_eviction{id_of(ev[i].tensor), ev[i].size, ev[i].cost, ev[i].last_access, ev[i].model_id.c_str()};
+    return static_cast<uint32_t>(ev.size());
+}
+
+uint32_t tg_plan_relocations(const tg_plan* p, tg_relocation* buf, uint32_t cap) {
+    const auto& rl = p->plan.relocations;
+    for (uint32_t i = 0; buf && i < rl.size() && i < cap; ++i)
+        buf[i] = tg_relocation{id_of(rl[i].tensor), rl[i].from, rl[i].to, rl[i].size, 0};
+    return static_cast<uint32_t>(rl.size());
+}
+
+uint32_t tg_plan_placements(const tg_plan* p, tg_placement* buf, uint32_t cap) {
+    const auto& pl = p->plan.placements;
+    for (uint32_t i = 0; buf && i < pl.size() && i < cap; ++i) {
+        const TensorDesc& t = p->tensors[pl[i].tensor];
+        buf[i] = tg_placement{id_of(t.id), pl[i].off, t.size, 0};
+    }
+    return static_cast<uint32_t>(pl.size());
+}
+
+int tg_plan_costs(const tg_plan* p, double* ec, uint64_t* tm, uint64_t* pgp, uint64_t* init, uint64_t* fb) {
+    if (ec) *ec = p->plan.total_eviction_cost;
+    if (tm) *tm = p->plan.total_merge_cost;
+    if (pgp) *pgp = p->plan.pgp_merge_cost;
+    if (init) *init = p->plan.initial_merge_cost;
+    if (fb) *fb = p->plan.fallback_evictions;
+    return 0;
+}
+
+void tg_plan_destroy(tg_plan* p) { delete p; }
 
 // ---- scheduler ------------------------------------------------------------------------------
 static GpuView view_of(const tg_gpu_snapshot& g) {

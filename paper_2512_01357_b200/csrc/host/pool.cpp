@@ -142,11 +142,16 @@ St Pool::load_model(const ModelDesc& m, const RequestShares& stats, double clock
             if (!SourceRegistry::get().find(t.id, &src[i]) || src[i].size != t.size)
                 throw DeviceError(kErrNoSource, "no host source registered for tensor " + t.id.hex() + " (" +
                                                     t.model_id + "/" + t.name + ")");
+            if (src[i].on_device) {  // HBM-resident model cache: SM copy, not the PCIe engine
+                peer_src[i] = static_cast<const std::uint8_t*>(src[i].ptr);
+                rep->placement_src[i] = 2;
+            }
         }
     }
 
     // Relocation waves: wave(k) = 1 + max wave(j), j < k, dst_k ∩ src_j ≠ ∅.
-    const auto& rel = d.plan.relocations;
+    // (copy: the decision is moved into the report below)
+    const std::vector<Move> rel = d.plan.relocations;
     rep->reloc_wave.assign(rel.size(), 0);
     u32 waves = 0;
     for (std::size_t k = 0; k < rel.size(); ++k) {
@@ -173,7 +178,11 @@ St Pool::load_model(const ModelDesc& m, const RequestShares& stats, double clock
     LoadDecision& D = rep->decision;
     if (!has_device()) return ok();
 
-    for (std::size_t i = 0; i < np; ++i) (rep->placement_src[i] ? rep->peer_bytes : rep->pcie_bytes) += D.miss_desc[D.plan.placements[i].tensor].size;
+    for (std::size_t i = 0; i < np; ++i) {
+        const u64 sz = D.miss_desc[D.plan.placements[i].tensor].size;
+        const std::uint8_t k = rep->placement_src[i];
+        (k == 0 ? rep->pcie_bytes : k == 1 ? rep->peer_bytes : rep->device_src_bytes) += sz;
+    }
 
     // ---- event layout -----------------------------------------------------------
     // 0 t0 | 1 reloc start | 2 reloc end | 3 end | 4 h2d start | 5 h2d end | 6 peer start | 7 peer end
@@ -303,7 +312,7 @@ St Pool::load_model(const ModelDesc& m, const RequestShares& stats, double clock
     rep->t.total_ms = ms_between(ev(0), ev(3));
     rep->t.relocate_ms = waves ? ms_between(ev(1), ev(2)) : 0.0;
     rep->t.h2d_ms = rep->pcie_bytes ? ms_between(ev(4), ev(5)) : 0.0;
-    rep->t.peer_ms = rep->peer_bytes ? ms_between(ev(6), ev(7)) : 0.0;
+    rep->t.peer_ms = (rep->peer_bytes || rep->device_src_bytes) ? ms_between(ev(6), ev(7)) : 0.0;
     for (std::size_t f = 0; f < fp_i; ++f) {
         const double t = ms_between(ev(ev_fp + 2 * f), ev(ev_fp + 2 * f + 1));
         rep->t.fp_kernel_ms += t;

@@ -33,6 +33,7 @@ struct HostSource {
     u64 size = 0;
     bool has_expected = false;
     Digest expected;
+    bool on_device = false;  // HBM-resident source: placed by the K3 copy kernel
 };
 
 class SourceRegistry {
@@ -69,7 +70,7 @@ struct LoadReport {
     std::vector<u32> reloc_wave;     // WAR wave of each relocation
     std::vector<std::uint8_t> placement_src;  // 0 = host (PCIe), 1 = peer (NVLink)
     u32 waves = 0;
-    u64 pcie_bytes = 0, peer_bytes = 0, fingerprint_bytes = 0, repaired_bytes = 0;
+    u64 pcie_bytes = 0, peer_bytes = 0, device_src_bytes = 0, fingerprint_bytes = 0, repaired_bytes = 0;
     u32 verify_mismatches = 0, expected_mismatches = 0;
     std::vector<Digest> digests;     // per model tensor (model order), when fingerprinted
     LoadTimings t;

@@ -140,6 +140,13 @@ std::vector<Region> PoolMap::expanded() const {
     return out;
 }
 
+PoolMap PoolMap::from_regions(u64 pool_size, const std::vector<Region>& regs) {
+    PoolMap m;
+    m.pool_ = pool_size;
+    for (const Region& r : regs) m.put(Extent{r.off, r.len, r.kind, r.tensor, r.block, 1});
+    return m;
+}
+
 St PoolMap::validate() const {
     u64 cursor = 0, free_sum = 0, count = 0;
     bool prev_free = false;

@@ -107,6 +107,9 @@ public:
 
     std::vector<Region> expanded() const;
     St validate() const;
+    // Rebuild from an address-ordered tiling (RegionList::from_snapshot,
+    // region_pool.hpp:176-184); no coalescing is applied.
+    static PoolMap from_regions(u64 pool_size, const std::vector<Region>& regs);
 
 private:
     using It = std::map<u64, Extent>::iterator;

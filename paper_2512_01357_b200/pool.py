@@ -325,6 +325,7 @@ class LoadOutcome:
     waves: int = 0
     pcie_bytes: int = 0
     peer_bytes: int = 0
+    device_src_bytes: int = 0
     fingerprint_bytes: int = 0
     repaired_bytes: int = 0
     verify_mismatches: int = 0
@@ -409,7 +410,7 @@ class ReuseStore:
         t = {k: getattr(o, k) for k in ("plan_us", "total_ms", "relocate_ms", "h2d_ms", "peer_ms", "fp_kernel_ms",
                                         "fp_reuse_ms")}
         return LoadOutcome(hits, misses, o.bytes_transferred, o.bytes_merged, o.eviction_cost_total, plan,
-                           o.n_waves, o.pcie_bytes, o.peer_bytes, o.fingerprint_bytes, o.repaired_bytes,
+                           o.n_waves, o.pcie_bytes, o.peer_bytes, o.device_src_bytes, o.fingerprint_bytes, o.repaired_bytes,
                            o.verify_mismatches, o.expected_mismatches, t, digs)
 
     def end_instance(self, model_id):
@@ -651,6 +652,47 @@ class KvEngine:
         s = C.c_uint64()
         N.check_runtime(lib.tg_kv_device_tables(self._h, C.byref(t), C.byref(s), C.byref(a)), "tg_kv_device_tables")
         return t.value, s.value, a.value
+
+
+KIND_CODE = {"free": 0, "tensor": 1, "kv_block": 2}
+
+
+def plan_allocation(regions, new_tensors: Sequence[TensorSpec], candidates: Sequence[EvictionCandidate] = (),
+                    immovable: Sequence[TensorId] = (), strictness=0, merge=0, randomize_eviction=False) -> Result:
+    """plan_allocation (packing.hpp:311-483) over an explicit region tiling.
+    regions: [(offset, size, kind, TensorId|None, block_id)] with kind in
+    {"free", "tensor", "kv_block"}."""
+    R = (N.RegionC * max(1, len(regions)))()
+    for i, (off, size, kind, tid, blk) in enumerate(regions):
+        R[i] = N.RegionC(off, size, KIND_CODE[kind], (tid or TensorId()).c(), blk or 0)
+    keep = [t.name.encode() for t in new_tensors], [t.model_id.encode() for t in new_tensors]
+    T = (N.TensorSpecC * max(1, len(new_tensors)))()
+    for i, t in enumerate(new_tensors):
+        T[i] = N.TensorSpecC(t.id.c(), keep[0][i], t.size, keep[1][i])
+    mids = [c.model_id.encode() for c in candidates]
+    E = (N.EvictionC * max(1, len(candidates)))()
+    for i, c in enumerate(candidates):
+        E[i] = N.EvictionC(c.tensor.c(), c.size, c.cost, c.last_access, mids[i])
+    I = (N.TensorIdC * max(1, len(immovable)))(*[t.c() for t in immovable])
+    h = C.c_void_p()
+    rc = lib.tg_plan_allocation(R, len(regions), T, len(new_tensors), E, len(candidates), I, len(immovable),
+                                int(strictness), int(merge), int(randomize_eviction), C.byref(h))
+    N.check_runtime(rc, "tg_plan_allocation")
+    if rc:
+        return Result(error=Error(rc - 1))
+    try:
+        ev = [EvictionCandidate(TensorId(e.tensor.hi, e.tensor.lo), e.size, e.cost, e.last_access,
+                                e.model_id.decode()) for e in _fetch(lib.tg_plan_evictions, h,
+                                                                     N.EvictionC, lib.tg_plan_evictions(h, None, 0))]
+        rl = [Relocation(TensorId(r.tensor.hi, r.tensor.lo), r.from_, r.to, r.size)
+              for r in _fetch(lib.tg_plan_relocations, h, N.RelocationC, lib.tg_plan_relocations(h, None, 0))]
+        pl = [Placement(TensorId(p.tensor.hi, p.tensor.lo), p.offset, p.size)
+              for p in _fetch(lib.tg_plan_placements, h, N.PlacementC, lib.tg_plan_placements(h, None, 0))]
+        ec, tm, pgp, init, fb = C.c_double(), C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        lib.tg_plan_costs(h, C.byref(ec), C.byref(tm), C.byref(pgp), C.byref(init), C.byref(fb))
+        return Result(AllocationPlan(ev, rl, pl, ec.value, tm.value, pgp.value, init.value, fb.value))
+    finally:
+        lib.tg_plan_destroy(h)
 
 
 @dataclass

@@ -1,0 +1,256 @@
+"""Device load path on a B200: decisions bit-exact with the reference
+(golden fixtures from oracle/_ref), pooled bytes bit-exact with the CPU
+restatement (every resident tensor's device fingerprint equals tgfp1 of its
+synthetic checkpoint bytes computed on the CPU), block tables equal to the
+reference's.
+"""
+import ctypes as C
+import json
+import os
+
+import numpy as np
+import pytest
+
+from test_control_plane import result_json
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+GIB = 1 << 30
+
+
+def _expected_digest(cpu, tid, size):
+    data = cpu.synth(tid.hi, tid.lo, size)
+    return cpu.content_fingerprint(data, threads=16)[0]
+
+
+class HbmCache:
+    """Device-resident synthetic sources for a set of models."""
+
+    def __init__(self, tg, models, device=0):
+        from paper_2512_01357_b200 import _native as N
+        from paper_2512_01357_b200.checkpoint import DeviceBuffer
+        self.bufs = {}
+        for m in models:
+            for t in m.tensors:
+                if t.id in self.bufs:
+                    continue
+                b = DeviceBuffer(t.size, device)
+                assert N.lib.tg_synth_fill_device(t.id.c(), 0, t.size, C.c_void_p(b.ptr), device) == 0
+                assert N.lib.tg_host_register(t.id.c(), C.c_void_p(b.ptr), t.size, None) == 0
+                self.bufs[t.id] = b
+
+    def close(self):
+        from paper_2512_01357_b200 import _native as N
+        for tid, b in self.bufs.items():
+            N.lib.tg_host_unregister(tid.c())
+            b.free()
+
+
+def _check_pooled_bytes(tg, cpu, pool, expected_cache):
+    """Every resident tensor: device fingerprint == CPU tgfp1 of its bytes."""
+    dump = pool.dump()
+    for e in dump["tensor_map"]:
+        tid = tg.TensorId.from_hex(e["tensor"])
+        if tid not in expected_cache:
+            expected_cache[tid] = _expected_digest(cpu, tid, e["size"])
+        assert pool.fingerprint_tensor(tid) == expected_cache[tid], e
+        assert pool.tensor_info(tid)["digest"] == expected_cache[tid]
+
+
+@pytest.mark.parametrize("case,merge", [("pg_32", 0), ("gm_36", 1)])
+def test_c2_switch_bytes_and_decisions(tg, cpu, case, merge):
+    g = json.load(open(os.path.join(GOLDEN, "c1_c2_loads.json")))[case]
+    gib = int(case.split("_")[1])
+    cat = {m.model_id: m for m in tg.default_catalog()}
+    seq = ["opt13B", "opt6.7B", "opt13B", "opt6.7B", "opt13B"]
+    cache = HbmCache(tg, [cat["opt13B"], cat["opt6.7B"]])
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=gib * GIB), device=0)
+    stats = tg.ModelStatsTable()
+    expected = {}
+    try:
+        for i, mid in enumerate(seq):
+            stats.record_request(mid, 10.0 * i)
+            stats.set_load_bandwidth(mid, 55e9)
+            r = pool.load_model(cat[mid], stats, 10.0 * i, tg.LoadPolicy(merge=merge))
+            assert result_json(r) == g["loads"][i], f"load {i}"
+            o = r.value()
+            assert o.verify_mismatches == 0 and o.repaired_bytes == 0
+            assert o.device_src_bytes == o.bytes_transferred
+            _check_pooled_bytes(tg, cpu, pool, expected)
+            pool.end_instance(mid)
+        assert pool.dump() == g["final_dump"]
+    finally:
+        pool.close()
+        cache.close()
+
+
+def test_c1_cold_then_warm_from_host(tg, cpu):
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    g = json.load(open(os.path.join(GOLDEN, "c1_c2_loads.json")))["c1_160"]
+    m = {x.model_id: x for x in tg.default_catalog()}["opt1.3B"]
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=160 * GIB), device=0)
+    stats = tg.ModelStatsTable()
+    with HostCheckpoint([m]) as ck:
+        outs = []
+        for i in range(2):
+            stats.record_request(m.model_id, 10.0 * i)
+            stats.set_load_bandwidth(m.model_id, 55e9)
+            r = pool.load_model(m, stats, 10.0 * i)
+            assert result_json(r) == g["loads"][i]
+            outs.append(r.value())
+            pool.end_instance(m.model_id)
+        cold, warm = outs
+        assert cold.pcie_bytes == m.total_size and warm.pcie_bytes == 0
+        for i, t in enumerate(m.tensors):
+            want = cpu.content_fingerprint(ck.view(t.id), threads=16)[0]
+            assert cold.digests[i] == want and warm.digests[i] == want
+        assert warm.fingerprint_bytes == m.total_size and warm.verify_mismatches == 0
+    pool.close()
+
+
+def test_verification_repairs_drifted_bytes(tg, cpu):
+    """A reused tensor whose bytes no longer match its recorded fingerprint is
+    re-sent from its host source (content decides reuse vs transfer)."""
+    from paper_2512_01357_b200 import _native as N
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    m = tg.make_model("drift", 40_000_017, 3, 64)
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=64 << 20), device=0)
+    stats = tg.ModelStatsTable()
+    with HostCheckpoint([m]) as ck:
+        cold = pool.load_model(m, stats, 0.0).value()
+        pool.end_instance("drift")
+        victim = m.tensors[1]
+        info = pool.tensor_info(victim.id)
+        junk = np.full(4096, 0xAB, dtype=np.uint8)
+        N.lib.tg_memcpy(C.c_void_p(info["device_ptr"] + 1000), junk.ctypes.data_as(C.c_void_p), junk.size)
+        warm = pool.load_model(m, stats, 1.0).value()
+        assert warm.bytes_transferred == 0  # the key still says "hit"
+        assert warm.verify_mismatches == 1 and warm.repaired_bytes == victim.size
+        assert pool.fingerprint_tensor(victim.id) == cold.digests[1]
+        assert pool.fingerprint_tensor(victim.id) == cpu.content_fingerprint(ck.view(victim.id), threads=8)[0]
+    pool.close()
+
+
+def test_snapshot_restore_roundtrip(tg):
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    a, b = tg.make_model("a", 30_000_001, 2, 0), tg.make_model("b", 30_000_003, 3, 0)
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=70_000_000), device=0)
+    st = tg.ModelStatsTable()
+    with HostCheckpoint([a, b]):
+        pool.load_model(a, st, 0.0).value()
+        pool.end_instance("a")
+        snap = pool.snapshot()
+        d0 = pool.dump()
+        fps = {t.id: pool.fingerprint_tensor(t.id) for t in a.tensors}
+        st.record_request("b", 1.0)
+        pool.load_model(b, st, 1.0).value()  # evicts / moves a's tensors
+        assert pool.dump() != d0
+        pool.restore(snap)
+        assert pool.dump() == d0
+        assert {t.id: pool.fingerprint_tensor(t.id) for t in a.tensors} == fps
+    pool.close()
+
+
+def test_peer_pull_same_device(tg, cpu):
+    """Misses resident in a peer pool are pulled device-to-device (K5 path;
+    on one GPU the peer is a second pool on the same device)."""
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    m = tg.make_model("peer", 50_000_021, 3, 0)
+    a = tg.ReuseStore(tg.GpuSpec("gpu0", 80_000_000), device=0)
+    b = tg.ReuseStore(tg.GpuSpec("gpu1", 80_000_000), device=0)
+    b.add_peer(a)
+    sa, sb = tg.ModelStatsTable(), tg.ModelStatsTable()
+    with HostCheckpoint([m]) as ck:
+        oa = a.load_model(m, sa, 0.0).value()
+        assert b.peer_reuse_size(m) == m.total_size
+        ob = b.load_model(m, sb, 0.0, tg.LoadPolicy(flags=1 | 2 | 4)).value()
+        assert ob.peer_bytes == m.total_size and ob.pcie_bytes == 0
+        assert all(p.source == 1 for p in ob.plan.placements)
+        assert ob.digests == oa.digests
+        for i, t in enumerate(m.tensors):
+            assert ob.digests[i] == cpu.content_fingerprint(ck.view(t.id), threads=8)[0]
+    a.close()
+    b.close()
+
+
+def test_c3_kv_tables_match_reference(tg):
+    """Llama-2-13B + prefill burst (16 / 64 ShareGPT prompts, seed 7) and one
+    decode-step batch: device block tables equal the reference's."""
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    g = json.load(open(os.path.join(GOLDEN, "c3_kv.json")))
+    model = tg.make_model("llama2-13B", 26_000_000_000, 40, 819_200)
+    with HostCheckpoint([model]):
+        for n, case in g.items():
+            pool = tg.ReuseStore(tg.GpuSpec(pool_size=160 * GIB), device=0)
+            stats = tg.ModelStatsTable()
+            stats.record_request("llama2-13B", 0.0)
+            pool.load_model(model, stats, 0.0).value()
+            kv = tg.KvEngine("llama2-13B", 16, 819_200)
+            reqs = [tuple(r) for r in case["requests"]]
+            assert kv.batch_allocate(pool, stats, reqs).value() == case["burst"]
+            dec = [(r, (p + 15) // 16 * 16 + 1) for r, p in reqs]
+            assert kv.batch_allocate(pool, stats, dec).value() == case["decode"]
+            for rid, want in case["tables"].items():
+                t = kv.table(int(rid))
+                assert t.token_count == want["token_count"]
+                assert [[k, v] for k, v in sorted(t.lbn_to_pbn.items())] == want["lbn_to_pbn"]
+            # address table in HBM agrees with the host's carve runs
+            tables, stride, addr = kv.device_tables()
+            at = kv.address_table()
+            from paper_2512_01357_b200 import _native as N
+            hi = max(at) + 1
+            buf = (C.c_uint64 * hi)()
+            N.lib.tg_memcpy(buf, C.c_void_p(addr), 8 * hi)
+            assert all(buf[p] == off for p, (off, _) in at.items())
+            kv.instance_teardown(pool)
+            assert pool.kv_bytes() == 0 and pool.validate().ok()
+            pool.close()
+
+
+def test_kv_device_fuzz_vs_reference(tg, ref):
+    """Random batches / releases / teardowns on a device pool: every table
+    read back from HBM equals the reference's."""
+    import random
+    rnd = random.Random(11)
+    for trial in range(6):
+        pool_size = rnd.randint(40_000, 100_000)
+        mine = tg.ReuseStore(tg.GpuSpec(pool_size=pool_size), device=0)
+        theirs = ref.ReuseStore(pool_size)
+        sm, sr = tg.ModelStatsTable(), ref.ModelStatsTable()
+        kvm, kvr = tg.KvEngine("s", 8, 100), ref.KvEngine("s", 8, 100)
+        live, nxt = {}, 1
+        for step in range(60):
+            op = rnd.random()
+            if op < 0.6:
+                reqs = []
+                for _ in range(rnd.randint(1, 4)):
+                    if live and rnd.random() < 0.5:
+                        rid = rnd.choice(list(live))
+                        reqs.append((rid, live[rid] + rnd.randint(0, 20)))
+                    else:
+                        reqs.append((nxt, rnd.randint(0, 40)))
+                        nxt += 1
+                a = kvm.batch_allocate(mine, sm, reqs)
+                b = kvr.batch_allocate(theirs, sr, reqs)
+                assert a.ok() == b["ok"]
+                if b["ok"]:
+                    assert a.value() == b["granted"]
+                for rid, tok in reqs:
+                    tb = kvr.table(rid)
+                    if tb:
+                        live[rid] = tb["token_count"]
+            elif op < 0.9 and live:
+                rid = rnd.choice(list(live))
+                kvm.release_request(rid)
+                kvr.release_request(rid)
+                live.pop(rid)
+            else:
+                kvm.instance_teardown(mine)
+                kvr.instance_teardown(theirs)
+                live.clear()
+            for rid in live:
+                t, rt = kvm.table(rid), kvr.table(rid)
+                assert [[k, v] for k, v in sorted(t.lbn_to_pbn.items())] == rt["lbn_to_pbn"]
+            assert mine.dump() == theirs.dump()
+        mine.close()
