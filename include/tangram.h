@@ -87,8 +87,11 @@ typedef struct {
     int32_t merge;          /* 0 PartitionedGain, 1 GlobalMerge (packing.hpp:125) */
     int32_t strictness;     /* 0 Functional, 1 LiteralGuard (packing.hpp:92) */
     int32_t random_eviction;
-    tg_rng* rng;            /* required for random eviction */
+    tg_rng* rng;            /* required for random eviction (or the callback below) */
     uint32_t flags;         /* TG_LOAD_* ; 0 means TG_LOAD_DEFAULT */
+    /* alternative to rng: the caller's own stream, uniform in [0, n) */
+    uint64_t (*uniform_below)(void* ctx, uint64_t n);
+    void* rng_ctx;
 } tg_load_policy;
 
 /* warmsim::LoadOutcome (reuse_store.hpp:34-41) summary + measured data plane */
@@ -180,6 +183,12 @@ int tg_model_shard(const tg_model* m, uint32_t rank, uint32_t world, tg_model** 
 
 /* ---- request shares (ModelStatsTable, model.hpp:70-133) -------------------- */
 int tg_stats_create(double decay, tg_stats** out);
+/* Statistics owned by the caller (e.g. the reference's ModelStatsTable behind
+ * the C++ facade): p_m and b_m are read through callbacks when eviction costs
+ * are computed (reuse_store.hpp:104-105).  record_* calls do not apply. */
+int tg_stats_create_external(void* ctx, double (*miss_probability)(void* ctx, const char* model_id),
+                             double (*load_bandwidth_or)(void* ctx, const char* model_id, double fallback),
+                             tg_stats** out);
 void tg_stats_destroy(tg_stats* s);
 int tg_stats_record_request(tg_stats* s, const char* model_id, double t);
 int tg_stats_record_eviction(tg_stats* s, const char* model_id, double t);

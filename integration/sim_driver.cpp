@@ -1,0 +1,79 @@
+// Drop-in check driver: runs the reference's own discrete-event Simulator
+// (simulator.hpp, unmodified) on a generated trace and prints RunMetrics as
+// JSON.  Built twice by integration/Makefile: once against the pure reference
+// headers, once with integration/ first on the include path so that
+// "warmsim/reuse_store.hpp" and "warmsim/kv_engine.hpp" resolve to the B200
+// bindings.  tests/test_dropin.py requires byte-identical output.
+#include <cstdio>
+#include <cstdlib>
+#include <iostream>
+#include <string>
+
+#include "json.hpp"
+#include "warmsim/catalog.hpp"
+#include "warmsim/simulator.hpp"
+#include "warmsim/workload.hpp"
+
+int main(int argc, char** argv) {
+    using namespace warmsim;
+    if (argc < 11) {
+        std::fprintf(stderr,
+                     "usage: %s mode n_gpus pool_gib batch keep_alive n_requests seed eviction merge locality\n",
+                     argv[0]);
+        return 2;
+    }
+    const std::string mode = argv[1];
+    const int n = std::atoi(argv[2]);
+    const double pool_gib = std::atof(argv[3]);
+    const auto catalog = default_catalog();
+    TraceSpec ts;
+    ts.seed = std::strtoull(argv[7], nullptr, 10);
+    ts.num_requests = std::strtoull(argv[6], nullptr, 10);
+    ts.locality = locality_from_string(argv[10]);
+    ts.mean_interarrival = 0.5;
+    for (const auto& m : catalog) ts.model_ids.push_back(m.model_id);
+    const Trace trace = generate_trace(ts);
+    SimConfig cfg;
+    for (int g = 0; g < n; ++g)
+        cfg.gpus.push_back(GpuSpec{"gpu" + std::to_string(g), static_cast<Bytes>(pool_gib * (1ull << 30)), 55e9,
+                                   3000e9, 12e9});
+    cfg.mode = sim_mode_from_string(mode);
+    cfg.batch_size = static_cast<std::uint32_t>(std::atoi(argv[4]));
+    cfg.keep_alive = std::atof(argv[5]);
+    cfg.eviction = std::atoi(argv[8]) ? EvictionSelection::Random : EvictionSelection::MinCost;
+    cfg.merge = std::atoi(argv[9]) ? MergePolicy::GlobalMerge : MergePolicy::PartitionedGain;
+    cfg.emit_alloc_log = true;
+    cfg.emit_sched_log = true;
+    cfg.emit_timeseries = true;
+    RunMetrics m;
+    try {
+        Simulator sim(cfg, catalog);
+        m = sim.run(trace);
+    } catch (const std::exception& e) {  // ConfigError / RuntimeInfeasible: compare those too
+        std::cout << nlohmann::json{{"exception", e.what()}}.dump() << "\n";
+        return 0;
+    }
+    nlohmann::json j;
+    auto recs = nlohmann::json::array();
+    for (const auto& r : m.records)
+        recs.push_back({r.request_id, r.model_id, r.gpu_id, r.t_arrival, r.t_scheduled, r.queued_time, r.t_init,
+                        r.t_load, r.t_profile, r.t_prefill, r.ttft, r.t_complete, r.bytes_transferred,
+                        r.bytes_merged, r.cold_start});
+    j["records"] = recs;
+    const auto& a = m.aggregates;
+    j["aggregates"] = {a.mean_ttft, a.p99_ttft, a.mean_load, a.total_bytes_transferred, a.total_bytes_merged,
+                       a.mean_pool_utilization, a.cold_starts, a.warm_joins};
+    j["counters"] = {m.makespan, m.deferral_events, m.evictions, m.early_terminations, m.odkv_overhead_total,
+                     m.load_compute_total, m.load_merge_total, m.load_transfer_total};
+    j["kv"] = {m.kv.pool_invocations, m.kv.alloc_batches, m.kv.blocks_from_free_list, m.kv.blocks_from_pool,
+               m.kv.reclaim_events};
+    auto ts_arr = nlohmann::json::array();
+    for (const auto& s : m.timeseries) ts_arr.push_back({s.t, s.reusable, s.free_bytes, s.kv_bytes, s.utilization});
+    j["timeseries"] = ts_arr;
+    auto al = nlohmann::json::array();
+    for (const auto& r : m.alloc_log) al.push_back({r.t, r.request_id, r.blocks, r.source});
+    j["alloc_log"] = al;
+    j["sched_log"] = m.sched_log;
+    std::cout << j.dump() << "\n";
+    return 0;
+}

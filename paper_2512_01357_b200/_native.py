@@ -43,7 +43,8 @@ class ModelSpecC(C.Structure):
 
 
 class LoadPolicyC(C.Structure):
-    _fields_ = [("merge", i32), ("strictness", i32), ("random_eviction", i32), ("rng", vp), ("flags", u32)]
+    _fields_ = [("merge", i32), ("strictness", i32), ("random_eviction", i32), ("rng", vp), ("flags", u32),
+                ("uniform_below", vp), ("rng_ctx", vp)]
 
 
 class LoadOutcomeC(C.Structure):
@@ -114,6 +115,7 @@ _SIGS = {
     "tg_model_shard": (C.c_int, [vp, u32, u32, P(vp)]),
     "tg_stats_create": (C.c_int, [dbl, P(vp)]),
     "tg_stats_destroy": (None, [vp]),
+    "tg_stats_create_external": (C.c_int, [vp, vp, vp, P(vp)]),
     "tg_stats_record_request": (C.c_int, [vp, cp, dbl]),
     "tg_stats_record_eviction": (C.c_int, [vp, cp, dbl]),
     "tg_stats_set_load_bandwidth": (C.c_int, [vp, cp, dbl]),

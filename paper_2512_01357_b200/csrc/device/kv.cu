@@ -62,8 +62,17 @@ __global__ void kv_copy_kernel(const u64* __restrict__ src, u64 n, u64* __restri
 // Device-resident tables of one KV engine.
 class KvDeviceImpl final : public KvDevice {
 public:
-    KvDeviceImpl(int device, cudaStream_t stream) : dev_(device), s_(stream) {}
-    ~KvDeviceImpl() override { release_all(); }
+    // The engine owns its stream: block tables are independent of the arena
+    // bytes (KV allocation moves no bytes), and an engine may outlive the
+    // pool it was first used with.
+    explicit KvDeviceImpl(int device) : dev_(device) {
+        DeviceScope ds(dev_);
+        TG_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+    }
+    ~KvDeviceImpl() override {
+        release_all();
+        if (s_) cudaStreamDestroy(s_);
+    }
 
     int apply_batch(const KvBatchWork& w, u64 block_bytes, u64* out_pbns) override {
         DeviceScope ds(dev_);
@@ -155,12 +164,15 @@ public:
 
     std::unique_ptr<KvDevice> clone() const override {
         DeviceScope ds(dev_);
-        auto c = std::make_unique<KvDeviceImpl>(dev_, s_);
-        c->grow(slots_, stride_, free_cap_, pbn_cap_);
+        auto c = std::make_unique<KvDeviceImpl>(dev_);
+        c->grow(static_cast<u32>(slots_), stride_, free_cap_, pbn_cap_);
+        TG_CUDA(cudaStreamSynchronize(s_));  // source tables complete
+        cudaStream_t cs = c->s_;
         if (slots_ && stride_)
-            TG_CUDA(cudaMemcpyAsync(c->tables_, tables_, slots_ * stride_ * sizeof(u64), cudaMemcpyDeviceToDevice, s_));
-        if (free_cap_) TG_CUDA(cudaMemcpyAsync(c->free_, free_, free_cap_ * sizeof(u64), cudaMemcpyDeviceToDevice, s_));
-        if (pbn_cap_) TG_CUDA(cudaMemcpyAsync(c->addr_, addr_, pbn_cap_ * sizeof(u64), cudaMemcpyDeviceToDevice, s_));
+            TG_CUDA(cudaMemcpyAsync(c->tables_, tables_, slots_ * stride_ * sizeof(u64), cudaMemcpyDeviceToDevice, cs));
+        if (free_cap_) TG_CUDA(cudaMemcpyAsync(c->free_, free_, free_cap_ * sizeof(u64), cudaMemcpyDeviceToDevice, cs));
+        if (pbn_cap_) TG_CUDA(cudaMemcpyAsync(c->addr_, addr_, pbn_cap_ * sizeof(u64), cudaMemcpyDeviceToDevice, cs));
+        TG_CUDA(cudaStreamSynchronize(cs));
         return c;
     }
 
@@ -270,8 +282,8 @@ void kv_release_launch(const u64* table_row, u64 blocks, u64* free_list_dst, cud
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-std::unique_ptr<KvDevice> make_kv_device(int device, cudaStream_t stream) {
-    return std::make_unique<KvDeviceImpl>(device, stream);
+std::unique_ptr<KvDevice> make_kv_device(int device, cudaStream_t /*pool stream: not shared*/) {
+    return std::make_unique<KvDeviceImpl>(device);
 }
 
 }  // namespace tg

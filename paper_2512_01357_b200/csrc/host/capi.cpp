@@ -25,7 +25,9 @@ struct tg_pool {
     std::vector<std::string> strs;  // backing store for returned model ids
 };
 struct tg_stats {
-    RequestShares s;
+    RequestShares own;
+    std::unique_ptr<ExternalStats> ext;  // caller-owned statistics (tg_stats_create_external)
+    const StatsView& s_view() const { return ext ? static_cast<const StatsView&>(*ext) : own; }
 };
 struct tg_rng {
     Rng r;
@@ -85,13 +87,18 @@ ModelDesc model_of(const tg_model_spec* s) {
     return m;
 }
 
-LoadOptions options_of(const tg_load_policy* p) {
+LoadOptions options_of(const tg_load_policy* p, std::unique_ptr<UniformCallback>* keep) {
     LoadOptions o;
     if (!p) return o;
     o.merge = p->merge ? MergeMode::GlobalMerge : MergeMode::PartitionedGain;
     o.strictness = p->strictness ? Strictness::LiteralGuard : Strictness::Functional;
     o.random_eviction = p->random_eviction != 0;
-    o.rng = p->rng ? &p->rng->r : nullptr;
+    if (p->rng) {
+        o.rng = &p->rng->r;
+    } else if (p->uniform_below) {
+        *keep = std::make_unique<UniformCallback>(p->rng_ctx, p->uniform_below);
+        o.rng = keep->get();
+    }
     return o;
 }
 
@@ -220,17 +227,23 @@ int tg_model_shard(const tg_model* m, uint32_t rank, uint32_t world, tg_model** 
 
 // ---- stats / rng ------------------------------------------------------------------
 int tg_stats_create(double decay, tg_stats** out) {
-    *out = new tg_stats{RequestShares(decay)};
+    *out = new tg_stats{RequestShares(decay), nullptr};
+    return 0;
+}
+int tg_stats_create_external(void* ctx, double (*miss_probability)(void*, const char*),
+                             double (*load_bandwidth_or)(void*, const char*, double), tg_stats** out) {
+    if (!miss_probability || !load_bandwidth_or || !out) return TG_ERR_BAD_ARG;
+    *out = new tg_stats{RequestShares(), std::make_unique<ExternalStats>(ctx, miss_probability, load_bandwidth_or)};
     return 0;
 }
 void tg_stats_destroy(tg_stats* s) { delete s; }
-int tg_stats_record_request(tg_stats* s, const char* m, double t) { return code_of(s->s.record_request(m, t)); }
-int tg_stats_record_eviction(tg_stats* s, const char* m, double t) { return code_of(s->s.record_eviction(m, t)); }
+int tg_stats_record_request(tg_stats* s, const char* m, double t) { return code_of(s->own.record_request(m, t)); }
+int tg_stats_record_eviction(tg_stats* s, const char* m, double t) { return code_of(s->own.record_eviction(m, t)); }
 int tg_stats_set_load_bandwidth(tg_stats* s, const char* m, double bw) {
-    s->s.set_load_bandwidth(m, bw);
+    s->own.set_load_bandwidth(m, bw);
     return 0;
 }
-double tg_stats_miss_probability(const tg_stats* s, const char* m) { return s->s.miss_probability(m); }
+double tg_stats_miss_probability(const tg_stats* s, const char* m) { return s->own.miss_probability(m); }
 
 int tg_rng_create(uint64_t seed, tg_rng** out) {
     *out = new tg_rng{Rng(seed)};
@@ -291,7 +304,8 @@ int tg_load_model(tg_pool* p, const tg_model_spec* ms, const tg_stats* s, double
         const ModelDesc m = model_of(ms);
         const u32 flags = (pol && pol->flags) ? pol->flags : static_cast<u32>(TG_LOAD_DEFAULT);
         LoadReport& r = p->last;
-        St st = p->pool->load_model(m, s->s, clock, options_of(pol), flags, &r);
+        std::unique_ptr<UniformCallback> cb;
+        St st = p->pool->load_model(m, s->s_view(), clock, options_of(pol, &cb), flags, &r);
         if (!st) return code_of(st);
         if (out) {
             const Plan& pl = r.decision.plan;
@@ -425,7 +439,7 @@ int tg_peer_reuse_size(const tg_pool* p, const tg_model_spec* ms, uint64_t* out)
 
 int tg_eviction_candidates(tg_pool* p, const tg_stats* s, const char* exclude, tg_eviction* buf, uint32_t cap,
                            uint32_t* n) {
-    auto c = p->pool->store().candidates(s->s, exclude ? exclude : "");
+    auto c = p->pool->store().candidates(s->s_view(), exclude ? exclude : "");
     *n = static_cast<uint32_t>(c.size());
     p->strs.clear();
     p->strs.reserve(c.size());
@@ -618,7 +632,7 @@ int tg_kv_ensure_capacity(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t rid
         std::vector<u64> g;
         u64 n = 0;
         const bool want = granted && p->pool->has_device();
-        St st = kv->a->ensure_capacity(p->pool->store(), s->s, rid, tokens, want ? &g : nullptr, &n);
+        St st = kv->a->ensure_capacity(p->pool->store(), s->s_view(), rid, tokens, want ? &g : nullptr, &n);
         if (n_granted) *n_granted = n;
         if (want)
             for (u64 i = 0; i < g.size() && i < cap; ++i) granted[i] = g[i];
@@ -634,7 +648,7 @@ int tg_kv_batch_allocate(tg_kv* kv, tg_pool* p, const tg_stats* s, const uint64_
         for (uint64_t i = 0; i < n; ++i) reqs[i] = {rids[i], tokens[i]};
         std::vector<u64> c, g;
         const bool want = pbns && p->pool->has_device();
-        St st = kv->a->batch_allocate(p->pool->store(), s->s, reqs, &c, want ? &g : nullptr);
+        St st = kv->a->batch_allocate(p->pool->store(), s->s_view(), reqs, &c, want ? &g : nullptr);
         u64 t = 0;
         for (uint64_t i = 0; i < n; ++i) {
             if (counts) counts[i] = c[i];
@@ -660,7 +674,7 @@ int tg_kv_teardown(tg_kv* kv, tg_pool* p) {
 int tg_kv_urgent_reclaim(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t blocks) {
     return guard([&] {
         if (int rc = bind_kv(kv, p)) return rc;
-        return code_of(kv->a->urgent_reclaim(p->pool->store(), s->s, blocks));
+        return code_of(kv->a->urgent_reclaim(p->pool->store(), s->s_view(), blocks));
     });
 }
 int tg_kv_table(const tg_kv* kv, uint64_t rid, uint64_t* pbns, uint64_t cap, uint64_t* n, uint64_t* token_count) {

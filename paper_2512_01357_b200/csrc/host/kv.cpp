@@ -58,7 +58,7 @@ u64 KvAllocator::fittable(const Store& s) const {
     return n;
 }
 
-u64 KvAllocator::acquire(Store& s, const RequestShares& st, u32 slot, u64 lbn0, u64 need, bool* touched,
+u64 KvAllocator::acquire(Store& s, const StatsView& st, u32 slot, u64 lbn0, u64 need, bool* touched,
                          KvBatchWork* w, bool* exhausted) {
     u64 got = 0;
     // LIFO free list first (kv_engine.hpp:205-210).
@@ -98,7 +98,7 @@ u64 KvAllocator::acquire(Store& s, const RequestShares& st, u32 slot, u64 lbn0, 
     return got;
 }
 
-St KvAllocator::ensure_one(Store& s, const RequestShares& st, u64 rid, u64 tokens, KvBatchWork* w, u64* granted) {
+St KvAllocator::ensure_one(Store& s, const StatsView& st, u64 rid, u64 tokens, KvBatchWork* w, u64* granted) {
     *granted = 0;
     Req& r = req(rid);
     if (tokens < r.tokens) return Err::InvalidArgument;
@@ -126,7 +126,7 @@ int KvAllocator::flush(KvBatchWork& w, std::vector<u64>* pbns) {
     return dev_->apply_batch(w, block_bytes_, pbns ? pbns->data() : nullptr);
 }
 
-St KvAllocator::ensure_capacity(Store& s, const RequestShares& st, u64 rid, u64 tokens, std::vector<u64>* granted,
+St KvAllocator::ensure_capacity(Store& s, const StatsView& st, u64 rid, u64 tokens, std::vector<u64>* granted,
                                 u64* n_granted) {
     KvBatchWork w;
     w.free_before = free_count_;
@@ -138,7 +138,7 @@ St KvAllocator::ensure_capacity(Store& s, const RequestShares& st, u64 rid, u64 
     return res;
 }
 
-St KvAllocator::batch_allocate(Store& s, const RequestShares& st, const std::vector<std::pair<u64, u64>>& reqs,
+St KvAllocator::batch_allocate(Store& s, const StatsView& st, const std::vector<std::pair<u64, u64>>& reqs,
                                std::vector<u64>* counts, std::vector<u64>* pbns) {
     counts->assign(reqs.size(), 0);
     u64 needed = 0;
@@ -223,7 +223,7 @@ void KvAllocator::teardown(Store& s) {
     if (dev_) dev_->reset();
 }
 
-St KvAllocator::urgent_reclaim(Store& s, const RequestShares& st, u64 blocks) {
+St KvAllocator::urgent_reclaim(Store& s, const StatsView& st, u64 blocks) {
     auto cands = s.candidates(st, model_);
     std::sort(cands.begin(), cands.end(), candidate_before);
     std::size_t next = 0;

@@ -103,15 +103,15 @@ public:
 
     // ensure_capacity (kv_engine.hpp:75-102).  `granted` (nullable) receives
     // the new PBNs; *n_granted their count.
-    St ensure_capacity(Store& s, const RequestShares& st, u64 rid, u64 tokens, std::vector<u64>* granted,
+    St ensure_capacity(Store& s, const StatsView& st, u64 rid, u64 tokens, std::vector<u64>* granted,
                        u64* n_granted);
     // batch_allocate (kv_engine.hpp:107-161).  counts[i] = blocks granted to
     // request i; `pbns` (nullable) receives all new PBNs in order.
-    St batch_allocate(Store& s, const RequestShares& st, const std::vector<std::pair<u64, u64>>& reqs,
+    St batch_allocate(Store& s, const StatsView& st, const std::vector<std::pair<u64, u64>>& reqs,
                       std::vector<u64>* counts, std::vector<u64>* pbns);
     St release_request(u64 rid);
     void teardown(Store& s);
-    St urgent_reclaim(Store& s, const RequestShares& st, u64 blocks);
+    St urgent_reclaim(Store& s, const StatsView& st, u64 blocks);
 
     // table(rid) / address_table() readers.
     St table(u64 rid, std::vector<u64>* lbn_to_pbn, u64* tokens) const;
@@ -127,9 +127,9 @@ private:
     Req& req(u64 rid);
     // Acquire `need` blocks for `slot` in order; appends to *w.  Returns the
     // number granted (== need unless the pool is exhausted).
-    u64 acquire(Store& s, const RequestShares& st, u32 slot, u64 lbn0, u64 need, bool* touched, KvBatchWork* w,
+    u64 acquire(Store& s, const StatsView& st, u32 slot, u64 lbn0, u64 need, bool* touched, KvBatchWork* w,
                 bool* exhausted);
-    St ensure_one(Store& s, const RequestShares& st, u64 rid, u64 tokens, KvBatchWork* w, u64* granted);
+    St ensure_one(Store& s, const StatsView& st, u64 rid, u64 tokens, KvBatchWork* w, u64* granted);
     int flush(KvBatchWork& w, std::vector<u64>* pbns);
 
     std::string model_;

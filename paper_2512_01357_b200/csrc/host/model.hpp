@@ -41,10 +41,35 @@ struct GpuDesc {
     double store_bw = 0;
 };
 
+// What the eviction cost needs from the request statistics
+// (reuse_store.hpp:104-105): p_m and b_m per model.
+class StatsView {
+public:
+    virtual ~StatsView() = default;
+    virtual double miss_probability(const std::string& model) const = 0;
+    virtual double load_bandwidth_or(const std::string& model, double fallback) const = 0;
+};
+
+// Statistics owned by the caller (e.g. the reference's own ModelStatsTable
+// behind the C++ facade), read through callbacks.
+class ExternalStats final : public StatsView {
+public:
+    using PFn = double (*)(void*, const char*);
+    using BFn = double (*)(void*, const char*, double);
+    ExternalStats(void* ctx, PFn p, BFn b) : ctx_(ctx), p_(p), b_(b) {}
+    double miss_probability(const std::string& m) const override { return p_(ctx_, m.c_str()); }
+    double load_bandwidth_or(const std::string& m, double f) const override { return b_(ctx_, m.c_str(), f); }
+
+private:
+    void* ctx_;
+    PFn p_;
+    BFn b_;
+};
+
 // Exponentially-decayed request counters; miss probability = share of the
 // total.  Arithmetic order is kept statement-for-statement with
 // model.hpp:87-105 so every double is bit-identical.
-class RequestShares {
+class RequestShares final : public StatsView {
 public:
     explicit RequestShares(double decay = 0.95) : decay_(decay) {}
 
@@ -75,12 +100,12 @@ public:
 
     void set_load_bandwidth(const std::string& model, double bw) { row(model).load_bw = bw; }
 
-    double miss_probability(const std::string& model) const {
+    double miss_probability(const std::string& model) const override {
         auto it = rows_.find(model);
         return it == rows_.end() ? 0.0 : it->second.p_miss;
     }
 
-    double load_bandwidth_or(const std::string& model, double fallback) const {
+    double load_bandwidth_or(const std::string& model, double fallback) const override {
         auto it = rows_.find(model);
         return (it != rows_.end() && it->second.load_bw > 0.0) ? it->second.load_bw : fallback;
     }

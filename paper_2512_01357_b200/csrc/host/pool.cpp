@@ -103,7 +103,7 @@ u64 build_tasks(std::vector<FpTask>& tasks) {
 
 }  // namespace
 
-St Pool::load_model(const ModelDesc& m, const RequestShares& stats, double clock, const LoadOptions& opt, u32 flags,
+St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, const LoadOptions& opt, u32 flags,
                     LoadReport* rep) {
     using clk = std::chrono::steady_clock;
     *rep = LoadReport{};

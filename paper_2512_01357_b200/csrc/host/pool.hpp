@@ -92,7 +92,7 @@ public:
     cudaStream_t stream() const { return s_main_; }
     int sm_count() const { return sm_count_; }
 
-    St load_model(const ModelDesc& m, const RequestShares& stats, double clock, const LoadOptions& opt, u32 flags,
+    St load_model(const ModelDesc& m, const StatsView& stats, double clock, const LoadOptions& opt, u32 flags,
                   LoadReport* rep);
     St move_tensor(const Key& k, u64 to);  // metadata + bytes
 

@@ -18,7 +18,7 @@ u64 Store::reuse_size(const ModelDesc& m) const {
     return s;
 }
 
-std::vector<Candidate> Store::candidates(const RequestShares& stats, const std::string& exclude) const {
+std::vector<Candidate> Store::candidates(const StatsView& stats, const std::string& exclude) const {
     std::vector<Candidate> out;
     out.reserve(tensors_.size());
     for (const auto& [k, e] : tensors_) {
@@ -31,7 +31,7 @@ std::vector<Candidate> Store::candidates(const RequestShares& stats, const std::
     return out;
 }
 
-Res<LoadDecision> Store::decide(const ModelDesc& m, const RequestShares& stats, const LoadOptions& opt) {
+Res<LoadDecision> Store::decide(const ModelDesc& m, const StatsView& stats, const LoadOptions& opt) {
     set_alpha(m.model_id, m.alpha);
     u64 pinned_self = 0;  // an already-active model reloading itself stays idempotent
     for (const auto& t : m.tensors)

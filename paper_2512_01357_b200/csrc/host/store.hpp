@@ -25,13 +25,20 @@ struct DeviceError : std::runtime_error {
     DeviceError(int c, const std::string& what) : std::runtime_error(what), code(c) {}
 };
 
+// Uniform draws for random-eviction order (reuse_store.hpp:143-147).
+class Uniform {
+public:
+    virtual ~Uniform() = default;
+    virtual u64 uniform_below(u64 n) = 0;
+};
+
 // mt19937_64 stream + rejection-sampled uniform_below; the same stream the
 // reference Rng produces (rng.hpp:18-73).
-class Rng {
+class Rng final : public Uniform {
 public:
     explicit Rng(u64 seed) : gen_(seed) {}
     u64 next() { return gen_(); }
-    u64 uniform_below(u64 n) {
+    u64 uniform_below(u64 n) override {
         const u64 limit = UINT64_MAX - UINT64_MAX % n;
         u64 x;
         do x = gen_();
@@ -43,11 +50,22 @@ private:
     std::mt19937_64 gen_;
 };
 
+// Caller-owned random stream (e.g. the simulator's own Rng behind the facade).
+class UniformCallback final : public Uniform {
+public:
+    UniformCallback(void* ctx, u64 (*fn)(void*, u64)) : ctx_(ctx), fn_(fn) {}
+    u64 uniform_below(u64 n) override { return fn_(ctx_, n); }
+
+private:
+    void* ctx_;
+    u64 (*fn_)(void*, u64);
+};
+
 struct LoadOptions {
     MergeMode merge = MergeMode::PartitionedGain;
     Strictness strictness = Strictness::Functional;
     bool random_eviction = false;
-    Rng* rng = nullptr;
+    Uniform* rng = nullptr;
 };
 
 struct Digest {
@@ -102,12 +120,12 @@ public:
     void lookup(const ModelDesc& m, std::vector<u32>* hits, std::vector<u32>* misses) const;
     u64 reuse_size(const ModelDesc& m) const;
     // eviction_candidates (reuse_store.hpp:99-115)
-    std::vector<Candidate> candidates(const RequestShares& stats, const std::string& exclude) const;
+    std::vector<Candidate> candidates(const StatsView& stats, const std::string& exclude) const;
 
     // load_model, split in two (reuse_store.hpp:120-174).  decide() performs
     // the alpha update, the capacity check, lookup and planning without
     // touching the layout; commit() applies the decision and pins.
-    Res<LoadDecision> decide(const ModelDesc& m, const RequestShares& stats, const LoadOptions& opt);
+    Res<LoadDecision> decide(const ModelDesc& m, const StatsView& stats, const LoadOptions& opt);
     void commit(const ModelDesc& m, LoadDecision& d, double clock);
 
     void end_instance(const std::string& model);

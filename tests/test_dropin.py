@@ -1,0 +1,49 @@
+"""Drop-in boundary: the reference's own Simulator (simulator.hpp, unmodified)
+compiled against the B200 bindings in integration/warmsim/ produces
+byte-identical RunMetrics (per-request records, aggregates, KV counters,
+schedule log, allocation log, utilisation series) to the pure-reference build.
+Pools are control-plane-only here (TANGRAM_DEVICE=none): the simulator models
+8 GPUs in one process; the byte-moving path is covered by the GPU tests."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BUILD = os.path.join(ROOT, "integration", "_build")
+
+CONFIGS = [
+    # mode, n_gpus, pool_gib, batch, keep_alive, n_requests, seed, eviction, merge, locality
+    ("reuse_odkv", 8, 48, 4, 2, 2000, 42, 0, 0, "L3"),   # C5
+    ("reuse", 8, 48, 4, 2, 2000, 42, 0, 0, "L3"),
+    ("baseline", 8, 48, 4, 2, 2000, 42, 0, 0, "L3"),
+    ("reuse_odkv", 4, 48, 2, 1, 800, 7, 1, 0, "L1"),     # random eviction (simulator Rng stream)
+    ("reuse", 4, 48, 2, 2, 600, 3, 0, 1, "L2"),          # global merge
+    ("reuse", 8, 48, 1, 2, 600, 3, 0, 1, "L2"),
+    ("baseline", 4, 64, 2, 1, 500, 9, 1, 0, "L1"),
+    ("reuse_odkv", 1, 64, 8, 0.5, 600, 11, 0, 0, "L4"),
+    ("reuse_odkv", 3, 48, 4, 1, 500, 5, 1, 1, "L3"),
+    ("reuse_odkv", 4, 40, 2, 1, 800, 7, 1, 0, "L1"),     # RuntimeInfeasible in both builds
+]
+
+
+@pytest.fixture(scope="module")
+def binaries():
+    if not os.path.isdir("/root/reference/proj/include/warmsim"):
+        if not (os.path.exists(os.path.join(BUILD, "sim_reference")) and
+                os.path.exists(os.path.join(BUILD, "sim_tangram"))):
+            pytest.skip("reference headers absent and drop-in binaries not prebuilt")
+    else:
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "integration")], check=True)
+    return os.path.join(BUILD, "sim_reference"), os.path.join(BUILD, "sim_tangram")
+
+
+@pytest.mark.parametrize("cfg", CONFIGS, ids=[f"{c[0]}-{c[1]}x{c[2]}G-ev{c[7]}-gm{c[8]}-{c[9]}" for c in CONFIGS])
+def test_simulator_runmetrics_identical(binaries, cfg):
+    ref_bin, tg_bin = binaries
+    args = [str(x) for x in cfg]
+    env = dict(os.environ, TANGRAM_DEVICE="none")
+    a = subprocess.run([ref_bin] + args, capture_output=True, check=True, timeout=300).stdout
+    b = subprocess.run([tg_bin] + args, capture_output=True, check=True, timeout=300, env=env).stdout
+    assert a.strip()
+    assert a == b
