@@ -359,14 +359,32 @@ def run_ours(args):
     hbm_peak, peak_src = peaks()
     h2d_peak = measured_h2d_peak(local)
     fp_bytes = sum(t.size for t in target.tensors if t.id not in set(miss_ids))
-    fp_ms = statistics.mean(o.timings["fp_reuse_ms"] for o in outs_v)
+    # K1 roofline from the e2e phase: there the reuse verification competes
+    # only with the 55 GB/s H2D stream (in the value phase it shares HBM with
+    # the concurrent K3 waves and placement copies, see roofline_step)
+    fp_ms = statistics.mean(o.timings["fp_reuse_ms"] for o in outs_e)
+    fp_ms_v = statistics.mean(o.timings["fp_reuse_ms"] for o in outs_v)
     rel_ms = statistics.mean(o.timings["relocate_ms"] for o in outs_v)
     h2d_ms = statistics.mean(o.timings["h2d_ms"] for o in outs_e)
     fp_ach = fp_bytes / (fp_ms / 1e3) / 1e9
     rel_ach = 2 * o_v.bytes_merged / (rel_ms / 1e3) / 1e9
     h2d_ach = o_e.pcie_bytes / (h2d_ms / 1e3) / 1e9
+    step_bytes = 2 * o_v.bytes_merged + 2 * o_v.device_src_bytes + o_v.fingerprint_bytes
+    step_ach = step_bytes / (mv / 1e3) / 1e9
 
     cpu_base = None
+    extras = {}
+    if not args.profile and world == 1:
+        # free the C2 working set before the secondary configs
+        del snap
+        pool.close()
+        for b in cache.values():
+            b.free()
+        for b in host.values():
+            b.free()
+        lib.tg_host_clear()
+        extras["c1"] = run_c1(tg, local)
+        extras["c3"] = run_c3(tg, local)
     if not args.no_cpu_baseline and world == 1 and not args.profile:
         cpu_base = cpu_baseline(args)
 
@@ -405,13 +423,18 @@ def run_ours(args):
             "parallelism": f"{world} independent pools (one per GPU)",
         },
         "latency_ms": {"value_path": mv, "e2e": me, "plan_us": o_v.timings["plan_us"],
-                       "relocate_ms": rel_ms, "h2d_ms": h2d_ms, "fp_reuse_ms": fp_ms,
-                       "fp_kernel_ms_total": o_v.timings["fp_kernel_ms"]},
+                       "relocate_ms": rel_ms, "h2d_ms": h2d_ms, "fp_reuse_ms_e2e": fp_ms,
+                       "fp_reuse_ms_value": fp_ms_v, "fp_kernel_ms_total": o_v.timings["fp_kernel_ms"]},
         "e2e": {"value": world * total / (me / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": me,
                 "h2d_bytes_per_step": o_e.pcie_bytes, "d2h_bytes_per_step": 16 * len(target.tensors)},
-        "roofline": {"bound": "hbm", "kernel": "K1 fp_leaves_kernel (reuse verification launch)",
+        "roofline": {"bound": "hbm", "kernel": "K1 fp_smem_kernel (reuse verification: 2 launches, "
+                                               "untouched + relocated tensors; e2e phase)",
                      "achieved": fp_ach, "peak": hbm_peak, "unit": "GB/s", "frac": fp_ach / hbm_peak,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": fp_bytes, "peak_source": peak_src},
+                     "traffic": traffic, "algorithmic_bytes_per_step": fp_bytes, "peak_source": peak_src},
+        "roofline_step": {"bound": "hbm", "what": "value path: all device bytes of the step (K3 waves r+w, "
+                                                  "K3 placements r+w, K1 reads of all 41 tensors) / step time",
+                          "achieved": step_ach, "peak": hbm_peak, "unit": "GB/s", "frac": step_ach / hbm_peak,
+                          "algorithmic_bytes_per_step": step_bytes},
         "roofline_relocate": {"bound": "hbm", "kernel": "K3 relocate_kernel (3 waves)", "achieved": rel_ach,
                               "peak": hbm_peak, "unit": "GB/s", "frac": rel_ach / hbm_peak,
                               "algorithmic_bytes_per_load": 2 * o_v.bytes_merged},
@@ -423,11 +446,124 @@ def run_ours(args):
     }
     if cpu_base:
         line["cpu_baseline"] = cpu_base
+    if extras:
+        line["secondary_configs"] = extras
     print(json.dumps(line))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def _event_ms(stream_ptr, dev, fn):
+    import torch
+    s = torch.cuda.ExternalStream(stream_ptr, device=dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(s)
+    r = fn()
+    b.record(s)
+    b.synchronize()
+    return a.elapsed_time(b), r
+
+
+def run_c1(tg, dev, reps=3):
+    """C1: OPT-1.3B cold load (PCIe) and 100 % reuse reload (HBM verify)."""
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    m = {x.model_id: x for x in tg.default_catalog()}["opt1.3B"]
+    pool = tg.ReuseStore(tg.GpuSpec("gpu0", 8 * GIB), device=dev)
+    cold, warm, t = [], [], 0.0
+    with HostCheckpoint([m], device=dev):
+        stats = tg.ModelStatsTable()
+        for r in range(reps + 1):
+            stats.record_request(m.model_id, t)
+            ms_c, oc = _event_ms(pool.stream(), dev, lambda: pool.load_model(m, stats, t, details=False).value())
+            pool.end_instance(m.model_id)
+            t += 1.0
+            stats.record_request(m.model_id, t)
+            ms_w, ow = _event_ms(pool.stream(), dev, lambda: pool.load_model(m, stats, t, details=False).value())
+            pool.end_instance(m.model_id)
+            pool.evict_model(m.model_id)
+            t += 1.0
+            if r:  # first round is warm-up
+                cold.append(ms_c)
+                warm.append(ms_w)
+    pool.close()
+    mc, mw = statistics.mean(cold), statistics.mean(warm)
+    return {"workload": "C1 OPT-1.3B (2.6 GB, 25 tensors): cold load from pinned host, then 100% reuse reload "
+                        "(8 GiB pool; placements identical to any larger pool)",
+            "cold_ms": mc, "cold_effective_GBps": m.total_size / mc / 1e6,
+            "cold_h2d_bytes": oc.pcie_bytes, "cold_h2d_ms": oc.timings["h2d_ms"],
+            "warm_ms": mw, "warm_effective_GBps": m.total_size / mw / 1e6,
+            "warm_fingerprint_bytes": ow.fingerprint_bytes, "warm_verify_mismatches": ow.verify_mismatches,
+            "plan_us_cold": oc.timings["plan_us"], "plan_us_warm": ow.timings["plan_us"]}
+
+
+def run_c3(tg, dev):
+    """C3: Llama-2-13B load + on-demand KV block allocation under a prefill
+    burst (16 / 64 ShareGPT prompts, seed 7 — the golden request lists) and one
+    decode-step batch; device block tables; vs the reference KvEngine."""
+    import time
+    import torch
+    from paper_2512_01357_b200 import _native as N
+    from paper_2512_01357_b200.checkpoint import DeviceBuffer
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "c3_kv.json")))
+    model = tg.make_model("llama2-13B", 26_000_000_000, 40, 819_200)
+    bufs = []
+    for t in model.tensors:
+        b = DeviceBuffer(t.size, dev)
+        N.lib.tg_synth_fill_device(t.id.c(), 0, t.size, C.c_void_p(b.ptr), dev)
+        N.lib.tg_host_register(t.id.c(), C.c_void_p(b.ptr), t.size, None)
+        bufs.append(b)
+    pool = tg.ReuseStore(tg.GpuSpec("gpu0", 120 * GIB), device=dev)
+    stats = tg.ModelStatsTable()
+    stats.record_request(model.model_id, 0.0)
+    pool.load_model(model, stats, 0.0).value()
+    for b in bufs:
+        b.free()
+    N.lib.tg_host_clear()
+    out = {}
+    try:
+        from oracle import ref
+        have_ref = ref.available()
+    except Exception:
+        have_ref = False
+    for n, case in golden.items():
+        reqs = [tuple(r) for r in case["requests"]]
+        dec = [(r, (p + 15) // 16 * 16 + 1) for r, p in reqs]
+        kv = tg.KvEngine("llama2-13B", 16, 819_200)
+        kv.batch_allocate(pool, stats, reqs, want_pbns=False)  # warm-up (device arrays sized)
+        kv.instance_teardown(pool)
+        best_b, best_d, counts = 1e9, 1e9, None
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            counts = kv.batch_allocate(pool, stats, reqs, want_pbns=False).value()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            kv.batch_allocate(pool, stats, dec, want_pbns=False).value()
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            best_b, best_d = min(best_b, t1 - t0), min(best_d, t2 - t1)
+            kv.instance_teardown(pool)
+        blocks = sum(counts)
+        row = {"requests": len(reqs), "blocks": blocks, "blocks_match_reference": blocks == sum(
+                   len(g) for g in case["burst"]),
+               "burst_us": best_b * 1e6, "decode_step_us": best_d * 1e6, "blocks_per_us": blocks / (best_b * 1e6)}
+        if have_ref:
+            r = ref.ReuseStore(120 * GIB)
+            rs = ref.ModelStatsTable()
+            rs.record_request(model.model_id, 0.0)
+            r.load_model(model.to_json(), rs, 0.0)
+            rk = ref.KvEngine("llama2-13B", 16, 819_200)
+            rb = rk.batch_allocate(r, rs, reqs)
+            rd = rk.batch_allocate(r, rs, dec)
+            row["reference_cpu_burst_us"] = rb["ns"] / 1e3
+            row["reference_cpu_decode_step_us"] = rd["ns"] / 1e3
+        out[n] = row
+    pool.close()
+    return {"workload": "C3 Llama-2-13B (26 GB) in a 120 GiB pool; KV blocks of 16 tokens x 819,200 B/token; "
+                        "host+device time per batch incl. kernel completion, best of 3", "bursts": out}
 
 
 def check_parity(tg, pool, target, host, cache, dev):

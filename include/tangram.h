@@ -105,7 +105,7 @@ typedef struct {
     /* data plane (device pools) */
     uint64_t pcie_bytes, peer_bytes, device_src_bytes, fingerprint_bytes, repaired_bytes;
     uint32_t verify_mismatches, expected_mismatches;
-    double plan_us, total_ms, relocate_ms, h2d_ms, peer_ms, fp_kernel_ms, fp_reuse_ms;
+    double plan_us, total_ms, relocate_ms, h2d_ms, peer_ms, fp_kernel_ms, fp_reuse_ms, fp_reuse_max_ms;
 } tg_load_outcome;
 
 /* warmsim::EvictionCandidate (packing.hpp:32-38); model_id valid until the next call on the pool */
@@ -251,6 +251,10 @@ int tg_host_free(void* p);
 /* ---- raw device helpers ------------------------------------------------------ */
 int tg_fingerprint_device(const void* dptr, uint64_t n, int32_t device, tg_digest* out); /* K1 */
 int tg_synth_fill_device(tg_tensor_id id, uint64_t begin, uint64_t len, void* dptr, int32_t device);
+/* kernel-only microbenchmarks: reps launches timed with CUDA events on the launching stream */
+int tg_bench_fingerprint(const void* dptr, uint64_t n, int32_t device, int32_t reps, double* ms_per_launch,
+                         tg_digest* out);
+int tg_bench_relocate(void* dst, const void* src, uint64_t n, int32_t device, int32_t reps, double* ms_per_launch);
 int tg_synth_fill_host(tg_tensor_id id, uint64_t begin, uint64_t len, void* dst, int32_t threads);
 int tg_device_alloc(int32_t device, uint64_t size, void** out);
 int tg_device_free(int32_t device, void* p);

@@ -56,7 +56,7 @@ class LoadOutcomeC(C.Structure):
                 ("pcie_bytes", u64), ("peer_bytes", u64), ("device_src_bytes", u64), ("fingerprint_bytes", u64), ("repaired_bytes", u64),
                 ("verify_mismatches", u32), ("expected_mismatches", u32),
                 ("plan_us", dbl), ("total_ms", dbl), ("relocate_ms", dbl), ("h2d_ms", dbl), ("peer_ms", dbl),
-                ("fp_kernel_ms", dbl), ("fp_reuse_ms", dbl)]
+                ("fp_kernel_ms", dbl), ("fp_reuse_ms", dbl), ("fp_reuse_max_ms", dbl)]
 
 
 class EvictionC(C.Structure):
@@ -161,6 +161,8 @@ _SIGS = {
     "tg_host_free": (C.c_int, [vp]),
     "tg_fingerprint_device": (C.c_int, [vp, u64, i32, P(DigestC)]),
     "tg_synth_fill_device": (C.c_int, [TensorIdC, u64, u64, vp, i32]),
+    "tg_bench_fingerprint": (C.c_int, [vp, u64, i32, i32, P(dbl), P(DigestC)]),
+    "tg_bench_relocate": (C.c_int, [vp, vp, u64, i32, i32, P(dbl)]),
     "tg_synth_fill_host": (C.c_int, [TensorIdC, u64, u64, vp, i32]),
     "tg_device_alloc": (C.c_int, [i32, u64, P(vp)]),
     "tg_device_free": (C.c_int, [i32, vp]),

@@ -30,7 +30,7 @@ __device__ __forceinline__ u64 pack64(u32 lo, u32 hi) { return (static_cast<u64>
 // Hash `nblk` 16-byte blocks starting `4*Q + r8/8` bytes past the aligned
 // word pointer `wp`.
 template <int Q>
-__device__ __forceinline__ void hash_blocks(const uint4* __restrict__ wp, u32 nblk, u32 r8, u64& h1, u64& h2) {
+__device__ __forceinline__ void hash_blocks(const uint4* __restrict__ wp, u32 nblk, u32 r8, mm::W32& h1, mm::W32& h2) {
     uint4 w0 = __ldg(wp);
 #pragma unroll 4
     for (u32 j = 0; j < nblk; ++j) {
@@ -40,22 +40,22 @@ __device__ __forceinline__ void hash_blocks(const uint4* __restrict__ wp, u32 nb
         const u32 b = __funnelshift_r(u[Q + 1], u[Q + 2], r8);
         const u32 c = __funnelshift_r(u[Q + 2], u[Q + 3], r8);
         const u32 d = __funnelshift_r(u[Q + 3], u[Q + 4], r8);
-        mm::body(h1, h2, pack64(a, b), pack64(c, d));
+        mm::body_dev(h1, h2, mm::W32{a, b}, mm::W32{c, d});
         w0 = w1;
     }
 }
 
-__device__ __forceinline__ void hash_blocks_aligned(const uint4* __restrict__ wp, u32 nblk, u64& h1, u64& h2) {
+__device__ __forceinline__ void hash_blocks_aligned(const uint4* __restrict__ wp, u32 nblk, mm::W32& h1, mm::W32& h2) {
 #pragma unroll 4
     for (u32 j = 0; j < nblk; ++j) {
         const uint4 w = __ldg(wp + j);
-        mm::body(h1, h2, pack64(w.x, w.y), pack64(w.z, w.w));
+        mm::body_dev(h1, h2, mm::W32{w.x, w.y}, mm::W32{w.z, w.w});
     }
 }
 
 // murmur3_x64_128(p[0..len), seed) for len <= 4096.
 __device__ void leaf_digest(const std::uint8_t* p, u32 len, u64 seed, u64& d1, u64& d2) {
-    u64 h1 = seed, h2 = seed;
+    mm::W32 h1 = mm::w_of(seed), h2 = h1;
     const u32 nblk = len >> 4;
     const u32 o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p) & 15);
     const uint4* wp = reinterpret_cast<const uint4*>(p - o);
@@ -79,9 +79,10 @@ __device__ void leaf_digest(const std::uint8_t* p, u32 len, u64 seed, u64& d1, u
         if (b < 8) t1 |= v << (8 * b);
         else t2 |= v << (8 * (b - 8));
     }
-    mm::finish(h1, h2, t1, t2, rem, len);
-    d1 = h1;
-    d2 = h2;
+    u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
+    mm::finish(f1, f2, t1, t2, rem, len);
+    d1 = f1;
+    d2 = f2;
 }
 
 __device__ __forceinline__ u64 warp_sum(u64 v) {
@@ -181,7 +182,7 @@ __device__ __forceinline__ void issue_stage(uint4* buf, const std::uint8_t* a0, 
 }
 
 template <int Q>
-__device__ __forceinline__ void hash_stage(const uint4* slot, u32 r8, u64& h1, u64& h2) {
+__device__ __forceinline__ void hash_stage(const uint4* slot, u32 r8, mm::W32& h1, mm::W32& h2) {
     uint4 w[kSlotWords];
 #pragma unroll
     for (int q = 0; q < kSlotWords; ++q) w[q] = slot[q];
@@ -192,13 +193,13 @@ __device__ __forceinline__ void hash_stage(const uint4* slot, u32 r8, u64& h1, u
         const u32 c = __funnelshift_r(u[Q + 1], u[Q + 2], r8);
         const u32 d = __funnelshift_r(u[Q + 2], u[Q + 3], r8);
         const u32 e = __funnelshift_r(u[Q + 3], u[Q + 4], r8);
-        mm::body(h1, h2, pack64(a, c), pack64(d, e));
+        mm::body_dev(h1, h2, mm::W32{a, c}, mm::W32{d, e});
     }
 }
 
 template <int Q>
 __device__ __forceinline__ void hash_full_leaves(uint4* wbuf, const std::uint8_t* a0, u32 nfull, bool extra, u32 r8,
-                                                 u32 lane, u64& h1, u64& h2) {
+                                                 u32 lane, mm::W32& h1, mm::W32& h2) {
     constexpr int kStride = 32 * kSlotWords;
 #pragma unroll
     for (int s = 0; s < kStages - 1; ++s) issue_stage(wbuf + s * kStride, a0, nfull, extra, s, lane);
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
         const u32 o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p0) & 15);
         const std::uint8_t* a0 = p0 - o;
         const u64 my_leaf = leaf0 + lane;
-        u64 h1 = my_leaf, h2 = my_leaf;
+        mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
         if (nfull) {
             const u32 r8 = (o & 3) * 8;
             const bool extra = o != 0;
@@ -261,9 +262,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
             }
         }
         if (lane < nfull) {
-            mm::finish(h1, h2, 0, 0, 0, kLeafBytes);
-            acc_h += h1;
-            acc_l += h2;
+            u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
+            mm::finish(f1, f2, 0, 0, 0, kLeafBytes);
+            acc_h += f1;
+            acc_l += f2;
         } else if (lane == nfull && my_leaf * kLeafBytes < tk.n) {
             // the tensor's trailing partial leaf, hashed straight from global
             const u32 len = static_cast<u32>(tk.n - my_leaf * kLeafBytes);

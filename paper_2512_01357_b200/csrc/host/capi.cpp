@@ -338,6 +338,7 @@ int tg_load_model(tg_pool* p, const tg_model_spec* ms, const tg_stats* s, double
             out->peer_ms = r.t.peer_ms;
             out->fp_kernel_ms = r.t.fp_kernel_ms;
             out->fp_reuse_ms = r.t.fp_reuse_ms;
+            out->fp_reuse_max_ms = r.t.fp_reuse_max_ms;
         }
         return 0;
     });
@@ -551,6 +552,20 @@ int tg_fingerprint_device(const void* dptr, uint64_t n, int32_t device, tg_diges
         Digest d;
         fingerprint_device(dptr, n, device, &d);
         *out = tg_digest{d.hi, d.lo};
+        return 0;
+    });
+}
+int tg_bench_fingerprint(const void* dptr, uint64_t n, int32_t device, int32_t reps, double* ms, tg_digest* out) {
+    return guard([&] {
+        Digest d;
+        *ms = bench_fingerprint(dptr, n, device, reps < 1 ? 1 : reps, &d);
+        if (out) *out = tg_digest{d.hi, d.lo};
+        return 0;
+    });
+}
+int tg_bench_relocate(void* dst, const void* src, uint64_t n, int32_t device, int32_t reps, double* ms) {
+    return guard([&] {
+        *ms = bench_relocate(dst, src, n, device, reps < 1 ? 1 : reps);
         return 0;
     });
 }

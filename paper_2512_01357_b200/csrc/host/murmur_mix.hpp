@@ -37,6 +37,46 @@ TG_HD void body(std::uint64_t& h1, std::uint64_t& h2, std::uint64_t k1, std::uin
     h2 = (rol(h2, 31) + h1) * 5 + 0x38495ab5;
 }
 
+#if defined(__CUDACC__)
+// Device form of body(): the same arithmetic spelled on 32-bit halves so that
+// ptxas emits what the SM executes natively — a 64x64 low multiply by a
+// constant as IMAD.WIDE.U32 + 2 IMAD, a 64-bit rotate as 2 funnel shifts
+// (SHF), h*5+c as IMAD.WIDE.U32 with a 64-bit addend + IMAD.  The generic u64
+// spelling compiles to ~65 instructions per 16-byte block on sm_100a (rotates
+// become 4-instruction shift/or chains); this one to ~36.
+struct W32 {
+    std::uint32_t l, h;
+};
+__device__ __forceinline__ W32 w_of(std::uint64_t x) { return W32{static_cast<std::uint32_t>(x), static_cast<std::uint32_t>(x >> 32)}; }
+__device__ __forceinline__ std::uint64_t u_of(W32 a) { return (static_cast<std::uint64_t>(a.h) << 32) | a.l; }
+template <std::uint64_t C>
+__device__ __forceinline__ W32 mulc(W32 a) {
+    constexpr std::uint32_t cl = static_cast<std::uint32_t>(C), ch = static_cast<std::uint32_t>(C >> 32);
+    const std::uint64_t p = static_cast<std::uint64_t>(a.l) * cl;
+    return W32{static_cast<std::uint32_t>(p), static_cast<std::uint32_t>(p >> 32) + a.l * ch + a.h * cl};
+}
+template <int R>  // 0 < R < 32
+__device__ __forceinline__ W32 rol32(W32 a) {
+    return W32{__funnelshift_l(a.h, a.l, R), __funnelshift_l(a.l, a.h, R)};
+}
+__device__ __forceinline__ W32 rol33(W32 a) { return W32{__funnelshift_l(a.l, a.h, 1), __funnelshift_l(a.h, a.l, 1)}; }
+template <std::uint32_t C>
+__device__ __forceinline__ W32 mul5_add(W32 a) {
+    const std::uint64_t t = static_cast<std::uint64_t>(a.l) * 5u + C;
+    return W32{static_cast<std::uint32_t>(t), static_cast<std::uint32_t>(t >> 32) + a.h * 5u};
+}
+__device__ __forceinline__ W32 add64(W32 a, W32 b) { return w_of(u_of(a) + u_of(b)); }
+__device__ __forceinline__ W32 xor64(W32 a, W32 b) { return W32{a.l ^ b.l, a.h ^ b.h}; }
+
+// body() on halves; k1 = (k1l, k1h), k2 = (k2l, k2h).
+__device__ __forceinline__ void body_dev(W32& h1, W32& h2, W32 k1, W32 k2) {
+    k1 = mulc<kC2>(rol32<31>(mulc<kC1>(k1)));
+    h1 = mul5_add<0x52dce729u>(add64(rol32<27>(xor64(h1, k1)), h2));
+    k2 = mulc<kC1>(rol33(mulc<kC2>(k2)));
+    h2 = mul5_add<0x38495ab5u>(add64(rol32<31>(xor64(h2, k2)), h1));
+}
+#endif
+
 // Tail (len % 16 bytes packed little-endian into t1 | t2) and finalisation.
 TG_HD void finish(std::uint64_t& h1, std::uint64_t& h2, std::uint64_t t1, std::uint64_t t2, unsigned rem,
                   std::uint64_t len) {

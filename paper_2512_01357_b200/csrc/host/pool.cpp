@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <unordered_set>
 
 #include "../device/common.cuh"
 #include "../device/kernels.hpp"
@@ -42,7 +43,7 @@ Pool::Pool(GpuDesc gpu, int device) : store_(std::move(gpu)), device_(device) {
     // +256 B slack: aligned 16-byte word reads at a tensor's last byte may
     // touch the following word.
     TG_CUDA(cudaMalloc(reinterpret_cast<void**>(&arena_), store_.pool_size() + 256));
-    for (cudaStream_t* s : {&s_main_, &s_copy_, &s_fp_, &s_peer_})
+    for (cudaStream_t* s : {&s_main_, &s_copy_, &s_fp_, &s_peer_, &s_verify_})
         TG_CUDA(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
 }
 
@@ -51,7 +52,7 @@ Pool::~Pool() {
     DeviceScope ds(device_);
     cudaDeviceSynchronize();
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
-    for (cudaStream_t s : {s_main_, s_copy_, s_fp_, s_peer_})
+    for (cudaStream_t s : {s_main_, s_copy_, s_fp_, s_peer_, s_verify_})
         if (s) cudaStreamDestroy(s);
     if (arena_) cudaFree(arena_);
     if (d_stage_) cudaFree(d_stage_);
@@ -110,7 +111,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     std::unique_ptr<DeviceScope> ds;
     if (has_device()) {
         ds = std::make_unique<DeviceScope>(device_);
-        ensure_events(8);
+        ensure_events(9);
         TG_CUDA(cudaEventRecord(ev(0), s_main_));  // t0: entry
     }
     const auto h0 = clk::now();
@@ -186,11 +187,22 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
 
     // ---- event layout -----------------------------------------------------------
     // 0 t0 | 1 reloc start | 2 reloc end | 3 end | 4 h2d start | 5 h2d end | 6 peer start | 7 peer end
-    // 8.. wave ends (waves) | then per placement "bytes landed" | then fp start/end pairs
-    const std::size_t ev_wave = 8, ev_land = ev_wave + waves, ev_fp = ev_land + np;
+    // 8 verify joined | 9.. wave ends (waves) | then per placement "bytes landed" | then fp start/end pairs
+    const std::size_t ev_wave = 9, ev_land = ev_wave + waves, ev_fp = ev_land + np;
     const bool fp_new = flags & kLoadFingerprintNew, fp_reuse = (flags & kLoadVerifyReuse) && !hit_keys.empty();
-    const std::size_t n_fp_launch = (fp_new ? np : 0) + (fp_reuse ? 1 : 0);
+    const std::size_t n_fp_launch = (fp_new ? np : 0) + (fp_reuse ? 2 : 0);
     ensure_events(ev_fp + 2 * n_fp_launch);
+    // Reused tensors that no relocation touches are verified right away, in
+    // parallel with the waves; relocated ones after the waves at their new
+    // offsets.  hit_keys is reordered [untouched..., relocated...].
+    std::size_t n_still = 0;
+    if (fp_reuse) {
+        std::unordered_set<Key, KeyHash> moved;
+        for (const Move& r : rel) moved.insert(r.tensor);
+        auto mid = std::stable_partition(hit_keys.begin(), hit_keys.end(),
+                                         [&](const Key& k) { return !moved.count(k); });
+        n_still = static_cast<std::size_t>(mid - hit_keys.begin());
+    }
 
     // ---- fingerprint task table (one H2D of descriptors) -------------------------
     // tasks: [placements (one launch each)] [hits (one launch)]
@@ -205,7 +217,11 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             const Entry* e = store_.entry(k);
             hit_tasks.push_back(FpTask{arena_ + e->off, e->size, 0});
         }
-    const u64 hit_tiles = build_tasks(hit_tasks);
+    std::vector<FpTask> still(hit_tasks.begin(), hit_tasks.begin() + static_cast<long>(n_still));
+    std::vector<FpTask> moved_hits(hit_tasks.begin() + static_cast<long>(n_still), hit_tasks.end());
+    const u64 still_tiles = build_tasks(still), moved_tiles = build_tasks(moved_hits);
+    std::copy(still.begin(), still.end(), hit_tasks.begin());
+    std::copy(moved_hits.begin(), moved_hits.end(), hit_tasks.begin() + static_cast<long>(n_still));
     std::vector<u64> new_tiles(tasks.size());
     for (std::size_t i = 0; i < tasks.size(); ++i) {
         std::vector<FpTask> one{tasks[i]};
@@ -285,17 +301,27 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             ++fp_i;
         }
     }
-    // ---- K1 over reused tensors at their final offsets (after the waves) ------------
-    std::size_t fp_reuse_slot = 0;
+    // ---- K1 over reused tensors: untouched ones now (verify stream), relocated
+    // ones at their final offsets after the waves (main stream) -------------------
+    std::size_t fp_reuse_slot = 0, fp_reuse_launches = 0;
     if (fp_reuse) {
         fp_reuse_slot = fp_i;
         const std::size_t base = tasks.size();
-        TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s_main_));
-        fp_launch(d_tasks + base, static_cast<u32>(hit_tasks.size()), hit_tiles, d_sums + 2 * base, d_dig + 2 * base,
-                  sm_count_, s_main_);
-        TG_CUDA(cudaGetLastError());
-        TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s_main_));
-        ++fp_i;
+        auto launch = [&](cudaStream_t s, std::size_t first, std::size_t count, u64 tiles) {
+            if (!count) return;
+            TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s));
+            fp_launch(d_tasks + base + first, static_cast<u32>(count), tiles, d_sums + 2 * (base + first),
+                      d_dig + 2 * (base + first), sm_count_, s);
+            TG_CUDA(cudaGetLastError());
+            TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s));
+            ++fp_i;
+            ++fp_reuse_launches;
+        };
+        TG_CUDA(cudaStreamWaitEvent(s_verify_, ev(1)));  // descriptors uploaded, sums zeroed
+        launch(s_verify_, 0, n_still, still_tiles);
+        launch(s_main_, n_still, hit_tasks.size() - n_still, moved_tiles);
+        TG_CUDA(cudaEventRecord(ev(8), s_verify_));
+        TG_CUDA(cudaStreamWaitEvent(s_main_, ev(8)));
     }
     // ---- join, read digests, end ------------------------------------------------
     TG_CUDA(cudaStreamWaitEvent(s_main_, ev(5)));
@@ -316,7 +342,10 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     for (std::size_t f = 0; f < fp_i; ++f) {
         const double t = ms_between(ev(ev_fp + 2 * f), ev(ev_fp + 2 * f + 1));
         rep->t.fp_kernel_ms += t;
-        if (fp_reuse && f == fp_reuse_slot) rep->t.fp_reuse_ms = t;
+        if (fp_reuse && f >= fp_reuse_slot && f < fp_reuse_slot + fp_reuse_launches) {
+            rep->t.fp_reuse_ms += t;
+            rep->t.fp_reuse_max_ms = std::max(rep->t.fp_reuse_max_ms, t);
+        }
     }
 
     // ---- record / verify digests ----------------------------------------------
@@ -466,6 +495,69 @@ void fingerprint_device(const void* ptr, u64 n, int device, Digest* out) {
     TG_CUDA(cudaStreamSynchronize(s));
     TG_CUDA(cudaStreamDestroy(s));
     *out = Digest{h[0], h[1]};
+}
+
+// Kernel-only timing of K1 / K3 for microbenchmarks: setup outside the timed
+// region, `reps` back-to-back launches bracketed by CUDA events on the
+// launching stream.  Returns the mean ms per launch.
+double bench_fingerprint(const void* ptr, u64 n, int device, int reps, Digest* out) {
+    DeviceScope ds(device);
+    int sms = 148;
+    TG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    std::vector<FpTask> t{FpTask{static_cast<const std::uint8_t*>(ptr), n, 0}};
+    const u64 tiles = build_tasks(t);
+    cudaStream_t s;
+    TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    void* d = nullptr;
+    const std::size_t per = 4 * sizeof(u64);
+    TG_CUDA(cudaMalloc(&d, sizeof(FpTask) + per * (reps + 1)));
+    TG_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(FpTask), cudaMemcpyHostToDevice, s));
+    auto* sums = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(d) + sizeof(FpTask));
+    TG_CUDA(cudaMemsetAsync(sums, 0, per * (reps + 1), s));
+    fp_launch(static_cast<const FpTask*>(d), 1, tiles, sums, sums + 2, sms, s);  // warm-up
+    cudaEvent_t a, b;
+    TG_CUDA(cudaEventCreate(&a));
+    TG_CUDA(cudaEventCreate(&b));
+    TG_CUDA(cudaEventRecord(a, s));
+    for (int r = 1; r <= reps; ++r)
+        fp_launch(static_cast<const FpTask*>(d), 1, tiles, sums + 4 * r, sums + 4 * r + 2, sms, s);
+    TG_CUDA(cudaEventRecord(b, s));
+    TG_CUDA(cudaGetLastError());
+    u64 h[2];
+    TG_CUDA(cudaMemcpyAsync(h, sums + 4 * reps + 2, sizeof h, cudaMemcpyDeviceToHost, s));
+    TG_CUDA(cudaStreamSynchronize(s));
+    float ms = 0;
+    TG_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d);
+    cudaStreamDestroy(s);
+    if (out) *out = Digest{h[0], h[1]};
+    return ms / reps;
+}
+
+double bench_relocate(void* dst, const void* src, u64 n, int device, int reps) {
+    DeviceScope ds(device);
+    int sms = 148;
+    TG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    cudaStream_t s;
+    TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    MoveDesc md{reinterpret_cast<u64>(src), reinterpret_cast<u64>(dst), n};
+    relocate_launch(&md, 1, sms, s);  // warm-up
+    cudaEvent_t a, b;
+    TG_CUDA(cudaEventCreate(&a));
+    TG_CUDA(cudaEventCreate(&b));
+    TG_CUDA(cudaEventRecord(a, s));
+    for (int r = 0; r < reps; ++r) relocate_launch(&md, 1, sms, s);
+    TG_CUDA(cudaEventRecord(b, s));
+    TG_CUDA(cudaGetLastError());
+    TG_CUDA(cudaStreamSynchronize(s));
+    float ms = 0;
+    TG_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaStreamDestroy(s);
+    return ms / reps;
 }
 
 void synth_fill_device(const Key& k, u64 begin, u64 len, void* dst, int device) {

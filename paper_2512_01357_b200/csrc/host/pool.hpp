@@ -62,7 +62,8 @@ struct LoadTimings {
     double h2d_ms = 0;           // first .. last host→device copy
     double peer_ms = 0;          // peer pulls
     double fp_kernel_ms = 0;     // Σ K1 launch durations
-    double fp_reuse_ms = 0;      // K1 over reused tensors
+    double fp_reuse_ms = 0;      // Σ K1 launch durations over reused tensors (≤ 2 launches)
+    double fp_reuse_max_ms = 0;  // the longer of the two
 };
 
 struct LoadReport {
@@ -116,7 +117,7 @@ private:
     int device_ = -1;
     int sm_count_ = 148;
     std::uint8_t* arena_ = nullptr;
-    cudaStream_t s_main_ = nullptr, s_copy_ = nullptr, s_fp_ = nullptr, s_peer_ = nullptr;
+    cudaStream_t s_main_ = nullptr, s_copy_ = nullptr, s_fp_ = nullptr, s_peer_ = nullptr, s_verify_ = nullptr;
     std::vector<cudaEvent_t> events_;
     std::vector<Pool*> peers_;
     // staging
@@ -129,5 +130,7 @@ private:
 std::unique_ptr<KvDevice> make_kv_device(int device, cudaStream_t stream);
 void fingerprint_device(const void* ptr, u64 n, int device, Digest* out);
 void synth_fill_device(const Key& k, u64 begin, u64 len, void* dst, int device);
+double bench_fingerprint(const void* ptr, u64 n, int device, int reps, Digest* out);
+double bench_relocate(void* dst, const void* src, u64 n, int device, int reps);
 
 }  // namespace tg
