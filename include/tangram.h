@@ -146,6 +146,10 @@ typedef struct {
     uint64_t region_count, extent_count, tensor_count, largest_free;
     int32_t device;
     void* arena;
+    /* data plane totals since creation (device pools) */
+    uint64_t loads;
+    double data_plane_ms;
+    uint64_t pcie_bytes, peer_bytes, device_src_bytes, fingerprint_bytes, relocated_bytes;
 } tg_pool_info;
 
 typedef struct {

@@ -45,6 +45,24 @@ int main(int argc, char** argv) {
     cfg.emit_alloc_log = true;
     cfg.emit_sched_log = true;
     cfg.emit_timeseries = true;
+#ifdef TANGRAM_BINDING
+    // Byte sources for every catalog tensor, synthesised in HBM on device 0
+    // (TANGRAM_SYNTH_SOURCES=1): pools that own a device then move real bytes.
+    std::vector<void*> sources;
+    if (std::getenv("TANGRAM_SYNTH_SOURCES")) {
+        for (const auto& model : catalog)
+            for (const auto& t : model.tensors) {
+                void* d = nullptr;
+                const tg_tensor_id id{t.id.hi, t.id.lo};
+                if (tg_device_alloc(0, t.size, &d) || tg_synth_fill_device(id, 0, t.size, d, 0) ||
+                    tg_host_register(id, d, t.size, nullptr)) {
+                    std::fprintf(stderr, "source setup failed: %s\n", tg_last_error_detail());
+                    return 3;
+                }
+                sources.push_back(d);
+            }
+    }
+#endif
     RunMetrics m;
     try {
         Simulator sim(cfg, catalog);
@@ -53,6 +71,16 @@ int main(int argc, char** argv) {
         std::cout << nlohmann::json{{"exception", e.what()}}.dump() << "\n";
         return 0;
     }
+#ifdef TANGRAM_BINDING
+    // data-plane totals per pool (stderr, so stdout stays comparable)
+    auto pools = nlohmann::json::array();
+    for (const auto& [gid, i] : tgb::finished_pools())
+        pools.push_back({{"gpu_id", gid}, {"device", i.device}, {"loads", i.loads}, {"data_plane_ms", i.data_plane_ms},
+                         {"pcie_bytes", i.pcie_bytes}, {"device_src_bytes", i.device_src_bytes},
+                         {"fingerprint_bytes", i.fingerprint_bytes}, {"relocated_bytes", i.relocated_bytes}});
+    std::cerr << nlohmann::json{{"pools", pools}}.dump() << "\n";
+    for (void* d : sources) tg_device_free(0, d);
+#endif
     nlohmann::json j;
     auto recs = nlohmann::json::array();
     for (const auto& r : m.records)

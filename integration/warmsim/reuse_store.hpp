@@ -117,8 +117,21 @@ inline int pick_device(const std::string& gpu_id) {
     return d < n ? d : TG_POOL_NO_DEVICE;
 }
 
+// Data-plane totals of every pool, collected when the pool is released, so a
+// driver can report what the bytes cost after the reference code is done.
+inline std::vector<std::pair<std::string, tg_pool_info>>& finished_pools() {
+    static std::vector<std::pair<std::string, tg_pool_info>> v;
+    return v;
+}
+
 struct PoolDeleter {
-    void operator()(tg_pool* p) const { tg_pool_destroy(p); }
+    std::string gpu_id;
+    void operator()(tg_pool* p) const {
+        tg_pool_info i{};
+        tg_pool_info_get(p, &i);
+        finished_pools().push_back({gpu_id, i});
+        tg_pool_destroy(p);
+    }
 };
 
 }  // namespace tgb
@@ -132,7 +145,7 @@ public:
                       gpu_.store_bandwidth};
         tg_pool* p = nullptr;
         if (int rc = tg_pool_create(&g, tgb::pick_device(gpu_.gpu_id), &p)) tgb::fail(rc, "tg_pool_create");
-        pool_.reset(p, tgb::PoolDeleter{});
+        pool_.reset(p, tgb::PoolDeleter{gpu_.gpu_id});
     }
 
     tg_pool* handle() const { return pool_.get(); }

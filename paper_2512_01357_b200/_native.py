@@ -80,7 +80,8 @@ class PoolInfoC(C.Structure):
                 ("pinned_bytes", u64), ("reusable_bytes", u64), ("bytes_merged_total", u64),
                 ("bytes_transferred_total", u64), ("evictions_total", u64), ("region_count", u64),
                 ("extent_count", u64), ("tensor_count", u64), ("largest_free", u64), ("device", i32),
-                ("arena", vp)]
+                ("arena", vp), ("loads", u64), ("data_plane_ms", dbl), ("pcie_bytes", u64), ("peer_bytes", u64),
+                ("device_src_bytes", u64), ("fingerprint_bytes", u64), ("relocated_bytes", u64)]
 
 
 class TensorInfoC(C.Structure):

@@ -284,6 +284,430 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
     }
 }
 
+// ---- v2: TMA bulk-copy staged leaves ------------------------------------------
+// Same smem layout as v1, but each lane stages its own leaf's 144-byte window
+// with ONE cp.async.bulk (TMA) per stage, completing on a per-warp, per-stage
+// mbarrier.  v1 spent ~25 of its ~64 instructions per 16-byte block on
+// LDGSTS address arithmetic (f/9, f%9, 64-bit adds, predicates); here the
+// producer side costs ~1 instruction per block and the kernel is left with
+// the hash itself.
+constexpr int kTmaStages = 3;
+constexpr int kTmaWarpWords = kTmaStages * 32 * kSlotWords;
+constexpr int kTmaSmemBytes = kWarpsPerCta * (kTmaWarpWords * 16 + kTmaStages * 8);
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void tma_stage(unsigned slot_smem, const std::uint8_t* src, unsigned bytes,
+                                          unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(slot_smem),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void bar_expect(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bar_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+template <int Q>
+__device__ __forceinline__ void hash_full_leaves_tma(uint4* wbuf, unsigned bars, unsigned* phase,
+                                                     const std::uint8_t* a0, u32 nfull, bool extra, u32 r8, u32 lane,
+                                                     mm::W32& h1, mm::W32& h2) {
+    constexpr int kStride = 32 * kSlotWords;  // words per stage buffer
+    const unsigned per_leaf = extra ? 144u : 128u;
+    const unsigned stage_bytes = per_leaf * nfull;
+    const unsigned my_slot = smem_u32(wbuf + lane * kSlotWords);
+    const std::uint8_t* my_src = a0 + static_cast<u64>(lane) * kLeafBytes;
+    auto issue = [&](int s) {
+        const int b = s % kTmaStages;
+        const unsigned bar = bars + 8u * b;
+        if (lane == 0) bar_expect(bar, stage_bytes);
+        __syncwarp();
+        if (lane < nfull) tma_stage(my_slot + b * kStride * 16, my_src + s * 128, per_leaf, bar);
+    };
+#pragma unroll
+    for (int s = 0; s < kTmaStages - 1; ++s) issue(s);
+    for (int s = 0; s < kStagesPerLeaf; ++s) {
+        const int nxt = s + kTmaStages - 1;
+        if (nxt < kStagesPerLeaf) issue(nxt);
+        const int b = s % kTmaStages;
+        bar_wait(bars + 8u * b, (*phase >> b) & 1u);
+        *phase ^= 1u << b;
+        if (lane < nfull) hash_stage<Q>(wbuf + b * kStride + lane * kSlotWords, r8, h1, h2);
+        // the slot is refilled by the async proxy in a later stage: order our
+        // generic-proxy reads before it
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
+    fp_tma_kernel(const FpTask* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums) {
+    extern __shared__ __align__(128) uint4 smem[];
+    const u32 lane = threadIdx.x & 31;
+    const u32 wid = threadIdx.x >> 5;
+    uint4* wbuf = smem + wid * kTmaWarpWords;
+    auto* bar_base = reinterpret_cast<unsigned long long*>(smem + kWarpsPerCta * kTmaWarpWords) + wid * kTmaStages;
+    const unsigned bars = smem_u32(bar_base);
+    if (lane == 0) {
+        for (int b = 0; b < kTmaStages; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bars + 8u * b) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+    unsigned phase = 0;
+    const u64 nwarps = static_cast<u64>(gridDim.x) * kWarpsPerCta;
+    int cur = -1;
+    u64 acc_h = 0, acc_l = 0;
+    for (u64 t = static_cast<u64>(blockIdx.x) * kWarpsPerCta + wid; t < total_tiles; t += nwarps) {
+        u32 lo = 0, hi = n_tasks - 1;
+        while (lo < hi) {
+            const u32 mid = (lo + hi + 1) >> 1;
+            if (tasks[mid].tile0 <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        const int ti = static_cast<int>(lo);
+        if (ti != cur) {
+            if (cur >= 0) {
+                const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
+                if (lane == 0) {
+                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
+                }
+            }
+            cur = ti;
+            acc_h = acc_l = 0;
+        }
+        const FpTask tk = tasks[ti];
+        const u64 leaf0 = (t - tk.tile0) * kLeavesPerTile;
+        const u64 full_leaves = tk.n / kLeafBytes;
+        const u32 nfull = full_leaves > leaf0 ? static_cast<u32>(min(full_leaves - leaf0, u64{32})) : 0u;
+        const std::uint8_t* p0 = tk.base + leaf0 * kLeafBytes;
+        const u32 o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p0) & 15);
+        const std::uint8_t* a0 = p0 - o;
+        const u64 my_leaf = leaf0 + lane;
+        mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
+        if (nfull) {
+            const u32 r8 = (o & 3) * 8;
+            const bool extra = o != 0;
+            switch (o >> 2) {
+                case 0: hash_full_leaves_tma<0>(wbuf, bars, &phase, a0, nfull, extra, r8, lane, h1, h2); break;
+                case 1: hash_full_leaves_tma<1>(wbuf, bars, &phase, a0, nfull, extra, r8, lane, h1, h2); break;
+                case 2: hash_full_leaves_tma<2>(wbuf, bars, &phase, a0, nfull, extra, r8, lane, h1, h2); break;
+                default: hash_full_leaves_tma<3>(wbuf, bars, &phase, a0, nfull, extra, r8, lane, h1, h2); break;
+            }
+        }
+        if (lane < nfull) {
+            u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
+            mm::finish(f1, f2, 0, 0, 0, kLeafBytes);
+            acc_h += f1;
+            acc_l += f2;
+        } else if (lane == nfull && my_leaf * kLeafBytes < tk.n) {
+            const u32 len = static_cast<u32>(tk.n - my_leaf * kLeafBytes);
+            u64 d1, d2;
+            leaf_digest(tk.base + my_leaf * kLeafBytes, len, my_leaf, d1, d2);
+            acc_h += d1;
+            acc_l += d2;
+        }
+    }
+    if (cur >= 0) {
+        const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
+        if (lane == 0) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
+            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
+        }
+    }
+}
+
+// ---- v3: v1 with swizzled 8-word slots (default) ---------------------------------
+// v1's 9-word slots cost a divide-by-9 per copied word; per-lane TMA (v2)
+// serialises on uniform operands.  v3 keeps cp.async but lays a stage out as
+// 32 slots of 8 words (128 B) with the word index XOR-swizzled by (leaf & 7),
+// plus a 32-word column holding each leaf's 9th (realignment) word.  Then
+// copy i of a lane is leaf 4i + lane/8, word lane%8: one base register plus
+// the immediate 16 KiB·i per LDGSTS, no predicates on full tiles, and both
+// the LDGSTS writes and the per-lane LDS.128 reads are bank-conflict free.
+constexpr int kV3Stages = 3;
+constexpr int kV3StageWords = 32 * kStageBlocks + 32;  // slots + extra column
+constexpr int kV3WarpWords = kV3Stages * kV3StageWords;
+constexpr int kV3SmemBytes = kWarpsPerCta * kV3WarpWords * 16;
+
+__device__ __forceinline__ void v3_issue(uint4* stage_buf, const std::uint8_t* src_lane, const std::uint8_t* src_extra,
+                                         u32 nfull, bool extra, u32 lane) {
+    // slot words: copy i -> leaf 4i + lane/8, word lane%8 (swizzled by leaf&7)
+    const u32 leaf_in_group = lane >> 3, q = lane & 7;
+    if (nfull == 32) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            // leaf l = 4i + g; its swizzle key is (4i + g) & 7 = ((4i) & 7) ^ g for g < 4
+            const u32 key = ((4 * i) & 7) ^ leaf_in_group;
+            cp_async16(stage_buf + (4 * i + leaf_in_group) * 8 + (q ^ key), src_lane + static_cast<u64>(i) * 16384);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const u32 l = 4 * i + leaf_in_group;
+            if (l < nfull) cp_async16(stage_buf + l * 8 + (q ^ (l & 7)), src_lane + static_cast<u64>(i) * 16384);
+        }
+    }
+    if (extra && lane < nfull) cp_async16(stage_buf + 32 * kStageBlocks + lane, src_extra);
+    cp_async_commit();
+}
+
+template <int Q>
+__device__ __forceinline__ void v3_hash_stage(const uint4* stage_buf, u32 lane, u32 r8, mm::W32& h1, mm::W32& h2) {
+    const uint4* slot = stage_buf + lane * 8;
+    const u32 key = lane & 7;
+    uint4 w[kSlotWords];
+#pragma unroll
+    for (int q = 0; q < kStageBlocks; ++q) w[q] = slot[q ^ key];
+    w[kStageBlocks] = stage_buf[32 * kStageBlocks + lane];
+#pragma unroll
+    for (int b = 0; b < kStageBlocks; ++b) {
+        const u32 u[8] = {w[b].x, w[b].y, w[b].z, w[b].w, w[b + 1].x, w[b + 1].y, w[b + 1].z, w[b + 1].w};
+        const u32 a = __funnelshift_r(u[Q + 0], u[Q + 1], r8);
+        const u32 c = __funnelshift_r(u[Q + 1], u[Q + 2], r8);
+        const u32 d = __funnelshift_r(u[Q + 2], u[Q + 3], r8);
+        const u32 e = __funnelshift_r(u[Q + 3], u[Q + 4], r8);
+        mm::body_dev(h1, h2, mm::W32{a, c}, mm::W32{d, e});
+    }
+}
+
+template <int Q>
+__device__ __forceinline__ void v3_hash_full_leaves(uint4* wbuf, const std::uint8_t* a0, u32 nfull, bool extra,
+                                                    u32 r8, u32 lane, mm::W32& h1, mm::W32& h2) {
+    // copy i of this lane reads leaf (4i + lane/8), word lane%8 of the stage
+    const std::uint8_t* src_lane = a0 + static_cast<u64>(lane >> 3) * kLeafBytes + (lane & 7) * 16;
+    const std::uint8_t* src_extra = a0 + static_cast<u64>(lane) * kLeafBytes + 128;
+#pragma unroll
+    for (int s = 0; s < kV3Stages - 1; ++s)
+        v3_issue(wbuf + s * kV3StageWords, src_lane + s * 128, src_extra + s * 128, nfull, extra, lane);
+    for (int s = 0; s < kStagesPerLeaf; ++s) {
+        const int nxt = s + kV3Stages - 1;
+        if (nxt < kStagesPerLeaf)
+            v3_issue(wbuf + (nxt % kV3Stages) * kV3StageWords, src_lane + nxt * 128, src_extra + nxt * 128, nfull,
+                     extra, lane);
+        else
+            cp_async_commit();
+        cp_async_wait<kV3Stages - 1>();
+        __syncwarp();
+        if (lane < nfull) v3_hash_stage<Q>(wbuf + (s % kV3Stages) * kV3StageWords, lane, r8, h1, h2);
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
+    fp_v3_kernel(const FpTask* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums) {
+    extern __shared__ uint4 smem[];
+    const u32 lane = threadIdx.x & 31;
+    const u32 wid = threadIdx.x >> 5;
+    uint4* wbuf = smem + wid * kV3WarpWords;
+    const u64 nwarps = static_cast<u64>(gridDim.x) * kWarpsPerCta;
+    int cur = -1;
+    u64 acc_h = 0, acc_l = 0;
+    for (u64 t = static_cast<u64>(blockIdx.x) * kWarpsPerCta + wid; t < total_tiles; t += nwarps) {
+        u32 lo = 0, hi = n_tasks - 1;
+        while (lo < hi) {
+            const u32 mid = (lo + hi + 1) >> 1;
+            if (tasks[mid].tile0 <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        const int ti = static_cast<int>(lo);
+        if (ti != cur) {
+            if (cur >= 0) {
+                const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
+                if (lane == 0) {
+                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
+                }
+            }
+            cur = ti;
+            acc_h = acc_l = 0;
+        }
+        const FpTask tk = tasks[ti];
+        const u64 leaf0 = (t - tk.tile0) * kLeavesPerTile;
+        const u64 full_leaves = tk.n / kLeafBytes;
+        const u32 nfull = full_leaves > leaf0 ? static_cast<u32>(min(full_leaves - leaf0, u64{32})) : 0u;
+        const std::uint8_t* p0 = tk.base + leaf0 * kLeafBytes;
+        const u32 o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p0) & 15);
+        const std::uint8_t* a0 = p0 - o;
+        const u64 my_leaf = leaf0 + lane;
+        mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
+        if (nfull) {
+            const u32 r8 = (o & 3) * 8;
+            const bool extra = o != 0;
+            switch (o >> 2) {
+                case 0: v3_hash_full_leaves<0>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
+                case 1: v3_hash_full_leaves<1>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
+                case 2: v3_hash_full_leaves<2>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
+                default: v3_hash_full_leaves<3>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
+            }
+        }
+        if (lane < nfull) {
+            u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
+            mm::finish(f1, f2, 0, 0, 0, kLeafBytes);
+            acc_h += f1;
+            acc_l += f2;
+        } else if (lane == nfull && my_leaf * kLeafBytes < tk.n) {
+            const u32 len = static_cast<u32>(tk.n - my_leaf * kLeafBytes);
+            u64 d1, d2;
+            leaf_digest(tk.base + my_leaf * kLeafBytes, len, my_leaf, d1, d2);
+            acc_h += d1;
+            acc_l += d2;
+        }
+    }
+    if (cur >= 0) {
+        const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
+        if (lane == 0) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
+            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
+        }
+    }
+}
+
+// ---- v4: v3 + cross-tile pipelining (default) ---------------------------------
+// v3 drains its cp.async pipeline at every tile boundary: the prologue of tile
+// k+1 waits a full DRAM latency (~1.5 us) after ~5 us of hashing, which ncu
+// shows as the dominant long-scoreboard stall.  v4 treats a warp's tiles as
+// one continuous stream of 32-stage groups: the stages of tile k+1 are
+// already in flight while the last stages of tile k are hashed.
+struct TileRef {
+    const std::uint8_t* a0;  // aligned base of leaf 0 of the tile
+    const std::uint8_t* base;  // tensor base
+    u64 n;                   // tensor bytes
+    u64 leaf0;
+    u32 nfull;
+    u32 o;
+    int task;
+};
+
+__device__ __forceinline__ TileRef tile_ref(const FpTask* __restrict__ tasks, u32 n_tasks, u64 t, u64 total_tiles) {
+    TileRef r{nullptr, nullptr, 0, 0, 0, 0, -1};
+    if (t >= total_tiles) return r;
+    u32 lo = 0, hi = n_tasks - 1;
+    while (lo < hi) {
+        const u32 mid = (lo + hi + 1) >> 1;
+        if (tasks[mid].tile0 <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    const FpTask tk = tasks[lo];
+    r.task = static_cast<int>(lo);
+    r.base = tk.base;
+    r.n = tk.n;
+    r.leaf0 = (t - tk.tile0) * kLeavesPerTile;
+    const u64 full_leaves = tk.n / kLeafBytes;
+    r.nfull = full_leaves > r.leaf0 ? static_cast<u32>(min(full_leaves - r.leaf0, u64{32})) : 0u;
+    const std::uint8_t* p0 = tk.base + r.leaf0 * kLeafBytes;
+    r.o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p0) & 15);
+    r.a0 = p0 - r.o;
+    return r;
+}
+
+__device__ __forceinline__ void v4_issue(uint4* stage_buf, const TileRef& tr, int s, u32 lane) {
+    if (tr.task < 0 || tr.nfull == 0) {
+        cp_async_commit();
+        return;
+    }
+    const std::uint8_t* src_lane =
+        tr.a0 + static_cast<u64>(lane >> 3) * kLeafBytes + (lane & 7) * 16 + static_cast<u64>(s) * 128;
+    const std::uint8_t* src_extra = tr.a0 + static_cast<u64>(lane) * kLeafBytes + static_cast<u64>(s) * 128 + 128;
+    v3_issue(stage_buf, src_lane, src_extra, tr.nfull, tr.o != 0, lane);
+}
+
+__device__ __forceinline__ void v4_hash(const uint4* stage_buf, const TileRef& tr, u32 lane, mm::W32& h1,
+                                        mm::W32& h2) {
+    const u32 r8 = (tr.o & 3) * 8;
+    switch (tr.o >> 2) {
+        case 0: v3_hash_stage<0>(stage_buf, lane, r8, h1, h2); break;
+        case 1: v3_hash_stage<1>(stage_buf, lane, r8, h1, h2); break;
+        case 2: v3_hash_stage<2>(stage_buf, lane, r8, h1, h2); break;
+        default: v3_hash_stage<3>(stage_buf, lane, r8, h1, h2); break;
+    }
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
+    fp_v4_kernel(const FpTask* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums) {
+    extern __shared__ uint4 smem[];
+    const u32 lane = threadIdx.x & 31;
+    const u32 wid = threadIdx.x >> 5;
+    uint4* wbuf = smem + wid * kV3WarpWords;
+    const u64 nwarps = static_cast<u64>(gridDim.x) * kWarpsPerCta;
+    u64 t = static_cast<u64>(blockIdx.x) * kWarpsPerCta + wid;
+    if (t >= total_tiles) return;
+    TileRef cur = tile_ref(tasks, n_tasks, t, total_tiles);
+    TileRef nxt = tile_ref(tasks, n_tasks, t + nwarps, total_tiles);
+    int cur_task = -1;
+    u64 acc_h = 0, acc_l = 0;
+    u32 buf = 0;  // running stage-buffer index
+    constexpr int kAhead = kV3Stages - 1;
+#pragma unroll
+    for (int s = 0; s < kAhead; ++s) v4_issue(wbuf + s * kV3StageWords, cur, s, lane);
+    while (cur.task >= 0) {
+        if (cur.task != cur_task) {
+            if (cur_task >= 0) {
+                const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
+                if (lane == 0) {
+                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task), sh);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task + 1), sl);
+                }
+            }
+            cur_task = cur.task;
+            acc_h = acc_l = 0;
+        }
+        const u64 my_leaf = cur.leaf0 + lane;
+        mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
+        for (int s = 0; s < kStagesPerLeaf; ++s) {
+            const int ahead = s + kAhead;
+            u32 fill = buf + kAhead;
+            fill = fill >= kV3Stages ? fill - kV3Stages : fill;
+            if (ahead < kStagesPerLeaf) v4_issue(wbuf + fill * kV3StageWords, cur, ahead, lane);
+            else v4_issue(wbuf + fill * kV3StageWords, nxt, ahead - kStagesPerLeaf, lane);
+            cp_async_wait<kV3Stages - 1>();
+            __syncwarp();
+            if (lane < cur.nfull) v4_hash(wbuf + buf * kV3StageWords, cur, lane, h1, h2);
+            __syncwarp();
+            buf = buf + 1 == kV3Stages ? 0 : buf + 1;
+        }
+        if (lane < cur.nfull) {
+            u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
+            mm::finish(f1, f2, 0, 0, 0, kLeafBytes);
+            acc_h += f1;
+            acc_l += f2;
+        } else if (lane == cur.nfull && my_leaf * kLeafBytes < cur.n) {
+            const u32 len = static_cast<u32>(cur.n - my_leaf * kLeafBytes);
+            u64 d1, d2;
+            leaf_digest(cur.base + my_leaf * kLeafBytes, len, my_leaf, d1, d2);
+            acc_h += d1;
+            acc_l += d2;
+        }
+        t += nwarps;
+        cur = nxt;
+        nxt = tile_ref(tasks, n_tasks, t + nwarps, total_tiles);
+    }
+    cp_async_wait<0>();
+    if (cur_task >= 0) {
+        const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
+        if (lane == 0) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task), sh);
+            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task + 1), sl);
+        }
+    }
+}
+
 // root = murmur3(le64 H ‖ le64 L ‖ le64 n, seed 0): one body block + an
 // 8-byte tail.
 __global__ void fp_finalize_kernel(const FpTask* __restrict__ tasks, u32 n_tasks, const u64* __restrict__ sums,
@@ -302,11 +726,50 @@ __global__ void fp_finalize_kernel(const FpTask* __restrict__ tasks, u32 n_tasks
 void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, int sm_count,
                cudaStream_t s) {
     if (n_tasks == 0) return;
-    static const bool v0 = [] {
+    // TANGRAM_FP_KERNEL=v0..v3 selects the earlier variants (A/B runs); v4 is the default.
+    static const int variant = [] {
         const char* e = std::getenv("TANGRAM_FP_KERNEL");
-        return e && std::strcmp(e, "v0") == 0;
+        if (e && std::strcmp(e, "v0") == 0) return 0;
+        if (e && std::strcmp(e, "v1") == 0) return 1;
+        if (e && std::strcmp(e, "v2") == 0) return 2;
+        if (e && std::strcmp(e, "v3") == 0) return 3;
+        return 4;
     }();
-    if (total_tiles > 0 && v0) {
+    const bool v0 = variant == 0;
+    if (total_tiles > 0 && variant == 4) {
+        static const bool attr = [] {
+            return cudaFuncSetAttribute(fp_v4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV3SmemBytes) ==
+                   cudaSuccess;
+        }();
+        (void)attr;
+        const u64 want = (total_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
+        const u64 cap = static_cast<u64>(sm_count) * 2;
+        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
+        fp_v4_kernel<<<blocks, kWarpsPerCta * 32, kV3SmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
+        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+    } else if (total_tiles > 0 && variant == 3) {
+        static const bool attr = [] {
+            return cudaFuncSetAttribute(fp_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV3SmemBytes) ==
+                   cudaSuccess;
+        }();
+        (void)attr;
+        const u64 want = (total_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
+        const u64 cap = static_cast<u64>(sm_count) * 2;
+        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
+        fp_v3_kernel<<<blocks, kWarpsPerCta * 32, kV3SmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
+        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+    } else if (total_tiles > 0 && variant == 2) {
+        static const bool attr = [] {
+            return cudaFuncSetAttribute(fp_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemBytes) ==
+                   cudaSuccess;
+        }();
+        (void)attr;
+        const u64 want = (total_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
+        const u64 cap = static_cast<u64>(sm_count) * 2;
+        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
+        fp_tma_kernel<<<blocks, kWarpsPerCta * 32, kTmaSmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
+        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+    } else if (total_tiles > 0 && v0) {
         const u64 want = (total_tiles + 7) / 8;  // 8 warps per block
         const u64 cap = static_cast<u64>(sm_count) * 4;
         const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);

@@ -282,7 +282,16 @@ int tg_pool_info_get(const tg_pool* p, tg_pool_info* o) {
                       s.pinned_tensor_bytes(), s.pinned_bytes(),  s.reusable_bytes(),
                       s.merged_total(),    s.transferred_total(), s.evictions_total(),
                       s.map().region_count(), s.map().extent_count(), s.tensors().size(),
-                      s.map().largest_free(), p->pool->device(),  p->pool->arena()};
+                      s.map().largest_free(), p->pool->device(),  p->pool->arena(),
+                      0, 0.0, 0, 0, 0, 0, 0};
+    const Pool::Totals& t = p->pool->totals();
+    o->loads = t.loads;
+    o->data_plane_ms = t.data_plane_ms;
+    o->pcie_bytes = t.pcie_bytes;
+    o->peer_bytes = t.peer_bytes;
+    o->device_src_bytes = t.device_src_bytes;
+    o->fingerprint_bytes = t.fingerprint_bytes;
+    o->relocated_bytes = t.relocated_bytes;
     return 0;
 }
 

@@ -384,6 +384,13 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             e->has_digest = true;
         }
     }
+    totals_.loads += 1;
+    totals_.data_plane_ms += rep->t.total_ms;
+    totals_.pcie_bytes += rep->pcie_bytes;
+    totals_.peer_bytes += rep->peer_bytes;
+    totals_.device_src_bytes += rep->device_src_bytes;
+    totals_.fingerprint_bytes += rep->fingerprint_bytes;
+    totals_.relocated_bytes += D.plan.total_merge_cost;
     return ok();
 }
 

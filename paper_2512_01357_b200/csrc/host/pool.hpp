@@ -93,6 +93,13 @@ public:
     cudaStream_t stream() const { return s_main_; }
     int sm_count() const { return sm_count_; }
 
+    struct Totals {
+        u64 loads = 0;
+        double data_plane_ms = 0;
+        u64 pcie_bytes = 0, peer_bytes = 0, device_src_bytes = 0, fingerprint_bytes = 0, relocated_bytes = 0;
+    };
+    const Totals& totals() const { return totals_; }
+
     St load_model(const ModelDesc& m, const StatsView& stats, double clock, const LoadOptions& opt, u32 flags,
                   LoadReport* rep);
     St move_tensor(const Key& k, u64 to);  // metadata + bytes
@@ -120,6 +127,7 @@ private:
     cudaStream_t s_main_ = nullptr, s_copy_ = nullptr, s_fp_ = nullptr, s_peer_ = nullptr, s_verify_ = nullptr;
     std::vector<cudaEvent_t> events_;
     std::vector<Pool*> peers_;
+    Totals totals_;
     // staging
     void* h_stage_ = nullptr;
     void* d_stage_ = nullptr;

@@ -1,0 +1,68 @@
+"""Turn raw ncu outputs from gpurun_out/ into the committed summaries under
+profiles/ (the .ncu-rep files stay in gpurun_out/, which is scratch).
+
+    python tools/make_profiles.py r01
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+from ncu_summary import summarise  # noqa: E402
+
+
+def launch_shares(path):
+    rows = []
+    with open(path) as f:
+        lines = [ln for ln in f if ln.startswith('"')]
+    rd = csv.DictReader(io.StringIO("".join(lines)))
+    per = defaultdict(lambda: [0, 0.0])
+    order = []
+    for r in rd:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        name = r["Kernel Name"].split("(")[0].replace("unnamed>::", "")
+        ns = float(r["Metric Value"].replace(",", ""))
+        unit = r.get("Metric Unit", "ns")
+        ns = ns * {"ns": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}.get(unit, 1)
+        per[name][0] += 1
+        per[name][1] += ns
+        order.append((name, ns))
+    total = sum(v[1] for v in per.values())
+    return {"total_kernel_ms": total / 1e6, "launches": len(order),
+            "by_kernel": {k: {"launches": v[0], "ms": v[1] / 1e6, "share": v[1] / total if total else 0}
+                          for k, v in sorted(per.items(), key=lambda kv: -kv[1][1])}}
+
+
+def main():
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    os.makedirs(PROF, exist_ok=True)
+    out = {}
+    for name in sorted(os.listdir(OUT)):
+        p = os.path.join(OUT, name)
+        if name.endswith(".ncu-rep"):
+            out[name] = summarise(p)
+    if out:
+        with open(os.path.join(PROF, f"{tag}_ncu_full.json"), "w") as f:
+            json.dump(out, f, indent=1)
+    lp = os.path.join(OUT, "launches.csv")
+    if os.path.exists(lp):
+        with open(os.path.join(PROF, f"{tag}_launches_summary.json"), "w") as f:
+            json.dump(launch_shares(lp), f, indent=1)
+        subprocess.run(["cp", lp, os.path.join(PROF, f"{tag}_launches.csv")])
+    for extra in ("kernel_bench.json", "bench.json"):
+        p = os.path.join(OUT, extra)
+        if os.path.exists(p):
+            subprocess.run(["cp", p, os.path.join(PROF, f"{tag}_{extra}")])
+    print(json.dumps(sorted(os.listdir(PROF))))
+
+
+if __name__ == "__main__":
+    main()
