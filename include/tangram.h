@@ -238,6 +238,21 @@ int tg_regions(const tg_pool* p, tg_region* buf, uint64_t cap, uint64_t* n); /* 
 int tg_tensor_info_get(const tg_pool* p, tg_tensor_id id, tg_tensor_info* out);
 int tg_fingerprint_tensor(tg_pool* p, tg_tensor_id id, tg_digest* out);    /* K1 over resident bytes */
 int tg_pool_add_peer(tg_pool* p, tg_pool* peer);                           /* NVLink peer pool (K5) */
+/* Peers in other processes (one process per GPU): export the
+ * arena as a CUDA IPC handle plus the index of fingerprinted residents; a
+ * peer attaches both and then pulls misses over NVLink (TG_LOAD_PEER).  The
+ * pulled bytes are fingerprinted and checked against the index's digest; a
+ * stale index falls back to the host source. */
+typedef struct {
+    tg_tensor_id id;
+    uint64_t offset, size;
+    tg_digest digest;
+} tg_index_entry;
+#define TG_IPC_HANDLE_BYTES 64
+int tg_pool_export_ipc(const tg_pool* p, void* handle /* TG_IPC_HANDLE_BYTES */);
+int tg_pool_index(const tg_pool* p, tg_index_entry* buf, uint64_t cap, uint64_t* n);
+int tg_pool_attach_remote(tg_pool* p, const void* handle, const tg_index_entry* idx, uint64_t n, int32_t* peer_id);
+int tg_pool_update_remote(tg_pool* p, int32_t peer_id, const tg_index_entry* idx, uint64_t n);
 int tg_pool_snapshot(tg_pool* p, tg_snapshot** out);
 int tg_pool_restore(tg_pool* p, const tg_snapshot* s);
 void tg_snapshot_destroy(tg_snapshot* s);
@@ -255,10 +270,13 @@ int tg_host_free(void* p);
 /* ---- raw device helpers ------------------------------------------------------ */
 int tg_fingerprint_device(const void* dptr, uint64_t n, int32_t device, tg_digest* out); /* K1 */
 int tg_synth_fill_device(tg_tensor_id id, uint64_t begin, uint64_t len, void* dptr, int32_t device);
-/* kernel-only microbenchmarks: reps launches timed with CUDA events on the launching stream */
-int tg_bench_fingerprint(const void* dptr, uint64_t n, int32_t device, int32_t reps, double* ms_per_launch,
-                         tg_digest* out);
-int tg_bench_relocate(void* dst, const void* src, uint64_t n, int32_t device, int32_t reps, double* ms_per_launch);
+/* Kernel-only timing: one K1 launch over n_bufs device buffers / one K3 wave
+ * of n_moves (src, dst, len) moves, `reps` back-to-back launches bracketed by
+ * CUDA events on the launching stream (after a warm-up launch). */
+int tg_bench_fingerprint(const void* const* dptrs, const uint64_t* ns, uint32_t n_bufs, int32_t device, int32_t reps,
+                         double* ms_per_launch, tg_digest* out /* n_bufs, nullable */);
+int tg_bench_relocate(const uint64_t* moves /* src,dst,len triples (device addresses) */, uint32_t n_moves,
+                      int32_t device, int32_t reps, double* ms_per_launch);
 int tg_synth_fill_host(tg_tensor_id id, uint64_t begin, uint64_t len, void* dst, int32_t threads);
 int tg_device_alloc(int32_t device, uint64_t size, void** out);
 int tg_device_free(int32_t device, void* p);

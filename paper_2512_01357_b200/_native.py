@@ -95,6 +95,10 @@ class KvStatsC(C.Structure):
                 ("active_requests", u64), ("next_pbn", u64), ("block_bytes", u64)]
 
 
+class IndexEntryC(C.Structure):
+    _fields_ = [("id", TensorIdC), ("offset", u64), ("size", u64), ("digest", DigestC)]
+
+
 class GpuSnapshotC(C.Structure):
     _fields_ = [("gpu_id", cp), ("available", i32), ("pool_size", u64), ("free_bytes", u64),
                 ("pcie_bandwidth", dbl), ("store_bandwidth", dbl), ("nvlink_bandwidth", dbl)]
@@ -152,6 +156,10 @@ _SIGS = {
     "tg_tensor_info_get": (C.c_int, [vp, TensorIdC, P(TensorInfoC)]),
     "tg_fingerprint_tensor": (C.c_int, [vp, TensorIdC, P(DigestC)]),
     "tg_pool_add_peer": (C.c_int, [vp, vp]),
+    "tg_pool_export_ipc": (C.c_int, [vp, vp]),
+    "tg_pool_index": (C.c_int, [vp, P(IndexEntryC), u64, P(u64)]),
+    "tg_pool_attach_remote": (C.c_int, [vp, vp, P(IndexEntryC), u64, P(i32)]),
+    "tg_pool_update_remote": (C.c_int, [vp, i32, P(IndexEntryC), u64]),
     "tg_pool_snapshot": (C.c_int, [vp, P(vp)]),
     "tg_pool_restore": (C.c_int, [vp, vp]),
     "tg_snapshot_destroy": (None, [vp]),
@@ -162,8 +170,8 @@ _SIGS = {
     "tg_host_free": (C.c_int, [vp]),
     "tg_fingerprint_device": (C.c_int, [vp, u64, i32, P(DigestC)]),
     "tg_synth_fill_device": (C.c_int, [TensorIdC, u64, u64, vp, i32]),
-    "tg_bench_fingerprint": (C.c_int, [vp, u64, i32, i32, P(dbl), P(DigestC)]),
-    "tg_bench_relocate": (C.c_int, [vp, vp, u64, i32, i32, P(dbl)]),
+    "tg_bench_fingerprint": (C.c_int, [P(vp), P(u64), u32, i32, i32, P(dbl), P(DigestC)]),
+    "tg_bench_relocate": (C.c_int, [P(u64), u32, i32, i32, P(dbl)]),
     "tg_synth_fill_host": (C.c_int, [TensorIdC, u64, u64, vp, i32]),
     "tg_device_alloc": (C.c_int, [i32, u64, P(vp)]),
     "tg_device_free": (C.c_int, [i32, vp]),

@@ -507,6 +507,49 @@ int tg_pool_add_peer(tg_pool* p, tg_pool* peer) {
     });
 }
 
+static std::vector<RemoteEntry> entries_of(const tg_index_entry* idx, uint64_t n) {
+    std::vector<RemoteEntry> v;
+    v.reserve(n);
+    for (uint64_t i = 0; i < n; ++i)
+        v.push_back(RemoteEntry{key_of(idx[i].id), idx[i].offset, idx[i].size, Digest{idx[i].digest.hi, idx[i].digest.lo}});
+    return v;
+}
+
+int tg_pool_export_ipc(const tg_pool* p, void* handle) {
+    return guard([&] {
+        static_assert(sizeof(cudaIpcMemHandle_t) == TG_IPC_HANDLE_BYTES, "IPC handle size");
+        cudaIpcMemHandle_t h;
+        p->pool->export_handle(&h);
+        std::memcpy(handle, &h, sizeof h);
+        return 0;
+    });
+}
+
+int tg_pool_index(const tg_pool* p, tg_index_entry* buf, uint64_t cap, uint64_t* n) {
+    const auto idx = p->pool->index();
+    *n = idx.size();
+    for (uint64_t i = 0; buf && i < idx.size() && i < cap; ++i)
+        buf[i] = tg_index_entry{id_of(idx[i].id), idx[i].off, idx[i].size, {idx[i].digest.hi, idx[i].digest.lo}};
+    return buf && cap < idx.size() ? TG_ERR_BUFFER : 0;
+}
+
+int tg_pool_attach_remote(tg_pool* p, const void* handle, const tg_index_entry* idx, uint64_t n, int32_t* peer_id) {
+    return guard([&] {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        const int id = p->pool->attach_remote(h, entries_of(idx, n));
+        if (peer_id) *peer_id = id;
+        return 0;
+    });
+}
+
+int tg_pool_update_remote(tg_pool* p, int32_t peer_id, const tg_index_entry* idx, uint64_t n) {
+    return guard([&] {
+        p->pool->update_remote(peer_id, entries_of(idx, n));
+        return 0;
+    });
+}
+
 int tg_pool_snapshot(tg_pool* p, tg_snapshot** out) {
     return guard([&] {
         *out = new tg_snapshot{p->pool->snapshot()};
@@ -564,17 +607,23 @@ int tg_fingerprint_device(const void* dptr, uint64_t n, int32_t device, tg_diges
         return 0;
     });
 }
-int tg_bench_fingerprint(const void* dptr, uint64_t n, int32_t device, int32_t reps, double* ms, tg_digest* out) {
+int tg_bench_fingerprint(const void* const* dptrs, const uint64_t* ns, uint32_t n_bufs, int32_t device, int32_t reps,
+                         double* ms, tg_digest* out) {
     return guard([&] {
-        Digest d;
-        *ms = bench_fingerprint(dptr, n, device, reps < 1 ? 1 : reps, &d);
-        if (out) *out = tg_digest{d.hi, d.lo};
+        std::vector<std::pair<const void*, u64>> b;
+        for (uint32_t i = 0; i < n_bufs; ++i) b.push_back({dptrs[i], ns[i]});
+        std::vector<Digest> d;
+        *ms = bench_fingerprint(b, device, reps < 1 ? 1 : reps, &d);
+        for (uint32_t i = 0; out && i < n_bufs; ++i) out[i] = tg_digest{d[i].hi, d[i].lo};
         return 0;
     });
 }
-int tg_bench_relocate(void* dst, const void* src, uint64_t n, int32_t device, int32_t reps, double* ms) {
+int tg_bench_relocate(const uint64_t* triples /*src,dst,len*/, uint32_t n_moves, int32_t device, int32_t reps,
+                      double* ms) {
     return guard([&] {
-        *ms = bench_relocate(dst, src, n, device, reps < 1 ? 1 : reps);
+        std::vector<MoveDesc> mv;
+        for (uint32_t i = 0; i < n_moves; ++i) mv.push_back(MoveDesc{triples[3 * i], triples[3 * i + 1], triples[3 * i + 2]});
+        *ms = bench_relocate(mv, device, reps < 1 ? 1 : reps);
         return 0;
     });
 }

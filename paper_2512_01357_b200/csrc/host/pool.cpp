@@ -54,6 +54,8 @@ Pool::~Pool() {
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
     for (cudaStream_t s : {s_main_, s_copy_, s_fp_, s_peer_, s_verify_})
         if (s) cudaStreamDestroy(s);
+    for (RemotePeer& r : remotes_)
+        if (r.base) cudaIpcCloseMemHandle(r.base);
     if (arena_) cudaFree(arena_);
     if (d_stage_) cudaFree(d_stage_);
     if (h_stage_) cudaFreeHost(h_stage_);
@@ -125,6 +127,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     const std::size_t np = d.plan.placements.size();
     std::vector<HostSource> src(np);
     std::vector<const std::uint8_t*> peer_src(np, nullptr);
+    std::vector<Digest> peer_digest(np);  // what the peer's index says the bytes fingerprint to
     rep->placement_src.assign(np, 0);
     if (has_device()) {
         for (std::size_t i = 0; i < np; ++i) {
@@ -134,8 +137,17 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
                     const Entry* e = p->store_.entry(t.id);
                     if (e && e->size == t.size && e->has_digest) {
                         peer_src[i] = p->arena_ + e->off;
+                        peer_digest[i] = e->digest;
                         rep->placement_src[i] = 1;
                         break;
+                    }
+                }
+                for (std::size_t r = 0; !peer_src[i] && r < remotes_.size(); ++r) {
+                    auto it = remotes_[r].index.find(t.id);
+                    if (it != remotes_[r].index.end() && it->second.size == t.size) {
+                        peer_src[i] = remotes_[r].base + it->second.off;
+                        peer_digest[i] = it->second.digest;
+                        rep->placement_src[i] = 1;
                     }
                 }
             }
@@ -361,6 +373,19 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
         rep->digests[pos[t.id]] = g;
         rep->fingerprint_bytes += t.size;
         if (!rep->placement_src[i] && src[i].has_expected && !(src[i].expected == g)) ++rep->expected_mismatches;
+        if (rep->placement_src[i] == 1 && !(peer_digest[i] == g)) {
+            // The peer's index was stale (its bytes changed under us): fetch the
+            // tensor from its host source instead.
+            ++rep->verify_mismatches;
+            HostSource hs;
+            if (!SourceRegistry::get().find(t.id, &hs) || hs.size != t.size)
+                throw DeviceError(kErrVerify, "peer bytes of " + t.id.hex() + " fail verification and no host source");
+            TG_CUDA(cudaMemcpyAsync(arena_ + e->off, hs.ptr, t.size, cudaMemcpyDefault, s_main_));
+            TG_CUDA(cudaStreamSynchronize(s_main_));
+            rep->repaired_bytes += t.size;
+            e->digest = fingerprint_resident(t.id);
+            rep->digests[pos[t.id]] = e->digest;
+        }
     }
     for (std::size_t i = 0; i < hit_tasks.size(); ++i) {
         const Key& k = hit_keys[i];
@@ -434,13 +459,51 @@ u64 Pool::peer_reuse_size(const ModelDesc& m) const {
     u64 s = 0;
     for (const auto& t : m.tensors) {
         if (store_.tensors().count(t.id)) continue;
+        bool found = false;
         for (Pool* p : peers_)
             if (const auto it = p->store_.tensors().find(t.id); it != p->store_.tensors().end() && it->second.has_digest) {
-                s += t.size;
+                found = true;
                 break;
             }
+        for (const RemotePeer& r : remotes_)
+            if (!found && r.index.count(t.id)) found = true;
+        if (found) s += t.size;
     }
     return s;
+}
+
+// ---- cross-process peers (one process per GPU): CUDA IPC on the arena -----------
+void Pool::export_handle(cudaIpcMemHandle_t* h) const {
+    if (!has_device()) throw DeviceError(kErrNoDevice, "pool has no device");
+    DeviceScope ds(device_);
+    TG_CUDA(cudaIpcGetMemHandle(h, arena_));
+}
+
+std::vector<RemoteEntry> Pool::index() const {
+    std::vector<RemoteEntry> out;
+    out.reserve(store_.tensors().size());
+    for (const auto& [k, e] : store_.tensors())
+        if (e.has_digest) out.push_back(RemoteEntry{k, e.off, e.size, e.digest});
+    return out;
+}
+
+int Pool::attach_remote(const cudaIpcMemHandle_t& h, const std::vector<RemoteEntry>& idx) {
+    if (!has_device()) throw DeviceError(kErrNoDevice, "pool has no device");
+    DeviceScope ds(device_);
+    RemotePeer r;
+    void* p = nullptr;
+    TG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    r.base = static_cast<std::uint8_t*>(p);
+    for (const RemoteEntry& e : idx) r.index[e.id] = e;
+    remotes_.push_back(std::move(r));
+    return static_cast<int>(remotes_.size() - 1);
+}
+
+void Pool::update_remote(int id, const std::vector<RemoteEntry>& idx) {
+    if (id < 0 || static_cast<std::size_t>(id) >= remotes_.size()) throw DeviceError(104, "bad remote peer id");
+    auto& m = remotes_[static_cast<std::size_t>(id)].index;
+    m.clear();
+    for (const RemoteEntry& e : idx) m[e.id] = e;
 }
 
 struct Pool::Snapshot {
@@ -507,31 +570,35 @@ void fingerprint_device(const void* ptr, u64 n, int device, Digest* out) {
 // Kernel-only timing of K1 / K3 for microbenchmarks: setup outside the timed
 // region, `reps` back-to-back launches bracketed by CUDA events on the
 // launching stream.  Returns the mean ms per launch.
-double bench_fingerprint(const void* ptr, u64 n, int device, int reps, Digest* out) {
+double bench_fingerprint(const std::vector<std::pair<const void*, u64>>& bufs, int device, int reps,
+                         std::vector<Digest>* out) {
     DeviceScope ds(device);
     int sms = 148;
     TG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    std::vector<FpTask> t{FpTask{static_cast<const std::uint8_t*>(ptr), n, 0}};
+    std::vector<FpTask> t;
+    for (const auto& [p, n] : bufs) t.push_back(FpTask{static_cast<const std::uint8_t*>(p), n, 0});
     const u64 tiles = build_tasks(t);
+    const u32 nt = static_cast<u32>(t.size());
     cudaStream_t s;
     TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     void* d = nullptr;
-    const std::size_t per = 4 * sizeof(u64);
-    TG_CUDA(cudaMalloc(&d, sizeof(FpTask) + per * (reps + 1)));
-    TG_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(FpTask), cudaMemcpyHostToDevice, s));
-    auto* sums = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(d) + sizeof(FpTask));
+    const std::size_t per = 4 * sizeof(u64) * nt;  // sums + digests per rep
+    TG_CUDA(cudaMalloc(&d, sizeof(FpTask) * nt + per * (reps + 1)));
+    TG_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(FpTask) * nt, cudaMemcpyHostToDevice, s));
+    auto* sums = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(d) + sizeof(FpTask) * nt);
     TG_CUDA(cudaMemsetAsync(sums, 0, per * (reps + 1), s));
-    fp_launch(static_cast<const FpTask*>(d), 1, tiles, sums, sums + 2, sms, s);  // warm-up
+    auto rep_sums = [&](int r) { return sums + static_cast<std::size_t>(r) * 4 * nt; };
+    fp_launch(static_cast<const FpTask*>(d), nt, tiles, rep_sums(0), rep_sums(0) + 2 * nt, sms, s);  // warm-up
     cudaEvent_t a, b;
     TG_CUDA(cudaEventCreate(&a));
     TG_CUDA(cudaEventCreate(&b));
     TG_CUDA(cudaEventRecord(a, s));
     for (int r = 1; r <= reps; ++r)
-        fp_launch(static_cast<const FpTask*>(d), 1, tiles, sums + 4 * r, sums + 4 * r + 2, sms, s);
+        fp_launch(static_cast<const FpTask*>(d), nt, tiles, rep_sums(r), rep_sums(r) + 2 * nt, sms, s);
     TG_CUDA(cudaEventRecord(b, s));
     TG_CUDA(cudaGetLastError());
-    u64 h[2];
-    TG_CUDA(cudaMemcpyAsync(h, sums + 4 * reps + 2, sizeof h, cudaMemcpyDeviceToHost, s));
+    std::vector<u64> h(2 * nt);
+    TG_CUDA(cudaMemcpyAsync(h.data(), rep_sums(reps) + 2 * nt, 2 * nt * sizeof(u64), cudaMemcpyDeviceToHost, s));
     TG_CUDA(cudaStreamSynchronize(s));
     float ms = 0;
     TG_CUDA(cudaEventElapsedTime(&ms, a, b));
@@ -539,23 +606,26 @@ double bench_fingerprint(const void* ptr, u64 n, int device, int reps, Digest* o
     cudaEventDestroy(b);
     cudaFree(d);
     cudaStreamDestroy(s);
-    if (out) *out = Digest{h[0], h[1]};
+    if (out) {
+        out->clear();
+        for (u32 i = 0; i < nt; ++i) out->push_back(Digest{h[2 * i], h[2 * i + 1]});
+    }
     return ms / reps;
 }
 
-double bench_relocate(void* dst, const void* src, u64 n, int device, int reps) {
+double bench_relocate(const std::vector<MoveDesc>& moves, int device, int reps) {
     DeviceScope ds(device);
     int sms = 148;
     TG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     cudaStream_t s;
     TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    MoveDesc md{reinterpret_cast<u64>(src), reinterpret_cast<u64>(dst), n};
-    relocate_launch(&md, 1, sms, s);  // warm-up
+    const int nm = static_cast<int>(moves.size());
+    relocate_launch(moves.data(), nm, sms, s);  // warm-up
     cudaEvent_t a, b;
     TG_CUDA(cudaEventCreate(&a));
     TG_CUDA(cudaEventCreate(&b));
     TG_CUDA(cudaEventRecord(a, s));
-    for (int r = 0; r < reps; ++r) relocate_launch(&md, 1, sms, s);
+    for (int r = 0; r < reps; ++r) relocate_launch(moves.data(), nm, sms, s);
     TG_CUDA(cudaEventRecord(b, s));
     TG_CUDA(cudaGetLastError());
     TG_CUDA(cudaStreamSynchronize(s));

@@ -17,6 +17,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "../device/kernels.hpp"
 #include "kv.hpp"
 #include "store.hpp"
 
@@ -47,6 +48,14 @@ public:
 private:
     mutable std::mutex mu_;
     std::unordered_map<Key, HostSource, KeyHash> map_;
+};
+
+// A resident, fingerprinted tensor of a peer pool (what peers exchange).
+struct RemoteEntry {
+    Key id;
+    u64 off = 0;
+    u64 size = 0;
+    Digest digest;
 };
 
 // load flags (tg_load_policy.flags)
@@ -106,6 +115,12 @@ public:
 
     Digest fingerprint_resident(const Key& k);  // K1 over the resident bytes
     void add_peer(Pool* p);
+    // Peers in other processes: export this arena (CUDA IPC), publish the
+    // index of fingerprinted residents, attach a remote arena + its index.
+    void export_handle(cudaIpcMemHandle_t* h) const;
+    std::vector<RemoteEntry> index() const;
+    int attach_remote(const cudaIpcMemHandle_t& h, const std::vector<RemoteEntry>& idx);
+    void update_remote(int id, const std::vector<RemoteEntry>& idx);
     u64 peer_reuse_size(const ModelDesc& m) const;  // bytes of m's misses resident on a peer
 
     // Whole-pool checkpoint (metadata + arena bytes) for rollback / benchmarks.
@@ -127,6 +142,11 @@ private:
     cudaStream_t s_main_ = nullptr, s_copy_ = nullptr, s_fp_ = nullptr, s_peer_ = nullptr, s_verify_ = nullptr;
     std::vector<cudaEvent_t> events_;
     std::vector<Pool*> peers_;
+    struct RemotePeer {
+        std::uint8_t* base = nullptr;  // IPC-mapped peer arena
+        std::unordered_map<Key, RemoteEntry, KeyHash> index;
+    };
+    std::vector<RemotePeer> remotes_;
     Totals totals_;
     // staging
     void* h_stage_ = nullptr;
@@ -138,7 +158,8 @@ private:
 std::unique_ptr<KvDevice> make_kv_device(int device, cudaStream_t stream);
 void fingerprint_device(const void* ptr, u64 n, int device, Digest* out);
 void synth_fill_device(const Key& k, u64 begin, u64 len, void* dst, int device);
-double bench_fingerprint(const void* ptr, u64 n, int device, int reps, Digest* out);
-double bench_relocate(void* dst, const void* src, u64 n, int device, int reps);
+double bench_fingerprint(const std::vector<std::pair<const void*, u64>>& bufs, int device, int reps,
+                         std::vector<Digest>* out);
+double bench_relocate(const std::vector<MoveDesc>& moves, int device, int reps);
 
 }  // namespace tg

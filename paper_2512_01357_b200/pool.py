@@ -494,6 +494,38 @@ class ReuseStore:
     def add_peer(self, other: "ReuseStore"):
         N.check_runtime(lib.tg_pool_add_peer(self._h, other._h), "tg_pool_add_peer")
 
+    # -- peers in other processes (CUDA IPC + index exchange) ----------------------
+    def export_ipc(self) -> bytes:
+        h = (C.c_uint8 * 64)()
+        N.check_runtime(lib.tg_pool_export_ipc(self._h, h), "tg_pool_export_ipc")
+        return bytes(h)
+
+    def index(self):
+        """[(TensorId, offset, size, digest)] of fingerprinted residents."""
+        n = C.c_uint64()
+        lib.tg_pool_index(self._h, None, 0, C.byref(n))
+        buf = (N.IndexEntryC * max(1, n.value))()
+        lib.tg_pool_index(self._h, buf, n.value, C.byref(n))
+        return [(TensorId(e.id.hi, e.id.lo), e.offset, e.size, (e.digest.hi, e.digest.lo)) for e in buf[:n.value]]
+
+    @staticmethod
+    def _index_c(entries):
+        arr = (N.IndexEntryC * max(1, len(entries)))()
+        for i, (tid, off, size, dig) in enumerate(entries):
+            arr[i] = N.IndexEntryC(tid.c(), off, size, N.DigestC(*dig))
+        return arr
+
+    def attach_remote(self, handle: bytes, entries) -> int:
+        hb = (C.c_uint8 * 64)(*handle)
+        pid = C.c_int32()
+        N.check_runtime(lib.tg_pool_attach_remote(self._h, hb, self._index_c(entries), len(entries),
+                                                  C.byref(pid)), "tg_pool_attach_remote")
+        return pid.value
+
+    def update_remote(self, peer_id, entries):
+        N.check_runtime(lib.tg_pool_update_remote(self._h, peer_id, self._index_c(entries), len(entries)),
+                        "tg_pool_update_remote")
+
     def snapshot(self):
         s = C.c_void_p()
         N.check_runtime(lib.tg_pool_snapshot(self._h, C.byref(s)), "tg_pool_snapshot")

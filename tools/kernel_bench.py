@@ -40,8 +40,10 @@ def main():
         for shift in (0, 3, 8, 13):
             ms = C.c_double()
             d = N.DigestC()
-            N.check_runtime(lib.tg_bench_fingerprint(C.c_void_p(buf.ptr + shift), n, dev, args.reps, C.byref(ms),
-                                                     C.byref(d)), "bench fp")
+            ptrs = (C.c_void_p * 1)(buf.ptr + shift)
+            ns = (C.c_uint64 * 1)(n)
+            N.check_runtime(lib.tg_bench_fingerprint(ptrs, ns, 1, dev, args.reps, C.byref(ms), C.byref(d)),
+                            "bench fp")
             res[f"shift{shift}"] = {"ms": ms.value, "GBps": n / ms.value / 1e6}
         out["fp"] = {"bytes_per_launch": n, **res}
         buf.free()
@@ -52,8 +54,8 @@ def main():
         res = {}
         for so, do in ((0, 0), (0, 5), (3, 11), (7, 7), (13, 2)):
             ms = C.c_double()
-            N.check_runtime(lib.tg_bench_relocate(C.c_void_p(b.ptr + do), C.c_void_p(a.ptr + so), size, dev,
-                                                  args.reps, C.byref(ms)), "bench reloc")
+            mv = (C.c_uint64 * 3)(a.ptr + so, b.ptr + do, size)
+            N.check_runtime(lib.tg_bench_relocate(mv, 1, dev, args.reps, C.byref(ms)), "bench reloc")
             res[f"src{so}_dst{do}"] = {"ms": ms.value, "GBps_rw": 2 * size / ms.value / 1e6}
         out["reloc"] = {"bytes_per_launch": size, **res}
         a.free()
