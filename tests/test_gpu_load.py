@@ -254,3 +254,55 @@ def test_kv_device_fuzz_vs_reference(tg, ref):
                 assert [[k, v] for k, v in sorted(t.lbn_to_pbn.items())] == rt["lbn_to_pbn"]
             assert mine.dump() == theirs.dump()
         mine.close()
+
+
+def test_missing_source_leaves_pool_unchanged(tg):
+    """A miss without a byte source fails with TG_ERR_NO_SOURCE before any
+    state changes (like a failed plan, reuse_store.hpp:117-119)."""
+    from paper_2512_01357_b200 import _native as N
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    a, b = tg.make_model("src-a", 20_000_003, 2, 0), tg.make_model("src-b", 20_000_011, 2, 0)
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=30_000_000), device=0)
+    st = tg.ModelStatsTable()
+    with HostCheckpoint([a]):
+        pool.load_model(a, st, 0.0).value()
+        pool.end_instance("src-a")
+        before = pool.dump()
+        st.record_request("src-b", 1.0)
+        with pytest.raises(N.TangramRuntimeError) as ei:
+            pool.load_model(b, st, 1.0)
+        assert ei.value.code == 102
+        assert pool.dump() == before and pool.validate().ok()
+    pool.close()
+
+
+def test_insufficient_memory_is_a_domain_error(tg, ref):
+    """Planning failures come back as the reference's Error values, the pool
+    untouched, on a device pool too."""
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    a = tg.make_model("big", 50_000_000, 2, 0)
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=40_000_000), device=0)
+    st = tg.ModelStatsTable()
+    with HostCheckpoint([a]):
+        before = pool.dump()
+        r = pool.load_model(a, st, 0.0)
+        assert r.error() == tg.Error.InsufficientMemory and pool.dump() == before
+    rr = ref.ReuseStore(40_000_000)
+    assert rr.load_model(a.to_json(), ref.ModelStatsTable(), 0.0) == {"ok": False, "error": 0}
+    pool.close()
+
+
+def test_kv_tables_survive_engine_copy_and_pool_teardown(tg):
+    """KvEngine value semantics (copied in kv_engine.hpp:146 rollback and by
+    the simulator): a clone owns independent device tables."""
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=1 << 24), device=0)
+    st = tg.ModelStatsTable()
+    kv = tg.KvEngine("m", 4, 64)
+    a = kv.batch_allocate(pool, st, [(1, 10), (2, 30)]).value()
+    c = kv.clone()
+    assert c.table(1).lbn_to_pbn == kv.table(1).lbn_to_pbn
+    kv.release_request(1)
+    kv.batch_allocate(pool, st, [(3, 8)])
+    assert c.table(1) is not None and [c.table(1).lbn_to_pbn[i] for i in range(3)] == a[0]
+    pool.close()
+    del c, kv
