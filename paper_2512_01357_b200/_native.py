@@ -172,6 +172,7 @@ _SIGS = {
     "tg_synth_fill_device": (C.c_int, [TensorIdC, u64, u64, vp, i32]),
     "tg_bench_fingerprint": (C.c_int, [P(vp), P(u64), u32, i32, i32, P(dbl), P(DigestC)]),
     "tg_bench_relocate": (C.c_int, [P(u64), u32, i32, i32, P(dbl)]),
+    "tg_copy_fingerprint": (C.c_int, [P(u64), u32, i32, i32, P(dbl), P(DigestC)]),
     "tg_synth_fill_host": (C.c_int, [TensorIdC, u64, u64, vp, i32]),
     "tg_device_alloc": (C.c_int, [i32, u64, P(vp)]),
     "tg_device_free": (C.c_int, [i32, vp]),

@@ -721,7 +721,230 @@ __global__ void fp_finalize_kernel(const FpTask* __restrict__ tasks, u32 n_tasks
     digests[2 * i + 1] = h2;
 }
 
+// ---- K3F: copy + fingerprint in one pass ------------------------------------------
+// Moves a tensor (relocation wave member, HBM-cache or peer placement) and
+// computes its tgfp1 digest from the same staged bytes, so the bytes cross
+// HBM once in each direction instead of copy (r+w) + fingerprint (r).
+// Staging and hashing are v4's.  The destination is written from the staged
+// slots: with o = src & 15, od = dst & 15 and delta = (o - od) mod 16, the
+// 16-byte destination word of leaf l, stage s, index q holds tensor bytes
+// [x, x+16), x = 4096 l + 128 s - o + delta + 16 q — slot bytes delta+16q..,
+// i.e. slot words q, q+1 funnel-shifted by delta.  These words tile the
+// tensor without gaps or overlaps; the ones that would reach outside
+// [0, 4096 F) (F = full leaves) are left to an edge pass that copies the
+// head (< 16 B) and the tail (< 4 KiB + 16 B) bytewise.
+struct CopyTileRef {
+    TileRef t;
+    std::uint8_t* dst;  // destination of tensor byte 0
+    u32 delta;
+    u64 x_first, x_end;  // full-word writes cover tensor bytes [x_first, x_end)
+};
+
+__device__ __forceinline__ CopyTileRef copy_tile_ref(const CopyFpTask* __restrict__ tasks, u32 n_tasks, u64 t,
+                                                     u64 total_tiles) {
+    CopyTileRef r{};
+    r.t.task = -1;
+    if (t >= total_tiles) return r;
+    u32 lo = 0, hi = n_tasks - 1;
+    while (lo < hi) {
+        const u32 mid = (lo + hi + 1) >> 1;
+        if (tasks[mid].tile0 <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    const CopyFpTask tk = tasks[lo];
+    r.t.task = static_cast<int>(lo);
+    r.t.base = tk.src;
+    r.t.n = tk.n;
+    r.t.leaf0 = (t - tk.tile0) * kLeavesPerTile;
+    const u64 full = tk.n / kLeafBytes;
+    r.t.nfull = full > r.t.leaf0 ? static_cast<u32>(min(full - r.t.leaf0, u64{32})) : 0u;
+    const std::uint8_t* p0 = tk.src + r.t.leaf0 * kLeafBytes;
+    r.t.o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p0) & 15);
+    r.t.a0 = p0 - r.t.o;
+    r.dst = tk.dst;
+    const u32 od = static_cast<u32>(reinterpret_cast<std::uintptr_t>(tk.dst) & 15);
+    r.delta = (r.t.o - od) & 15;
+    // first x >= 0 on the grid x ≡ delta - o (mod 16); last with x + 16 <= 4096 F
+    const long long x0 = static_cast<long long>(r.delta) - static_cast<long long>(r.t.o);
+    r.x_first = static_cast<u64>(x0 < 0 ? x0 + 16 : x0);
+    const u64 lim = full * kLeafBytes;
+    r.x_end = lim >= r.x_first + 16 ? r.x_first + ((lim - r.x_first) / 16) * 16 : r.x_first;
+    return r;
+}
+
+template <int QD>
+__device__ __forceinline__ uint4 realign_words(uint4 w0, uint4 w1, u32 r8) {
+    const u32 u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    return make_uint4(__funnelshift_r(u[QD + 0], u[QD + 1], r8), __funnelshift_r(u[QD + 1], u[QD + 2], r8),
+                      __funnelshift_r(u[QD + 2], u[QD + 3], r8), __funnelshift_r(u[QD + 3], u[QD + 4], r8));
+}
+
+// Write this stage's destination words: lane -> leaf 4i + lane/8, word lane%8.
+__device__ __forceinline__ void write_stage(const uint4* stage_buf, const CopyTileRef& c, int s, u32 lane) {
+    const u32 g = lane >> 3, q = lane & 7;
+    const u32 qd = c.delta >> 2, r8 = (c.delta & 3) * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const u32 l = 4 * i + g;
+        if (l >= c.t.nfull) continue;
+        const u64 leaf = c.t.leaf0 + l;
+        const long long x = static_cast<long long>(leaf * kLeafBytes + static_cast<u64>(s) * 128 + q * 16 + c.delta) -
+                            static_cast<long long>(c.t.o);
+        if (x < static_cast<long long>(c.x_first) || static_cast<u64>(x) + 16 > c.x_end) continue;
+        const u32 key = l & 7;
+        const uint4 w0 = stage_buf[l * 8 + (q ^ key)];
+        const uint4 w1 = q == 7 ? stage_buf[32 * kStageBlocks + l] : stage_buf[l * 8 + ((q + 1) ^ key)];
+        uint4 v;
+        switch (qd) {
+            case 0: v = realign_words<0>(w0, w1, r8); break;
+            case 1: v = realign_words<1>(w0, w1, r8); break;
+            case 2: v = realign_words<2>(w0, w1, r8); break;
+            default: v = realign_words<3>(w0, w1, r8); break;
+        }
+        __stcs(reinterpret_cast<uint4*>(c.dst + x), v);
+    }
+}
+
+// The extra (9th) word of every leaf-stage is needed by the writes whenever
+// delta > 0, by the hash whenever o > 0; load it when it holds a tensor byte.
+__device__ __forceinline__ void copy_issue(uint4* stage_buf, const CopyTileRef& c, int s, u32 lane) {
+    const TileRef& tr = c.t;
+    if (tr.task < 0 || tr.nfull == 0) {
+        cp_async_commit();
+        return;
+    }
+    const std::uint8_t* src_lane =
+        tr.a0 + static_cast<u64>(lane >> 3) * kLeafBytes + (lane & 7) * 16 + static_cast<u64>(s) * 128;
+    const u64 extra_word = (tr.leaf0 + lane) * kLeafBytes + static_cast<u64>(s) * 128 + 128;  // tensor offset + o
+    const bool extra = (tr.o != 0 || c.delta != 0) && extra_word - tr.o < tr.n;
+    const std::uint8_t* src_extra = tr.a0 + static_cast<u64>(lane) * kLeafBytes + static_cast<u64>(s) * 128 + 128;
+    // v3_issue loads the extra column for lanes < nfull when `extra`
+    const u32 leaf_in_group = lane >> 3, q = lane & 7;
+    if (tr.nfull == 32) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const u32 key = ((4 * i) & 7) ^ leaf_in_group;
+            cp_async16(stage_buf + (4 * i + leaf_in_group) * 8 + (q ^ key), src_lane + static_cast<u64>(i) * 16384);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const u32 l = 4 * i + leaf_in_group;
+            if (l < tr.nfull) cp_async16(stage_buf + l * 8 + (q ^ (l & 7)), src_lane + static_cast<u64>(i) * 16384);
+        }
+    }
+    if (extra && lane < tr.nfull) cp_async16(stage_buf + 32 * kStageBlocks + lane, src_extra);
+    cp_async_commit();
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
+    copy_fp_kernel(const CopyFpTask* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums) {
+    extern __shared__ uint4 smem[];
+    const u32 lane = threadIdx.x & 31;
+    const u32 wid = threadIdx.x >> 5;
+    uint4* wbuf = smem + wid * kV3WarpWords;
+    const u64 nwarps = static_cast<u64>(gridDim.x) * kWarpsPerCta;
+    u64 t = static_cast<u64>(blockIdx.x) * kWarpsPerCta + wid;
+    if (t >= total_tiles) return;
+    CopyTileRef cur = copy_tile_ref(tasks, n_tasks, t, total_tiles);
+    CopyTileRef nxt = copy_tile_ref(tasks, n_tasks, t + nwarps, total_tiles);
+    int cur_task = -1;
+    u64 acc_h = 0, acc_l = 0;
+    u32 buf = 0;
+    constexpr int kAhead = kV3Stages - 1;
+#pragma unroll
+    for (int s = 0; s < kAhead; ++s) copy_issue(wbuf + s * kV3StageWords, cur, s, lane);
+    while (cur.t.task >= 0) {
+        if (cur.t.task != cur_task) {
+            if (cur_task >= 0) {
+                const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
+                if (lane == 0) {
+                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task), sh);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task + 1), sl);
+                }
+            }
+            cur_task = cur.t.task;
+            acc_h = acc_l = 0;
+        }
+        const u64 my_leaf = cur.t.leaf0 + lane;
+        mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
+        for (int s = 0; s < kStagesPerLeaf; ++s) {
+            const int ahead = s + kAhead;
+            u32 fill = buf + kAhead;
+            fill = fill >= kV3Stages ? fill - kV3Stages : fill;
+            if (ahead < kStagesPerLeaf) copy_issue(wbuf + fill * kV3StageWords, cur, ahead, lane);
+            else copy_issue(wbuf + fill * kV3StageWords, nxt, ahead - kStagesPerLeaf, lane);
+            cp_async_wait<kV3Stages - 1>();
+            __syncwarp();
+            const uint4* sb = wbuf + buf * kV3StageWords;
+            if (cur.t.nfull) write_stage(sb, cur, s, lane);
+            if (lane < cur.t.nfull) v4_hash(sb, cur.t, lane, h1, h2);
+            __syncwarp();
+            buf = buf + 1 == kV3Stages ? 0 : buf + 1;
+        }
+        if (lane < cur.t.nfull) {
+            u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
+            mm::finish(f1, f2, 0, 0, 0, kLeafBytes);
+            acc_h += f1;
+            acc_l += f2;
+        } else if (lane == cur.t.nfull && my_leaf * kLeafBytes < cur.t.n) {
+            const u32 len = static_cast<u32>(cur.t.n - my_leaf * kLeafBytes);
+            u64 d1, d2;
+            leaf_digest(cur.t.base + my_leaf * kLeafBytes, len, my_leaf, d1, d2);
+            acc_h += d1;
+            acc_l += d2;
+        }
+        // the tensor's last tile also copies the head and tail bytes
+        if (cur.t.leaf0 + 32 >= (cur.t.n + kLeafBytes - 1) / kLeafBytes) {
+            const std::uint8_t* src = cur.t.base;
+            for (u64 b = lane; b < cur.x_first && b < cur.t.n; b += 32) cur.dst[b] = src[b];
+            for (u64 b = cur.x_end + lane; b < cur.t.n; b += 32) cur.dst[b] = src[b];
+        }
+        t += nwarps;
+        cur = nxt;
+        nxt = copy_tile_ref(tasks, n_tasks, t + nwarps, total_tiles);
+    }
+    cp_async_wait<0>();
+    if (cur_task >= 0) {
+        const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
+        if (lane == 0) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task), sh);
+            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task + 1), sl);
+        }
+    }
+}
+
+__global__ void copy_fp_finalize_kernel(const CopyFpTask* __restrict__ tasks, u32 n_tasks,
+                                        const u64* __restrict__ sums, u64* __restrict__ digests) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_tasks) return;
+    u64 h1 = 0, h2 = 0;
+    mm::body(h1, h2, sums[2 * i], sums[2 * i + 1]);
+    mm::finish(h1, h2, tasks[i].n, 0, 8, 24);
+    digests[2 * i] = h1;
+    digests[2 * i + 1] = h2;
+}
+
 }  // namespace
+
+void copy_fp_launch(const CopyFpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests,
+                    int sm_count, cudaStream_t s) {
+    if (n_tasks == 0) return;
+    if (total_tiles > 0) {
+        static const bool attr = [] {
+            return cudaFuncSetAttribute(copy_fp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV3SmemBytes) ==
+                   cudaSuccess;
+        }();
+        (void)attr;
+        const u64 want = (total_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
+        const u64 cap = static_cast<u64>(sm_count) * 2;
+        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
+        copy_fp_kernel<<<blocks, kWarpsPerCta * 32, kV3SmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
+        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    copy_fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
 
 void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, int sm_count,
                cudaStream_t s) {

@@ -28,6 +28,19 @@ struct FpTask {
 void fp_launch(const FpTask* d_tasks, std::uint32_t n_tasks, std::uint64_t total_tiles, std::uint64_t* d_sums,
                std::uint64_t* d_digests, int sm_count, cudaStream_t s);
 
+// ---- K3F: copy + fingerprint in one pass ----------------------------------
+// Moves every task's n bytes src -> dst (any alignments; the tasks of one
+// launch must be hazard-free, e.g. one WAR wave) and produces the tgfp1
+// digest of the moved bytes, reading them once.
+struct CopyFpTask {
+    const std::uint8_t* src;
+    std::uint8_t* dst;
+    std::uint64_t n;
+    std::uint64_t tile0;  // tile prefix (32 leaves per tile), relative to the launch
+};
+void copy_fp_launch(const CopyFpTask* d_tasks, std::uint32_t n_tasks, std::uint64_t total_tiles, std::uint64_t* d_sums,
+                    std::uint64_t* d_digests, int sm_count, cudaStream_t s);
+
 // ---- K3: relocation wave (batched misaligned memcpy) ---------------------
 constexpr int kMaxMovesPerLaunch = 96;
 struct MoveDesc {

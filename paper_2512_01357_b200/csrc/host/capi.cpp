@@ -618,6 +618,18 @@ int tg_bench_fingerprint(const void* const* dptrs, const uint64_t* ns, uint32_t 
         return 0;
     });
 }
+int tg_copy_fingerprint(const uint64_t* triples, uint32_t n_moves, int32_t device, int32_t reps, double* ms,
+                        tg_digest* out) {
+    return guard([&] {
+        std::vector<MoveDesc> mv;
+        for (uint32_t i = 0; i < n_moves; ++i) mv.push_back(MoveDesc{triples[3 * i], triples[3 * i + 1], triples[3 * i + 2]});
+        std::vector<Digest> d;
+        const double t = bench_copy_fp(mv, device, reps < 0 ? 0 : reps, &d);
+        if (ms) *ms = t;
+        for (uint32_t i = 0; out && i < n_moves; ++i) out[i] = tg_digest{d[i].hi, d[i].lo};
+        return 0;
+    });
+}
 int tg_bench_relocate(const uint64_t* triples /*src,dst,len*/, uint32_t n_moves, int32_t device, int32_t reps,
                       double* ms) {
     return guard([&] {

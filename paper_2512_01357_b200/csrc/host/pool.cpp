@@ -200,95 +200,141 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     // ---- event layout -----------------------------------------------------------
     // 0 t0 | 1 reloc start | 2 reloc end | 3 end | 4 h2d start | 5 h2d end | 6 peer start | 7 peer end
     // 8 verify joined | 9.. wave ends (waves) | then per placement "bytes landed" | then fp start/end pairs
+    const bool fused = (flags & kLoadFused) != 0;
     const std::size_t ev_wave = 9, ev_land = ev_wave + waves, ev_fp = ev_land + np;
     const bool fp_new = flags & kLoadFingerprintNew, fp_reuse = (flags & kLoadVerifyReuse) && !hit_keys.empty();
-    const std::size_t n_fp_launch = (fp_new ? np : 0) + (fp_reuse ? 2 : 0);
-    ensure_events(ev_fp + 2 * n_fp_launch);
-    // Reused tensors that no relocation touches are verified right away, in
-    // parallel with the waves; relocated ones after the waves at their new
-    // offsets.  hit_keys is reordered [untouched..., relocated...].
-    std::size_t n_still = 0;
+    // Reused tensors no relocation touches are verified right away on the
+    // verify stream, in parallel with the waves.  Relocated ones are verified
+    // by the copy+fingerprint (K3F) of their wave — or, unfused, by a K1
+    // launch after the waves.  hit_keys is reordered [untouched..., relocated...].
+    std::unordered_map<Key, std::size_t, KeyHash> reloc_of;
+    for (std::size_t j = 0; j < rel.size(); ++j) reloc_of.emplace(rel[j].tensor, j);
+    std::size_t n_still = hit_keys.size();
     if (fp_reuse) {
-        std::unordered_set<Key, KeyHash> moved;
-        for (const Move& r : rel) moved.insert(r.tensor);
         auto mid = std::stable_partition(hit_keys.begin(), hit_keys.end(),
-                                         [&](const Key& k) { return !moved.count(k); });
+                                         [&](const Key& k) { return !reloc_of.count(k); });
         n_still = static_cast<std::size_t>(mid - hit_keys.begin());
     }
+    // K1 after landing: host-sourced placements always; device-sourced ones
+    // only when unfused (fused: K3F hashes them while it copies)
+    auto k1_placement = [&](std::size_t i) { return fp_new && (!fused || rep->placement_src[i] == 0); };
+    auto tiles_of = [](u64 n) { return ((n + kLeafBytes - 1) / kLeafBytes + kLeavesPerTile - 1) / kLeavesPerTile; };
+    constexpr std::size_t kNone = ~std::size_t{0};
 
-    // ---- fingerprint task table (one H2D of descriptors) -------------------------
-    // tasks: [placements (one launch each)] [hits (one launch)]
+    // ---- descriptor tables (one H2D) ---------------------------------------------
+    // FpTask:     [K1 placements...][untouched hits...][relocated hits (unfused)...]
+    // CopyFpTask: [wave 0 moves...][wave 1 moves...]...[device-source placements...] (fused)
     std::vector<FpTask> tasks;
-    for (std::size_t i = 0; i < np && fp_new; ++i) {
+    std::vector<std::size_t> fp_of_placement(np, kNone);
+    std::vector<u64> new_tiles;
+    for (std::size_t i = 0; i < np; ++i) {
+        if (!k1_placement(i)) continue;
         const auto& pl = D.plan.placements[i];
+        fp_of_placement[i] = tasks.size();
         tasks.push_back(FpTask{arena_ + pl.off, D.miss_desc[pl.tensor].size, 0});
+        new_tiles.push_back(tiles_of(tasks.back().n));
     }
-    std::vector<FpTask> hit_tasks;
+    const std::size_t hit_base = tasks.size();
+    std::vector<FpTask> still, moved_hits;
     if (fp_reuse)
-        for (const Key& k : hit_keys) {
-            const Entry* e = store_.entry(k);
-            hit_tasks.push_back(FpTask{arena_ + e->off, e->size, 0});
+        for (std::size_t h = 0; h < hit_keys.size(); ++h) {
+            const Entry* e = store_.entry(hit_keys[h]);
+            (h < n_still ? still : moved_hits).push_back(FpTask{arena_ + e->off, e->size, 0});
         }
-    std::vector<FpTask> still(hit_tasks.begin(), hit_tasks.begin() + static_cast<long>(n_still));
-    std::vector<FpTask> moved_hits(hit_tasks.begin() + static_cast<long>(n_still), hit_tasks.end());
     const u64 still_tiles = build_tasks(still), moved_tiles = build_tasks(moved_hits);
-    std::copy(still.begin(), still.end(), hit_tasks.begin());
-    std::copy(moved_hits.begin(), moved_hits.end(), hit_tasks.begin() + static_cast<long>(n_still));
-    std::vector<u64> new_tiles(tasks.size());
-    for (std::size_t i = 0; i < tasks.size(); ++i) {
-        std::vector<FpTask> one{tasks[i]};
-        new_tiles[i] = build_tasks(one);
+    tasks.insert(tasks.end(), still.begin(), still.end());
+    if (!fused) tasks.insert(tasks.end(), moved_hits.begin(), moved_hits.end());
+    std::vector<CopyFpTask> ctasks;
+    std::vector<std::size_t> ctask_of_reloc(rel.size(), kNone), ctask_of_placement(np, kNone);
+    std::vector<std::size_t> wave_first(waves + 1, 0);
+    std::vector<u64> wave_tiles(waves, 0);
+    if (fused) {
+        for (u32 w = 0; w < waves; ++w) {
+            wave_first[w] = ctasks.size();
+            u64 tl = 0;
+            for (std::size_t j = 0; j < rel.size(); ++j) {
+                if (rep->reloc_wave[j] != w) continue;
+                ctask_of_reloc[j] = ctasks.size();
+                ctasks.push_back(CopyFpTask{arena_ + rel[j].from, arena_ + rel[j].to, rel[j].size, tl});
+                tl += tiles_of(rel[j].size);
+            }
+            wave_tiles[w] = tl;
+        }
+        wave_first[waves] = ctasks.size();
+        for (std::size_t i = 0; i < np; ++i) {
+            if (rep->placement_src[i] == 0) continue;
+            const auto& pl = D.plan.placements[i];
+            ctask_of_placement[i] = ctasks.size();
+            ctasks.push_back(CopyFpTask{peer_src[i], arena_ + pl.off, D.miss_desc[pl.tensor].size, 0});
+        }
     }
-    const std::size_t n_tasks = tasks.size() + hit_tasks.size();
-    const std::size_t desc_bytes = n_tasks * sizeof(FpTask), sums_bytes = n_tasks * 2 * sizeof(u64);
+    const std::size_t nf = tasks.size(), nc = ctasks.size();
+    std::size_t n_fp_launch = 2;
+    for (std::size_t i = 0; i < np; ++i) n_fp_launch += fp_of_placement[i] != kNone;
+    ensure_events(ev_fp + 2 * n_fp_launch);
+    const std::size_t fdesc = nf * sizeof(FpTask), cdesc = nc * sizeof(CopyFpTask);
+    const std::size_t desc_bytes = (fdesc + cdesc + 15) & ~std::size_t{15};
+    const std::size_t sums_bytes = (nf + nc) * 2 * sizeof(u64);
     ensure_stage(desc_bytes + 2 * sums_bytes + 64);
     auto* h = static_cast<std::uint8_t*>(h_stage_);
     auto* dptr = static_cast<std::uint8_t*>(d_stage_);
-    std::memcpy(h, tasks.data(), tasks.size() * sizeof(FpTask));
-    std::memcpy(h + tasks.size() * sizeof(FpTask), hit_tasks.data(), hit_tasks.size() * sizeof(FpTask));
+    if (nf) std::memcpy(h, tasks.data(), fdesc);
+    if (nc) std::memcpy(h + fdesc, ctasks.data(), cdesc);
     const auto* d_tasks = reinterpret_cast<const FpTask*>(dptr);
+    const auto* d_ctasks = reinterpret_cast<const CopyFpTask*>(dptr + fdesc);
     auto* d_sums = reinterpret_cast<u64*>(dptr + desc_bytes);
     auto* d_dig = reinterpret_cast<u64*>(dptr + desc_bytes + sums_bytes);
-    if (n_tasks) {
+    if (nf + nc) {
         TG_CUDA(cudaMemcpyAsync(dptr, h, desc_bytes, cudaMemcpyHostToDevice, s_main_));
         TG_CUDA(cudaMemsetAsync(d_sums, 0, sums_bytes, s_main_));
     }
 
-    // ---- relocation waves on the main stream (K3) ---------------------------------
+    // ---- relocation waves on the main stream (K3F, or K3 unfused) ----------------
     TG_CUDA(cudaEventRecord(ev(1), s_main_));
     for (u32 w = 0; w < waves; ++w) {
-        std::vector<MoveDesc> mv;
-        for (std::size_t j = 0; j < rel.size(); ++j)
-            if (rep->reloc_wave[j] == w)
-                mv.push_back(MoveDesc{reinterpret_cast<u64>(arena_ + rel[j].from), reinterpret_cast<u64>(arena_ + rel[j].to),
-                                      rel[j].size});
-        relocate_launch(mv.data(), static_cast<int>(mv.size()), sm_count_, s_main_);
+        if (fused) {
+            const std::size_t c0 = wave_first[w], cn = wave_first[w + 1] - c0;
+            copy_fp_launch(d_ctasks + c0, static_cast<u32>(cn), wave_tiles[w], d_sums + 2 * (nf + c0),
+                           d_dig + 2 * (nf + c0), sm_count_, s_main_);
+        } else {
+            std::vector<MoveDesc> mv;
+            for (std::size_t j = 0; j < rel.size(); ++j)
+                if (rep->reloc_wave[j] == w)
+                    mv.push_back(MoveDesc{reinterpret_cast<u64>(arena_ + rel[j].from),
+                                          reinterpret_cast<u64>(arena_ + rel[j].to), rel[j].size});
+            relocate_launch(mv.data(), static_cast<int>(mv.size()), sm_count_, s_main_);
+        }
         TG_CUDA(cudaGetLastError());
         TG_CUDA(cudaEventRecord(ev(ev_wave + w), s_main_));
     }
     TG_CUDA(cudaEventRecord(ev(2), s_main_));
 
-    // ---- placements: host→device on the copy stream, peer pulls on the peer stream
-    // Independent placements first, then those gated on a relocation wave.
+    // ---- placements: host→device on the copy stream, device sources (peer pool,
+    // HBM cache) on the peer stream.  Independent placements first, then those
+    // gated on a relocation wave.
     std::vector<std::size_t> order(np);
     for (std::size_t i = 0; i < np; ++i) order[i] = i;
     std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) { return dep[a] < dep[b]; });
-    TG_CUDA(cudaStreamWaitEvent(s_copy_, ev(0)));  // descriptor H2D / memset ordered before
-    TG_CUDA(cudaStreamWaitEvent(s_peer_, ev(0)));
+    TG_CUDA(cudaStreamWaitEvent(s_copy_, ev(0)));
+    TG_CUDA(cudaStreamWaitEvent(s_peer_, ev(1)));  // K3F reads its descriptors
     TG_CUDA(cudaEventRecord(ev(4), s_copy_));
     TG_CUDA(cudaEventRecord(ev(6), s_peer_));
     int waited_copy = -1, waited_peer = -1;
     for (std::size_t i : order) {
         const auto& pl = D.plan.placements[i];
         const u64 sz = D.miss_desc[pl.tensor].size;
-        const bool peer = rep->placement_src[i] != 0;
-        cudaStream_t s = peer ? s_peer_ : s_copy_;
-        int& waited = peer ? waited_peer : waited_copy;
+        const bool dev_src = rep->placement_src[i] != 0;
+        cudaStream_t s = dev_src ? s_peer_ : s_copy_;
+        int& waited = dev_src ? waited_peer : waited_copy;
         if (dep[i] > waited) {
             TG_CUDA(cudaStreamWaitEvent(s, ev(ev_wave + dep[i])));
             waited = dep[i];
         }
-        if (peer) {
+        if (dev_src && fused) {
+            const std::size_t c = ctask_of_placement[i];
+            copy_fp_launch(d_ctasks + c, 1, tiles_of(sz), d_sums + 2 * (nf + c), d_dig + 2 * (nf + c), sm_count_, s);
+            TG_CUDA(cudaGetLastError());
+        } else if (dev_src) {
             MoveDesc md{reinterpret_cast<u64>(peer_src[i]), reinterpret_cast<u64>(arena_ + pl.off), sz};
             relocate_launch(&md, 1, sm_count_, s);
             TG_CUDA(cudaGetLastError());
@@ -302,49 +348,49 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
 
     // ---- K1 over placed tensors, trailing the copies ------------------------------
     std::size_t fp_i = 0;
-    if (fp_new) {
-        TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(1)));  // descriptors uploaded, sums zeroed
-        for (std::size_t i : order) {
-            TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(ev_land + i)));
-            TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s_fp_));
-            fp_launch(d_tasks + i, 1, new_tiles[i], d_sums + 2 * i, d_dig + 2 * i, sm_count_, s_fp_);
-            TG_CUDA(cudaGetLastError());
-            TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s_fp_));
-            ++fp_i;
-        }
+    bool fp_stream_used = false;
+    TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(1)));  // descriptors uploaded, sums zeroed
+    for (std::size_t i : order) {
+        const std::size_t k = fp_of_placement[i];
+        if (k == kNone) continue;
+        TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(ev_land + i)));
+        TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s_fp_));
+        fp_launch(d_tasks + k, 1, new_tiles[k], d_sums + 2 * k, d_dig + 2 * k, sm_count_, s_fp_);
+        TG_CUDA(cudaGetLastError());
+        TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s_fp_));
+        ++fp_i;
+        fp_stream_used = true;
     }
-    // ---- K1 over reused tensors: untouched ones now (verify stream), relocated
-    // ones at their final offsets after the waves (main stream) -------------------
-    std::size_t fp_reuse_slot = 0, fp_reuse_launches = 0;
+    // ---- K1 over reused tensors: untouched ones now (verify stream); relocated
+    // ones after the waves (main stream) unless K3F already hashed them --------
+    std::size_t fp_reuse_slot = fp_i, fp_reuse_launches = 0;
     if (fp_reuse) {
-        fp_reuse_slot = fp_i;
-        const std::size_t base = tasks.size();
         auto launch = [&](cudaStream_t s, std::size_t first, std::size_t count, u64 tiles) {
             if (!count) return;
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s));
-            fp_launch(d_tasks + base + first, static_cast<u32>(count), tiles, d_sums + 2 * (base + first),
-                      d_dig + 2 * (base + first), sm_count_, s);
+            fp_launch(d_tasks + first, static_cast<u32>(count), tiles, d_sums + 2 * first, d_dig + 2 * first,
+                      sm_count_, s);
             TG_CUDA(cudaGetLastError());
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s));
             ++fp_i;
             ++fp_reuse_launches;
         };
-        TG_CUDA(cudaStreamWaitEvent(s_verify_, ev(1)));  // descriptors uploaded, sums zeroed
-        launch(s_verify_, 0, n_still, still_tiles);
-        launch(s_main_, n_still, hit_tasks.size() - n_still, moved_tiles);
+        TG_CUDA(cudaStreamWaitEvent(s_verify_, ev(1)));
+        launch(s_verify_, hit_base, n_still, still_tiles);
+        if (!fused) launch(s_main_, hit_base + n_still, hit_keys.size() - n_still, moved_tiles);
         TG_CUDA(cudaEventRecord(ev(8), s_verify_));
         TG_CUDA(cudaStreamWaitEvent(s_main_, ev(8)));
     }
     // ---- join, read digests, end ------------------------------------------------
     TG_CUDA(cudaStreamWaitEvent(s_main_, ev(5)));
     TG_CUDA(cudaStreamWaitEvent(s_main_, ev(7)));
-    if (fp_new && !tasks.empty()) {
+    if (fp_stream_used) {
         TG_CUDA(cudaEventRecord(ev(3), s_fp_));
         TG_CUDA(cudaStreamWaitEvent(s_main_, ev(3)));
     }
     TG_CUDA(cudaEventRecord(ev(3), s_main_));
     auto* h_dig = reinterpret_cast<u64*>(h + desc_bytes + sums_bytes);
-    if (n_tasks) TG_CUDA(cudaMemcpyAsync(h_dig, d_dig, sums_bytes, cudaMemcpyDeviceToHost, s_main_));
+    if (nf + nc) TG_CUDA(cudaMemcpyAsync(h_dig, d_dig, sums_bytes, cudaMemcpyDeviceToHost, s_main_));
     TG_CUDA(cudaStreamSynchronize(s_main_));
 
     rep->t.total_ms = ms_between(ev(0), ev(3));
@@ -361,12 +407,17 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     }
 
     // ---- record / verify digests ----------------------------------------------
+    auto digest_at = [&](std::size_t slot) { return Digest{h_dig[2 * slot], h_dig[2 * slot + 1]}; };
     rep->digests.assign(m.tensors.size(), Digest{});
     std::unordered_map<Key, std::size_t, KeyHash> pos;
     for (std::size_t i = 0; i < m.tensors.size(); ++i) pos.emplace(m.tensors[i].id, i);
-    for (std::size_t i = 0; i < tasks.size(); ++i) {
+    for (std::size_t i = 0; i < np; ++i) {
+        std::size_t slot = kNone;
+        if (fp_of_placement[i] != kNone) slot = fp_of_placement[i];
+        else if (ctask_of_placement[i] != kNone) slot = nf + ctask_of_placement[i];
+        if (slot == kNone) continue;
         const TensorDesc& t = D.miss_desc[D.plan.placements[i].tensor];
-        const Digest g{h_dig[2 * i], h_dig[2 * i + 1]};
+        const Digest g = digest_at(slot);
         Entry* e = store_.entry(t.id);
         e->digest = g;
         e->has_digest = true;
@@ -387,9 +438,10 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             rep->digests[pos[t.id]] = e->digest;
         }
     }
-    for (std::size_t i = 0; i < hit_tasks.size(); ++i) {
-        const Key& k = hit_keys[i];
-        const Digest g{h_dig[2 * (tasks.size() + i)], h_dig[2 * (tasks.size() + i) + 1]};
+    for (std::size_t hix = 0; fp_reuse && hix < hit_keys.size(); ++hix) {
+        const Key& k = hit_keys[hix];
+        const std::size_t slot = (hix < n_still || !fused) ? hit_base + hix : nf + ctask_of_reloc[reloc_of.at(k)];
+        const Digest g = digest_at(slot);
         Entry* e = store_.entry(k);
         rep->digests[pos[k]] = g;
         rep->fingerprint_bytes += e->size;
@@ -400,7 +452,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             HostSource hs;
             if (!SourceRegistry::get().find(k, &hs) || hs.size != e->size)
                 throw DeviceError(kErrVerify, "reused tensor " + k.hex() + " fails verification and has no host source");
-            TG_CUDA(cudaMemcpyAsync(arena_ + e->off, hs.ptr, e->size, cudaMemcpyHostToDevice, s_main_));
+            TG_CUDA(cudaMemcpyAsync(arena_ + e->off, hs.ptr, e->size, cudaMemcpyDefault, s_main_));
             TG_CUDA(cudaStreamSynchronize(s_main_));
             rep->repaired_bytes += e->size;
             e->digest = fingerprint_resident(k);
@@ -611,6 +663,54 @@ double bench_fingerprint(const std::vector<std::pair<const void*, u64>>& bufs, i
         for (u32 i = 0; i < nt; ++i) out->push_back(Digest{h[2 * i], h[2 * i + 1]});
     }
     return ms / reps;
+}
+
+// K3F over hazard-free moves: one warm-up launch (whose digests are returned)
+// then `reps` timed launches; returns ms per launch (0 when reps == 0).
+double bench_copy_fp(const std::vector<MoveDesc>& moves, int device, int reps, std::vector<Digest>* out) {
+    DeviceScope ds(device);
+    int sms = 148;
+    TG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    std::vector<CopyFpTask> t;
+    u64 tiles = 0;
+    for (const MoveDesc& m : moves) {
+        t.push_back(CopyFpTask{reinterpret_cast<const std::uint8_t*>(m.src), reinterpret_cast<std::uint8_t*>(m.dst),
+                               m.len, tiles});
+        tiles += ((m.len + kLeafBytes - 1) / kLeafBytes + kLeavesPerTile - 1) / kLeavesPerTile;
+    }
+    const u32 nt = static_cast<u32>(t.size());
+    cudaStream_t s;
+    TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    void* d = nullptr;
+    const std::size_t per = 4 * sizeof(u64) * nt;
+    TG_CUDA(cudaMalloc(&d, sizeof(CopyFpTask) * nt + per * (reps + 1)));
+    TG_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(CopyFpTask) * nt, cudaMemcpyHostToDevice, s));
+    auto* sums = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(d) + sizeof(CopyFpTask) * nt);
+    TG_CUDA(cudaMemsetAsync(sums, 0, per * (reps + 1), s));
+    auto rep_sums = [&](int r) { return sums + static_cast<std::size_t>(r) * 4 * nt; };
+    const auto* dt = static_cast<const CopyFpTask*>(d);
+    copy_fp_launch(dt, nt, tiles, rep_sums(0), rep_sums(0) + 2 * nt, sms, s);
+    cudaEvent_t a, b;
+    TG_CUDA(cudaEventCreate(&a));
+    TG_CUDA(cudaEventCreate(&b));
+    TG_CUDA(cudaEventRecord(a, s));
+    for (int r = 1; r <= reps; ++r) copy_fp_launch(dt, nt, tiles, rep_sums(r), rep_sums(r) + 2 * nt, sms, s);
+    TG_CUDA(cudaEventRecord(b, s));
+    TG_CUDA(cudaGetLastError());
+    std::vector<u64> h(2 * nt);
+    TG_CUDA(cudaMemcpyAsync(h.data(), rep_sums(0) + 2 * nt, 2 * nt * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    TG_CUDA(cudaStreamSynchronize(s));
+    float ms = 0;
+    TG_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d);
+    cudaStreamDestroy(s);
+    if (out) {
+        out->clear();
+        for (u32 i = 0; i < nt; ++i) out->push_back(Digest{h[2 * i], h[2 * i + 1]});
+    }
+    return reps ? ms / reps : 0.0;
 }
 
 double bench_relocate(const std::vector<MoveDesc>& moves, int device, int reps) {

@@ -62,6 +62,12 @@ struct RemoteEntry {
 constexpr u32 kLoadVerifyReuse = 1u;     // fingerprint reused tensors, compare to the recorded digest
 constexpr u32 kLoadFingerprintNew = 2u;  // fingerprint placed tensors and record the digest
 constexpr u32 kLoadPeer = 4u;            // pull misses from peer pools that hold them
+// Opt-in: move + fingerprint relocated / device-sourced tensors in one pass
+// (K3F).  It reads those bytes once instead of twice, but per-lane hashing
+// makes it issue-bound (4.9 TB/s r+w alone vs 6.2 for K3 and 6.0 for K1), and
+// in the C2 step it measured 9.9 ms against 9.4 ms for the separate passes,
+// so the separate passes stay the default.
+constexpr u32 kLoadFused = 8u;
 constexpr u32 kLoadDefault = kLoadVerifyReuse | kLoadFingerprintNew;
 
 struct LoadTimings {
@@ -161,5 +167,6 @@ void synth_fill_device(const Key& k, u64 begin, u64 len, void* dst, int device);
 double bench_fingerprint(const std::vector<std::pair<const void*, u64>>& bufs, int device, int reps,
                          std::vector<Digest>* out);
 double bench_relocate(const std::vector<MoveDesc>& moves, int device, int reps);
+double bench_copy_fp(const std::vector<MoveDesc>& moves, int device, int reps, std::vector<Digest>* out);
 
 }  // namespace tg

@@ -58,8 +58,9 @@ def _check_pooled_bytes(tg, cpu, pool, expected_cache):
         assert pool.tensor_info(tid)["digest"] == expected_cache[tid]
 
 
+@pytest.mark.parametrize("fused", [False, True], ids=["K3+K1", "K3F"])
 @pytest.mark.parametrize("case,merge", [("pg_32", 0), ("gm_36", 1)])
-def test_c2_switch_bytes_and_decisions(tg, cpu, case, merge):
+def test_c2_switch_bytes_and_decisions(tg, cpu, case, merge, fused):
     g = json.load(open(os.path.join(GOLDEN, "c1_c2_loads.json")))[case]
     gib = int(case.split("_")[1])
     cat = {m.model_id: m for m in tg.default_catalog()}
@@ -72,7 +73,8 @@ def test_c2_switch_bytes_and_decisions(tg, cpu, case, merge):
         for i, mid in enumerate(seq):
             stats.record_request(mid, 10.0 * i)
             stats.set_load_bandwidth(mid, 55e9)
-            r = pool.load_model(cat[mid], stats, 10.0 * i, tg.LoadPolicy(merge=merge))
+            r = pool.load_model(cat[mid], stats, 10.0 * i,
+                                tg.LoadPolicy(merge=merge, flags=1 | 2 | (8 if fused else 0)))
             assert result_json(r) == g["loads"][i], f"load {i}"
             o = r.value()
             assert o.verify_mismatches == 0 and o.repaired_bytes == 0
@@ -152,7 +154,8 @@ def test_snapshot_restore_roundtrip(tg):
     pool.close()
 
 
-def test_peer_pull_same_device(tg, cpu):
+@pytest.mark.parametrize("fused", [False, True], ids=["K3+K1", "K3F"])
+def test_peer_pull_same_device(tg, cpu, fused):
     """Misses resident in a peer pool are pulled device-to-device (K5 path;
     on one GPU the peer is a second pool on the same device)."""
     from paper_2512_01357_b200.checkpoint import HostCheckpoint
@@ -164,7 +167,7 @@ def test_peer_pull_same_device(tg, cpu):
     with HostCheckpoint([m]) as ck:
         oa = a.load_model(m, sa, 0.0).value()
         assert b.peer_reuse_size(m) == m.total_size
-        ob = b.load_model(m, sb, 0.0, tg.LoadPolicy(flags=1 | 2 | 4)).value()
+        ob = b.load_model(m, sb, 0.0, tg.LoadPolicy(flags=1 | 2 | 4 | (8 if fused else 0))).value()
         assert ob.peer_bytes == m.total_size and ob.pcie_bytes == 0
         assert all(p.source == 1 for p in ob.plan.placements)
         assert ob.digests == oa.digests

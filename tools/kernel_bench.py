@@ -4,7 +4,7 @@ Kernel-only timing (tg_bench_*: reps back-to-back launches bracketed by CUDA
 events on the launching stream, after a warm-up launch); inputs >> L2.
 Prints one JSON object.
 
-    python tools/kernel_bench.py [--gib 16] [--only fp|reloc] [--reps 5]
+    python tools/kernel_bench.py [--gib 16] [--only fp|reloc]  (reloc also times the fused K3F) [--reps 5]
 """
 import argparse
 import ctypes as C
@@ -58,6 +58,14 @@ def main():
             N.check_runtime(lib.tg_bench_relocate(mv, 1, dev, args.reps, C.byref(ms)), "bench reloc")
             res[f"src{so}_dst{do}"] = {"ms": ms.value, "GBps_rw": 2 * size / ms.value / 1e6}
         out["reloc"] = {"bytes_per_launch": size, **res}
+        res = {}
+        for so, do in ((0, 0), (3, 11), (13, 2)):
+            ms = C.c_double()
+            mv = (C.c_uint64 * 3)(a.ptr + so, b.ptr + do, size)
+            dg = (N.DigestC * 1)()
+            N.check_runtime(lib.tg_copy_fingerprint(mv, 1, dev, args.reps, C.byref(ms), dg), "bench K3F")
+            res[f"src{so}_dst{do}"] = {"ms": ms.value, "GBps_rw": 2 * size / ms.value / 1e6}
+        out["copy_fp"] = {"bytes_per_launch": size, **res}
         a.free()
         b.free()
     print(json.dumps(out))
