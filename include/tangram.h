@@ -263,6 +263,12 @@ void tg_snapshot_destroy(tg_snapshot* s);
  * device memory, e.g. an HBM-resident model cache (placed by the K3 copy
  * kernel; source kind 2 in tg_placement). */
 int tg_host_register(tg_tensor_id id, const void* ptr, uint64_t size, const tg_digest* expected /*nullable*/);
+/* Model Store source (ModelLocation::ModelStore, model.hpp:24): the tensor's
+ * bytes are `size` bytes at `file_offset` of a checkpoint file; loads stream
+ * them file → pinned ring (reader threads) → HBM, overlapping storage reads
+ * with PCIe. */
+int tg_file_register(tg_tensor_id id, const char* path, uint64_t file_offset, uint64_t size,
+                     const tg_digest* expected /*nullable*/);
 int tg_host_unregister(tg_tensor_id id);
 int tg_host_clear(void);
 int tg_host_alloc(uint64_t size, void** out); /* pinned */

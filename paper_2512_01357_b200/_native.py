@@ -164,6 +164,7 @@ _SIGS = {
     "tg_pool_restore": (C.c_int, [vp, vp]),
     "tg_snapshot_destroy": (None, [vp]),
     "tg_host_register": (C.c_int, [TensorIdC, vp, u64, P(DigestC)]),
+    "tg_file_register": (C.c_int, [TensorIdC, cp, u64, u64, P(DigestC)]),
     "tg_host_unregister": (C.c_int, [TensorIdC]),
     "tg_host_clear": (C.c_int, []),
     "tg_host_alloc": (C.c_int, [u64, P(vp)]),

@@ -571,10 +571,26 @@ void tg_snapshot_destroy(tg_snapshot* s) {
 // ---- host sources ------------------------------------------------------------------
 int tg_host_register(tg_tensor_id id, const void* ptr, uint64_t size, const tg_digest* expected) {
     if (!ptr && size) return TG_ERR_BAD_ARG;
-    HostSource s{ptr, size, expected != nullptr, expected ? Digest{expected->hi, expected->lo} : Digest{}, false};
+    HostSource s;
+    s.ptr = ptr;
+    s.size = size;
+    s.has_expected = expected != nullptr;
+    if (expected) s.expected = Digest{expected->hi, expected->lo};
     cudaPointerAttributes a{};
     if (ptr && cudaPointerGetAttributes(&a, ptr) == cudaSuccess) s.on_device = a.type == cudaMemoryTypeDevice;
     cudaGetLastError();
+    SourceRegistry::get().put(key_of(id), s);
+    return 0;
+}
+int tg_file_register(tg_tensor_id id, const char* path, uint64_t file_offset, uint64_t size,
+                     const tg_digest* expected) {
+    if (!path || !*path) return TG_ERR_BAD_ARG;
+    HostSource s;
+    s.size = size;
+    s.has_expected = expected != nullptr;
+    if (expected) s.expected = Digest{expected->hi, expected->lo};
+    s.path = path;
+    s.file_off = file_offset;
     SourceRegistry::get().put(key_of(id), s);
     return 0;
 }

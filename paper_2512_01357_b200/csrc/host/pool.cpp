@@ -2,7 +2,11 @@
 
 #include <algorithm>
 #include <chrono>
+#include <fcntl.h>
+#include <unistd.h>
+
 #include <cstring>
+#include <thread>
 #include <unordered_set>
 
 #include "../device/common.cuh"
@@ -33,6 +37,81 @@ void SourceRegistry::erase(const Key& k) {
 void SourceRegistry::clear() {
     std::lock_guard<std::mutex> g(mu_);
     map_.clear();
+}
+
+// ---- file-backed sources (Model Store) ---------------------------------------
+FileStager::FileStager(int device, std::size_t chunk, int slots, int threads)
+    : device_(device), chunk_(chunk), threads_(threads) {
+    DeviceScope ds(device_);
+    for (int i = 0; i < slots; ++i) {
+        void* p = nullptr;
+        TG_CUDA(cudaMallocHost(&p, chunk_));
+        slot_.push_back(static_cast<std::uint8_t*>(p));
+        cudaEvent_t e;
+        TG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        free_.push_back(e);
+    }
+}
+
+FileStager::~FileStager() {
+    DeviceScope ds(device_);
+    for (cudaEvent_t e : free_) {
+        cudaEventSynchronize(e);
+        cudaEventDestroy(e);
+    }
+    for (std::uint8_t* p : slot_) cudaFreeHost(p);
+}
+
+void FileStager::stage(const std::string& path, u64 off, u64 size, std::uint8_t* dst, cudaStream_t s) {
+    const int fd = ::open(path.c_str(), O_RDONLY);
+    if (fd < 0) throw DeviceError(kErrNoSource, "cannot open " + path);
+    const int nslots = static_cast<int>(slot_.size());
+    // Read up to `threads_` chunks concurrently into free slots, then queue
+    // their H2D copies in order.
+    for (u64 base = 0; base < size;) {
+        struct Job {
+            int slot;
+            u64 at, n;
+            std::thread th;
+            bool ok = true;
+        };
+        std::vector<Job> jobs;
+        for (int k = 0; k < threads_ && base < size; ++k) {
+            const int sl = next_;
+            next_ = (next_ + 1) % nslots;
+            TG_CUDA(cudaEventSynchronize(free_[sl]));  // previous H2D from this slot drained
+            const u64 n = std::min<u64>(chunk_, size - base);
+            jobs.push_back(Job{sl, base, n, {}});
+            base += n;
+        }
+        for (Job& j : jobs)
+            j.th = std::thread([&, jp = &j] {
+                u64 done = 0;
+                while (done < jp->n) {
+                    const ssize_t r = ::pread(fd, slot_[jp->slot] + done, jp->n - done, static_cast<off_t>(off + jp->at + done));
+                    if (r <= 0) {
+                        jp->ok = false;
+                        return;
+                    }
+                    done += static_cast<u64>(r);
+                }
+            });
+        bool ok = true;
+        for (Job& j : jobs) {
+            j.th.join();
+            ok = ok && j.ok;
+        }
+        if (!ok) {
+            ::close(fd);
+            throw DeviceError(kErrNoSource, "short read from " + path);
+        }
+        for (Job& j : jobs) {
+            TG_CUDA(cudaMemcpyAsync(dst + j.at, slot_[j.slot], j.n, cudaMemcpyHostToDevice, s));
+            TG_CUDA(cudaEventRecord(free_[j.slot], s));
+            bytes_read_ += j.n;
+        }
+    }
+    ::close(fd);
 }
 
 // ---- pool --------------------------------------------------------------------
@@ -339,7 +418,12 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             relocate_launch(&md, 1, sm_count_, s);
             TG_CUDA(cudaGetLastError());
         } else {
-            TG_CUDA(cudaMemcpyAsync(arena_ + pl.off, src[i].ptr, sz, cudaMemcpyHostToDevice, s));
+            if (src[i].is_file()) {
+                if (!stager_) stager_ = std::make_unique<FileStager>(device_, 16u << 20, 8, 4);
+                stager_->stage(src[i].path, src[i].file_off, sz, arena_ + pl.off, s);
+            } else {
+                TG_CUDA(cudaMemcpyAsync(arena_ + pl.off, src[i].ptr, sz, cudaMemcpyHostToDevice, s));
+            }
         }
         TG_CUDA(cudaEventRecord(ev(ev_land + i), s));
     }
@@ -431,7 +515,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             HostSource hs;
             if (!SourceRegistry::get().find(t.id, &hs) || hs.size != t.size)
                 throw DeviceError(kErrVerify, "peer bytes of " + t.id.hex() + " fail verification and no host source");
-            TG_CUDA(cudaMemcpyAsync(arena_ + e->off, hs.ptr, t.size, cudaMemcpyDefault, s_main_));
+            fetch(hs, arena_ + e->off, t.size, s_main_);
             TG_CUDA(cudaStreamSynchronize(s_main_));
             rep->repaired_bytes += t.size;
             e->digest = fingerprint_resident(t.id);
@@ -452,7 +536,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             HostSource hs;
             if (!SourceRegistry::get().find(k, &hs) || hs.size != e->size)
                 throw DeviceError(kErrVerify, "reused tensor " + k.hex() + " fails verification and has no host source");
-            TG_CUDA(cudaMemcpyAsync(arena_ + e->off, hs.ptr, e->size, cudaMemcpyDefault, s_main_));
+            fetch(hs, arena_ + e->off, e->size, s_main_);
             TG_CUDA(cudaStreamSynchronize(s_main_));
             rep->repaired_bytes += e->size;
             e->digest = fingerprint_resident(k);
@@ -469,6 +553,16 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     totals_.fingerprint_bytes += rep->fingerprint_bytes;
     totals_.relocated_bytes += D.plan.total_merge_cost;
     return ok();
+}
+
+// Bytes of a registered source into the arena (repair paths).
+void Pool::fetch(const HostSource& hs, std::uint8_t* dst, u64 size, cudaStream_t s) {
+    if (hs.is_file()) {
+        if (!stager_) stager_ = std::make_unique<FileStager>(device_, 16u << 20, 8, 4);
+        stager_->stage(hs.path, hs.file_off, size, dst, s);
+    } else {
+        TG_CUDA(cudaMemcpyAsync(dst, hs.ptr, size, cudaMemcpyDefault, s));
+    }
 }
 
 St Pool::move_tensor(const Key& k, u64 to) {

@@ -35,6 +35,33 @@ struct HostSource {
     bool has_expected = false;
     Digest expected;
     bool on_device = false;  // HBM-resident source: placed by the K3 copy kernel
+    // Model Store source (model.hpp:24 ModelLocation::ModelStore): bytes live
+    // in a checkpoint file and stream file → pinned ring → HBM
+    std::string path;
+    u64 file_off = 0;
+    bool is_file() const { return !path.empty(); }
+};
+
+// Pinned staging ring for file-backed placements: reader threads pread chunks
+// into free slots while the copy engine drains filled ones, so storage and
+// PCIe overlap.  One per pool, created on first use.
+class FileStager {
+public:
+    FileStager(int device, std::size_t chunk, int slots, int threads);
+    ~FileStager();
+    // Enqueue `size` bytes of `path` at `off` into dst on stream s (stream
+    // order is preserved; returns once every chunk has been read and queued).
+    void stage(const std::string& path, u64 off, u64 size, std::uint8_t* dst, cudaStream_t s);
+    u64 bytes_read() const { return bytes_read_; }
+
+private:
+    int device_;
+    std::size_t chunk_;
+    std::vector<std::uint8_t*> slot_;
+    std::vector<cudaEvent_t> free_;  // recorded after the H2D that drained the slot
+    int threads_;
+    int next_ = 0;
+    u64 bytes_read_ = 0;
 };
 
 class SourceRegistry {
@@ -139,6 +166,7 @@ public:
 
 private:
     void ensure_events(std::size_t n);
+    void fetch(const HostSource& hs, std::uint8_t* dst, u64 size, cudaStream_t s);
     cudaEvent_t ev(std::size_t i) { return events_[i]; }
 
     Store store_;
@@ -153,6 +181,7 @@ private:
         std::unordered_map<Key, RemoteEntry, KeyHash> index;
     };
     std::vector<RemotePeer> remotes_;
+    std::unique_ptr<FileStager> stager_;
     Totals totals_;
     // staging
     void* h_stage_ = nullptr;

@@ -309,3 +309,29 @@ def test_kv_tables_survive_engine_copy_and_pool_teardown(tg):
     assert c.table(1) is not None and [c.table(1).lbn_to_pbn[i] for i in range(3)] == a[0]
     pool.close()
     del c, kv
+
+
+def test_model_store_file_sources(tg, cpu, tmp_path):
+    """Model Store placement (§8(f) row 2): tensors registered as ranges of a
+    checkpoint file stream file → pinned ring → HBM; bytes and fingerprints
+    equal the CPU restatement, decisions unchanged."""
+    from paper_2512_01357_b200 import _native as N
+    m = tg.make_model("store-model", 90_000_029, 4, 0, location=tg.ModelLocation.ModelStore)
+    path = tmp_path / "ckpt.bin"
+    with open(path, "wb") as f:
+        f.write(b"HDR!" * 3)  # odd header so tensor offsets in the file are unaligned
+        offs = {}
+        for t in m.tensors:
+            offs[t.id] = f.tell()
+            f.write(cpu.synth(t.id.hi, t.id.lo, t.size).tobytes())
+    for t in m.tensors:
+        assert N.lib.tg_file_register(t.id.c(), str(path).encode(), offs[t.id], t.size, None) == 0
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=128 << 20), device=0)
+    st = tg.ModelStatsTable()
+    o = pool.load_model(m, st, 0.0).value()
+    assert o.pcie_bytes == m.total_size
+    for i, t in enumerate(m.tensors):
+        assert o.digests[i] == cpu.content_fingerprint(cpu.synth(t.id.hi, t.id.lo, t.size), threads=8)[0]
+    for t in m.tensors:
+        N.lib.tg_host_unregister(t.id.c())
+    pool.close()
