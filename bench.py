@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
     p.add_argument("--profile", action="store_true", help="short run for ncu (no clocks, no baseline)")
+    p.add_argument("--timeline", default="", help="write the kernel timeline of one extra value-path step "
+                   "(CUPTI via torch.profiler, after the timed region) to this JSON file")
     p.add_argument("--workload", default="c2", choices=["c2", "c4"],
                    help="c2 (default): the C2 switch on every GPU; c4: GPT-20B sharded over the GPUs")
     return p.parse_args()
@@ -295,8 +297,9 @@ def run_ours(args):
             N.check_runtime(lib.tg_host_register(tid.c(), C.c_void_p(host[tid].ptr), host[tid].n, None))
 
     stream = torch.cuda.ExternalStream(pool.stream(), device=local)
-    # TANGRAM_FUSED=1: move + fingerprint in one pass (K3F) — A/B of TG_LOAD_FUSED
-    policy = tg.LoadPolicy(flags=1 | 2 | (8 if os.environ.get("TANGRAM_FUSED") else 0))
+    # default TG_LOAD_FUSED (one load-kernel launch); TANGRAM_UNFUSED=1 runs
+    # the separate K3 waves + K1 passes (A/B)
+    policy = tg.LoadPolicy(flags=1 | 2 | (0 if os.environ.get("TANGRAM_UNFUSED") else 8))
 
     def step():
         pool.restore(snap)
@@ -334,6 +337,8 @@ def run_ours(args):
     ms_v, outs_v, launches = phase(register_device)
     ms_e, outs_e, _ = phase(register_host)
     clk = clocks.stop() if not args.profile else {}
+    if args.timeline and rank == 0:
+        write_timeline(args.timeline, lambda: (register_device(miss_ids), step()))
 
     def maxrank(x):
         if world == 1:
@@ -371,14 +376,20 @@ def run_ours(args):
     fp_ms_v = statistics.mean(o.timings["fp_reuse_ms"] for o in outs_v)
     rel_ms = statistics.mean(o.timings["relocate_ms"] for o in outs_v)
     h2d_ms = statistics.mean(o.timings["h2d_ms"] for o in outs_e)
-    fp_ach = fp_bytes / (fp_ms / 1e3) / 1e9
+    fp_ach = fp_bytes / (fp_ms / 1e3) / 1e9 if fp_ms > 0 else None  # fused: inside the load kernel
     rel_ach = 2 * o_v.bytes_merged / (rel_ms / 1e3) / 1e9
     h2d_ach = o_e.pcie_bytes / (h2d_ms / 1e3) / 1e9
     # minimum HBM traffic of the step: relocations r+w, placements r+w, and a
     # read of every reused tensor no copy already streams (tensors that are
     # moved or placed are fingerprinted from the copy's own read)
-    step_bytes = 2 * o_v.bytes_merged + 2 * o_v.device_src_bytes + kernels.get("untouched_reused_bytes",
-                                                                                   o_v.fingerprint_bytes)
+    # the timed loads ran with details=False: one untimed detailed replay for
+    # the plan's relocation list and hit set
+    pool.restore(snap)
+    o_d = pool.load_model(target, fresh_stats(tg, 3), 20.0, policy).value()
+    moved = {r.tensor for r in o_d.plan.relocations}
+    hit_ids = set(o_d.hit_tensors)
+    untouched = sum(t.size for t in target.tensors if t.id in hit_ids and t.id not in moved)
+    step_bytes = 2 * o_v.bytes_merged + 2 * o_v.device_src_bytes + untouched
     step_ach = step_bytes / (mv / 1e3) / 1e9
 
     cpu_base = None
@@ -398,13 +409,30 @@ def run_ours(args):
         cpu_base = cpu_baseline(args)
 
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "fp_reuse_traffic.json")
+    tf = os.path.join(ROOT, "profiles", "load_kernel_traffic.json" if policy.flags & 8 else "fp_reuse_traffic.json")
     if os.path.exists(tf):
         try:
             traffic = json.load(open(tf)).get("traffic_bytes_per_launch")
         except Exception:
             traffic = None
 
+    fused = policy.flags & 8
+    if fused:
+        # the dominant (only) kernel of the step: the load kernel, timed by CUDA
+        # events on the pool stream around its launch (relocate_ms), per load
+        roofline_main = {
+            "bound": "hbm", "kernel": "K3F copy_fp_kernel, the load kernel: WAR waves r+w, HBM-source placements "
+                                      "r+w, in-place verification reads, one launch per load",
+            "achieved": step_bytes / (rel_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": step_bytes / (rel_ms / 1e3) / 1e9 / hbm_peak, "traffic": traffic,
+            "algorithmic_bytes_per_launch": step_bytes, "ms_per_launch": rel_ms, "peak_source": peak_src}
+    else:
+        roofline_main = {
+            "bound": "hbm", "kernel": "K1 (fingerprint-only load kernel) over the reused tensors, timed alone",
+            "achieved": kernels.get("k1", {}).get("GBps"), "peak": hbm_peak, "unit": "GB/s",
+            "frac": (kernels.get("k1", {}).get("GBps") or 0) / hbm_peak, "traffic": None,
+            "algorithmic_bytes_per_launch": fp_bytes, "ms_per_launch": kernels.get("k1", {}).get("ms_per_launch"),
+            "peak_source": peak_src, "in_step": {"GBps": fp_ach}}
     line = {
         "metric": METRIC,
         "value": world * total / (mv / 1e3) / 1e9,
@@ -422,8 +450,10 @@ def run_ours(args):
             "workload": "C2 OPT-6.7B->OPT-13B switch, load #3 (opt13B) in a 32 GiB pool",
             "model_bytes": total, "reuse_ratio": round(1 - o_v.bytes_transferred / total, 4),
             "bytes_transferred": o_v.bytes_transferred, "bytes_merged": o_v.bytes_merged,
-            "relocations": 15, "waves": o_v.waves, "placements": len(miss_ids), "reused": len(hits),
-            "value_sources": "missing tensors resident in HBM (model cache), placed by K3",
+            "relocations": len(o_d.plan.relocations), "waves": o_v.waves, "placements": len(miss_ids),
+            "reused": len(hits), "load_path": "one load-kernel launch (TG_LOAD_FUSED)" if policy.flags & 8
+            else "K3 waves + K1 passes (TANGRAM_UNFUSED)",
+            "value_sources": "missing tensors resident in HBM (model cache), placed by the load kernel",
             "e2e_sources": "missing tensors in pinned host memory, cudaMemcpyAsync H2D",
             "fingerprint": "tgfp1 over all 41 tensors (13 placed + 28 reused verified)",
             "l2": "no flush: every step streams >= 20 GB, >> 126 MB L2; arena restored (D2D 32 GiB) between steps",
@@ -436,14 +466,13 @@ def run_ours(args):
                        "fp_reuse_ms_value": fp_ms_v, "fp_kernel_ms_total": o_v.timings["fp_kernel_ms"]},
         "e2e": {"value": world * total / (me / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": me,
                 "h2d_bytes_per_step": o_e.pcie_bytes, "d2h_bytes_per_step": 16 * len(target.tensors)},
-        "roofline": {"bound": "hbm", "kernel": "K1 fp_v4_kernel (content fingerprint) over the step's 28 reused "
-                                               "tensors at their final offsets, one launch, timed alone",
-                     "achieved": kernels.get("k1", {}).get("GBps"), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": (kernels.get("k1", {}).get("GBps") or 0) / hbm_peak,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": fp_bytes,
-                     "ms_per_launch": kernels.get("k1", {}).get("ms_per_launch"), "peak_source": peak_src,
-                     "in_step": {"GBps": fp_ach, "note": "same bytes inside the e2e step, 2 launches sharing HBM "
-                                                         "with K3 waves and H2D"}},
+        "roofline": roofline_main,
+        "roofline_k1": {"bound": "hbm", "kernel": "K1 = load kernel with fingerprint-only tasks over the step's "
+                                                  "28 reused tensors at their final offsets, one launch, timed alone",
+                        "achieved": kernels.get("k1", {}).get("GBps"), "peak": hbm_peak, "unit": "GB/s",
+                        "frac": (kernels.get("k1", {}).get("GBps") or 0) / hbm_peak,
+                        "algorithmic_bytes_per_launch": fp_bytes,
+                        "ms_per_launch": kernels.get("k1", {}).get("ms_per_launch"), "peak_source": peak_src},
         "roofline_step": {"bound": "hbm", "what": "value path: minimum device traffic of the step (relocation "
                                                   "waves r+w, HBM-source placements r+w, one read of each reused "
                                                   "tensor no copy streams) / step time",
@@ -471,6 +500,27 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def write_timeline(path, fn):
+    """Kernel/memcpy start, end and stream of one step (untimed diagnostics)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    fn()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    evs = []
+    for e in prof.events():
+        if e.device_type.name != "CUDA":
+            continue
+        evs.append({"name": e.name[:80], "start_us": e.time_range.start, "dur_us": e.time_range.elapsed_us()})
+    t0 = min((e["start_us"] for e in evs), default=0)
+    for e in evs:
+        e["start_us"] -= t0
+    evs.sort(key=lambda e: e["start_us"])
+    with open(path, "w") as f:
+        json.dump(evs, f, indent=0)
 
 
 def isolated_kernels(tg, pool, snap, target, miss_ids, dev, reps=5):

@@ -42,8 +42,8 @@ extern "C" {
 #define TG_LOAD_VERIFY_REUSE 1u    /* fingerprint reused tensors, compare to the recorded digest */
 #define TG_LOAD_FINGERPRINT_NEW 2u /* fingerprint placed tensors, record the digest */
 #define TG_LOAD_PEER 4u            /* pull misses resident on a peer pool over NVLink */
-#define TG_LOAD_FUSED 8u           /* opt-in: move + fingerprint in one pass (K3F) instead of K3 then K1 */
-#define TG_LOAD_DEFAULT 3u
+#define TG_LOAD_FUSED 8u           /* one load-kernel launch (move + fingerprint in one pass) instead of K3 waves then K1 */
+#define TG_LOAD_DEFAULT 11u
 
 typedef struct tg_pool tg_pool;
 typedef struct tg_stats tg_stats;
@@ -284,8 +284,9 @@ int tg_bench_fingerprint(const void* const* dptrs, const uint64_t* ns, uint32_t 
                          double* ms_per_launch, tg_digest* out /* n_bufs, nullable */);
 int tg_bench_relocate(const uint64_t* moves /* src,dst,len triples (device addresses) */, uint32_t n_moves,
                       int32_t device, int32_t reps, double* ms_per_launch);
-/* K3F: move n_moves hazard-free (src, dst, len) byte ranges and return each
- * one's tgfp1 digest from the same pass (one launch, then `reps` timed ones). */
+/* K3F (the load kernel): move n_moves hazard-free (src, dst, len) byte ranges
+ * and return each one's tgfp1 digest from the same pass (one launch, then
+ * `reps` timed ones); dst == 0 fingerprints the range in place. */
 int tg_copy_fingerprint(const uint64_t* moves, uint32_t n_moves, int32_t device, int32_t reps, double* ms_per_launch,
                         tg_digest* digests /* n_moves */);
 int tg_synth_fill_host(tg_tensor_id id, uint64_t begin, uint64_t len, void* dst, int32_t threads);

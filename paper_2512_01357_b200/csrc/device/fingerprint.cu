@@ -160,6 +160,17 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
+// One LDS.128 for a 16-byte staged word.  Plain uint4 loads whose components
+// are only partly used get split into LDS.64 pairs, and a half-warp LDS.64
+// phase sees leaves l and l+8 on the same swizzled bank pair (2-way conflict).
+__device__ __forceinline__ uint4 lds128(const uint4* p) {
+    uint4 v;
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(s));
+    return v;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -474,8 +485,8 @@ __device__ __forceinline__ void v3_hash_stage(const uint4* stage_buf, u32 lane, 
     const u32 key = lane & 7;
     uint4 w[kSlotWords];
 #pragma unroll
-    for (int q = 0; q < kStageBlocks; ++q) w[q] = slot[q ^ key];
-    w[kStageBlocks] = stage_buf[32 * kStageBlocks + lane];
+    for (int q = 0; q < kStageBlocks; ++q) w[q] = lds128(slot + (q ^ key));
+    w[kStageBlocks] = lds128(stage_buf + 32 * kStageBlocks + lane);
 #pragma unroll
     for (int b = 0; b < kStageBlocks; ++b) {
         const u32 u[8] = {w[b].x, w[b].y, w[b].z, w[b].w, w[b + 1].x, w[b + 1].y, w[b + 1].z, w[b + 1].w};
@@ -484,6 +495,17 @@ __device__ __forceinline__ void v3_hash_stage(const uint4* stage_buf, u32 lane, 
         const u32 d = __funnelshift_r(u[Q + 2], u[Q + 3], r8);
         const u32 e = __funnelshift_r(u[Q + 3], u[Q + 4], r8);
         mm::body_dev(h1, h2, mm::W32{a, c}, mm::W32{d, e});
+    }
+}
+
+// 16-byte-aligned leaves: the blocks are the staged words themselves.
+__device__ __forceinline__ void v3_hash_stage_aligned(const uint4* stage_buf, u32 lane, mm::W32& h1, mm::W32& h2) {
+    const uint4* slot = stage_buf + lane * 8;
+    const u32 key = lane & 7;
+#pragma unroll
+    for (int b = 0; b < kStageBlocks; ++b) {
+        const uint4 w = lds128(slot + (b ^ key));
+        mm::body_dev(h1, h2, mm::W32{w.x, w.y}, mm::W32{w.z, w.w});
     }
 }
 
@@ -630,6 +652,10 @@ __device__ __forceinline__ void v4_issue(uint4* stage_buf, const TileRef& tr, in
 
 __device__ __forceinline__ void v4_hash(const uint4* stage_buf, const TileRef& tr, u32 lane, mm::W32& h1,
                                         mm::W32& h2) {
+    if (tr.o == 0) {
+        v3_hash_stage_aligned(stage_buf, lane, h1, h2);
+        return;
+    }
     const u32 r8 = (tr.o & 3) * 8;
     switch (tr.o >> 2) {
         case 0: v3_hash_stage<0>(stage_buf, lane, r8, h1, h2); break;
@@ -639,21 +665,22 @@ __device__ __forceinline__ void v4_hash(const uint4* stage_buf, const TileRef& t
     }
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
+template <int STAGES, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 2)
     fp_v4_kernel(const FpTask* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums) {
     extern __shared__ uint4 smem[];
     const u32 lane = threadIdx.x & 31;
     const u32 wid = threadIdx.x >> 5;
-    uint4* wbuf = smem + wid * kV3WarpWords;
-    const u64 nwarps = static_cast<u64>(gridDim.x) * kWarpsPerCta;
-    u64 t = static_cast<u64>(blockIdx.x) * kWarpsPerCta + wid;
+    uint4* wbuf = smem + wid * (STAGES * kV3StageWords);
+    const u64 nwarps = static_cast<u64>(gridDim.x) * WARPS;
+    u64 t = static_cast<u64>(blockIdx.x) * WARPS + wid;
     if (t >= total_tiles) return;
     TileRef cur = tile_ref(tasks, n_tasks, t, total_tiles);
     TileRef nxt = tile_ref(tasks, n_tasks, t + nwarps, total_tiles);
     int cur_task = -1;
     u64 acc_h = 0, acc_l = 0;
     u32 buf = 0;  // running stage-buffer index
-    constexpr int kAhead = kV3Stages - 1;
+    constexpr int kAhead = STAGES - 1;
 #pragma unroll
     for (int s = 0; s < kAhead; ++s) v4_issue(wbuf + s * kV3StageWords, cur, s, lane);
     while (cur.task >= 0) {
@@ -673,14 +700,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
         for (int s = 0; s < kStagesPerLeaf; ++s) {
             const int ahead = s + kAhead;
             u32 fill = buf + kAhead;
-            fill = fill >= kV3Stages ? fill - kV3Stages : fill;
+            fill = fill >= STAGES ? fill - STAGES : fill;
             if (ahead < kStagesPerLeaf) v4_issue(wbuf + fill * kV3StageWords, cur, ahead, lane);
             else v4_issue(wbuf + fill * kV3StageWords, nxt, ahead - kStagesPerLeaf, lane);
-            cp_async_wait<kV3Stages - 1>();
+            cp_async_wait<STAGES - 1>();
             __syncwarp();
             if (lane < cur.nfull) v4_hash(wbuf + buf * kV3StageWords, cur, lane, h1, h2);
             __syncwarp();
-            buf = buf + 1 == kV3Stages ? 0 : buf + 1;
+            buf = buf + 1 == STAGES ? 0 : buf + 1;
         }
         if (lane < cur.nfull) {
             u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
@@ -733,14 +760,31 @@ __global__ void fp_finalize_kernel(const FpTask* __restrict__ tasks, u32 n_tasks
 // tensor without gaps or overlaps; the ones that would reach outside
 // [0, 4096 F) (F = full leaves) are left to an edge pass that copies the
 // head (< 16 B) and the tail (< 4 KiB + 16 B) bytewise.
+//
+// Those words are stored one 128-byte destination line per leaf and stage:
+// with k = ((dst + delta - o) mod 128) / 16, line lane q takes word
+// (q - k) mod 8 of stage s when q >= k, else of stage s - 1 (still in the
+// ring), and each leaf stores the k words of its stage 31 that spill into
+// the next line after its last stage.  An unaligned 128-byte run would
+// touch two lines and five sectors per leaf-stage and leave half sectors
+// for L2 to merge (measured: 3.4 vs 5.0 TB/s for delta = 8, dst % 32 = 8).
 struct CopyTileRef {
     TileRef t;
-    std::uint8_t* dst;  // destination of tensor byte 0
+    std::uint8_t* dst;  // destination of tensor byte 0 (nullptr: fingerprint only)
     u32 delta;
+    u32 k;               // destination line phase of the word grid, in words
     u64 x_first, x_end;  // full-word writes cover tensor bytes [x_first, x_end)
+    int gate, wave;
 };
 
-__device__ __forceinline__ CopyTileRef copy_tile_ref(const CopyFpTask* __restrict__ tasks, u32 n_tasks, u64 t,
+// K1 runs through the load kernel too: an FpTask is a fingerprint-only task.
+__device__ __forceinline__ CopyFpTask as_copy_task(const CopyFpTask& t) { return t; }
+__device__ __forceinline__ CopyFpTask as_copy_task(const FpTask& t) {
+    return CopyFpTask{t.base, nullptr, t.n, t.tile0, -1, -1};
+}
+
+template <class Task>
+__device__ __forceinline__ CopyTileRef copy_tile_ref(const Task* __restrict__ tasks, u32 n_tasks, u64 t,
                                                      u64 total_tiles) {
     CopyTileRef r{};
     r.t.task = -1;
@@ -751,7 +795,7 @@ __device__ __forceinline__ CopyTileRef copy_tile_ref(const CopyFpTask* __restric
         if (tasks[mid].tile0 <= t) lo = mid;
         else hi = mid - 1;
     }
-    const CopyFpTask tk = tasks[lo];
+    const CopyFpTask tk = as_copy_task(tasks[lo]);
     r.t.task = static_cast<int>(lo);
     r.t.base = tk.src;
     r.t.n = tk.n;
@@ -762,10 +806,14 @@ __device__ __forceinline__ CopyTileRef copy_tile_ref(const CopyFpTask* __restric
     r.t.o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p0) & 15);
     r.t.a0 = p0 - r.t.o;
     r.dst = tk.dst;
+    r.gate = tk.gate;
+    r.wave = tk.wave;
+    if (!tk.dst) return r;  // delta = k = 0: no realignment, no writes
     const u32 od = static_cast<u32>(reinterpret_cast<std::uintptr_t>(tk.dst) & 15);
     r.delta = (r.t.o - od) & 15;
     // first x >= 0 on the grid x ≡ delta - o (mod 16); last with x + 16 <= 4096 F
     const long long x0 = static_cast<long long>(r.delta) - static_cast<long long>(r.t.o);
+    r.k = static_cast<u32>(((reinterpret_cast<std::uintptr_t>(tk.dst) + static_cast<std::uintptr_t>(x0)) & 127) >> 4);
     r.x_first = static_cast<u64>(x0 < 0 ? x0 + 16 : x0);
     const u64 lim = full * kLeafBytes;
     r.x_end = lim >= r.x_first + 16 ? r.x_first + ((lim - r.x_first) / 16) * 16 : r.x_first;
@@ -779,19 +827,27 @@ __device__ __forceinline__ uint4 realign_words(uint4 w0, uint4 w1, u32 r8) {
                       __funnelshift_r(u[QD + 2], u[QD + 3], r8), __funnelshift_r(u[QD + 3], u[QD + 4], r8));
 }
 
-// Write this stage's destination words: lane -> leaf 4i + lane/8, word lane%8.
-// The lane's tensor offset x_lane = 4096 (leaf0 + g) + 16 q + delta - o +
-// 128 s is computed once per stage and copy i adds 16 KiB; the swizzled smem
-// positions only depend on i's parity; interior tiles skip the edge test.
-// (A straightforward per-word version cost ~46 instructions per 16-byte word
-// and held K3F at 4.9 TB/s; this one is ~8.)
-template <int QD>
-__device__ __forceinline__ void write_stage_fast(const uint4* stage_buf, const CopyTileRef& c, long long x_lane,
-                                                 bool check, u32 r8, u32 lane) {
+// Store one destination line per leaf of the tile: lane -> leaf 4i + lane/8,
+// line word q = lane%8, which is word j = (q - k) mod 8 of stage `so` (s for
+// q >= k, s - 1 for q < k; see CopyTileRef).  The lane's tensor offset and
+// swizzled smem positions are computed once; copy i adds 16 KiB (4 leaves),
+// interior tiles skip the edge test.  SHIFT = false is the delta = 0 case:
+// the staged word is the destination word.
+template <int QD, bool SHIFT>
+__device__ __forceinline__ void write_lines(const uint4* cur_buf, const uint4* prev_buf, const CopyTileRef& c, int s,
+                                            bool use_cur, bool use_prev, bool check, u32 r8, u32 lane) {
     const u32 g = lane >> 3, q = lane & 7;
-    const uint4* base = stage_buf + g * 8;
-    const u32 pa0 = q ^ g, pb0 = q ^ (4u ^ g);
-    const u32 pa1 = ((q + 1) & 7) ^ g, pb1 = ((q + 1) & 7) ^ (4u ^ g);
+    const bool from_cur = q >= c.k;
+    if (!(from_cur ? use_cur : use_prev)) return;
+    const u32 j = (q - c.k) & 7;
+    const int so = from_cur ? s : s - 1;
+    const uint4* sbuf = from_cur ? cur_buf : prev_buf;
+    const uint4* base = sbuf + g * 8;
+    const uint4* extra = sbuf + 32 * kStageBlocks + g;
+    const u32 pa0 = j ^ g, pb0 = j ^ (4u ^ g);
+    const u32 pa1 = ((j + 1) & 7) ^ g, pb1 = ((j + 1) & 7) ^ (4u ^ g);
+    const long long x_lane = static_cast<long long>((c.t.leaf0 + g) * kLeafBytes) + 16LL * j +
+                             static_cast<long long>(c.delta) - static_cast<long long>(c.t.o) + 128LL * so;
     std::uint8_t* dst_lane = c.dst + x_lane;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -799,25 +855,33 @@ __device__ __forceinline__ void write_stage_fast(const uint4* stage_buf, const C
         if (l >= c.t.nfull) continue;
         const long long x = x_lane + 16384LL * i;
         if (check && (x < static_cast<long long>(c.x_first) || x + 16 > static_cast<long long>(c.x_end))) continue;
-        const uint4 w0 = base[32 * i + ((i & 1) ? pb0 : pa0)];
-        const uint4 w1 = q == 7 ? stage_buf[32 * kStageBlocks + l] : base[32 * i + ((i & 1) ? pb1 : pa1)];
-        __stcs(reinterpret_cast<uint4*>(dst_lane + 16384LL * i), realign_words<QD>(w0, w1, r8));
+        const uint4 w0 = lds128(base + 32 * i + ((i & 1) ? pb0 : pa0));
+        uint4 v = w0;
+        if constexpr (SHIFT) {
+            const uint4 w1 = lds128(j == 7 ? extra + 4 * i : base + 32 * i + ((i & 1) ? pb1 : pa1));
+            v = realign_words<QD>(w0, w1, r8);
+        }
+        __stcs(reinterpret_cast<uint4*>(dst_lane + 16384LL * i), v);
     }
 }
 
-__device__ __forceinline__ void write_stage_dispatch(const uint4* stage_buf, const CopyTileRef& c, int s, u32 lane) {
-    const long long x_lane = static_cast<long long>((c.t.leaf0 + (lane >> 3)) * kLeafBytes) + (lane & 7) * 16 +
-                             static_cast<long long>(c.delta) - static_cast<long long>(c.t.o) + 128LL * s;
-    // the whole tile is inside [x_first, x_end) unless it holds the tensor's first or last full leaf
+__device__ __forceinline__ void write_lines_dispatch(const uint4* cur_buf, const uint4* prev_buf, const CopyTileRef& c,
+                                                     int s, bool use_cur, bool use_prev, u32 lane) {
+    // the whole tile is inside [x_first, x_end) unless it holds the tensor's
+    // first or last full leaf (its words are within 16 bytes of its leaves)
     const long long tile_lo = static_cast<long long>(c.t.leaf0 * kLeafBytes) - 16;
     const long long tile_hi = static_cast<long long>((c.t.leaf0 + c.t.nfull) * kLeafBytes) + 16;
     const bool check = tile_lo < static_cast<long long>(c.x_first) || tile_hi > static_cast<long long>(c.x_end);
+    if (c.delta == 0) {
+        write_lines<0, false>(cur_buf, prev_buf, c, s, use_cur, use_prev, check, 0, lane);
+        return;
+    }
     const u32 r8 = (c.delta & 3) * 8;
     switch (c.delta >> 2) {
-        case 0: write_stage_fast<0>(stage_buf, c, x_lane, check, r8, lane); break;
-        case 1: write_stage_fast<1>(stage_buf, c, x_lane, check, r8, lane); break;
-        case 2: write_stage_fast<2>(stage_buf, c, x_lane, check, r8, lane); break;
-        default: write_stage_fast<3>(stage_buf, c, x_lane, check, r8, lane); break;
+        case 0: write_lines<0, true>(cur_buf, prev_buf, c, s, use_cur, use_prev, check, r8, lane); break;
+        case 1: write_lines<1, true>(cur_buf, prev_buf, c, s, use_cur, use_prev, check, r8, lane); break;
+        case 2: write_lines<2, true>(cur_buf, prev_buf, c, s, use_cur, use_prev, check, r8, lane); break;
+        default: write_lines<3, true>(cur_buf, prev_buf, c, s, use_cur, use_prev, check, r8, lane); break;
     }
 }
 
@@ -853,21 +917,45 @@ __device__ __forceinline__ void copy_issue(uint4* stage_buf, const CopyTileRef& 
     cp_async_commit();
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
-    copy_fp_kernel(const CopyFpTask* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums) {
+__device__ __forceinline__ u64 ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Tiles are handed out in task order by one counter, so every tile of the
+// wave a gated tile waits for was taken earlier by a running warp: the wait
+// always ends, whatever the residency.  Reads never wait: a wave never writes
+// into a later wave's (or an in-place task's) source bytes.
+__device__ __forceinline__ u64 next_tile(unsigned long long* counter, u32 lane) {
+    unsigned long long t = 0;
+    if (lane == 0) t = atomicAdd(counter, 1ull);
+    return __shfl_sync(0xffffffffu, t, 0);
+}
+
+// The load kernel keeps four stage slots per warp: stage s - 1 (still read
+// by the line stores), stage s, and two stages in flight.  Six warps per CTA
+// keep two CTAs (2 x 108 KiB) resident per SM.
+constexpr int kCopyStages = 4;
+constexpr int kCopyWarps = 6;
+constexpr int kCopyWarpWords = kCopyStages * kV3StageWords;
+constexpr int kCopySmemBytes = kCopyWarps * kCopyWarpWords * 16;
+
+template <class Task>
+__global__ void __launch_bounds__(kCopyWarps * 32, 2)
+    copy_fp_kernel(const Task* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums,
+                   unsigned long long* __restrict__ sync, const u64* __restrict__ need) {
     extern __shared__ uint4 smem[];
     const u32 lane = threadIdx.x & 31;
     const u32 wid = threadIdx.x >> 5;
-    uint4* wbuf = smem + wid * kV3WarpWords;
-    const u64 nwarps = static_cast<u64>(gridDim.x) * kWarpsPerCta;
-    u64 t = static_cast<u64>(blockIdx.x) * kWarpsPerCta + wid;
-    if (t >= total_tiles) return;
-    CopyTileRef cur = copy_tile_ref(tasks, n_tasks, t, total_tiles);
-    CopyTileRef nxt = copy_tile_ref(tasks, n_tasks, t + nwarps, total_tiles);
+    uint4* wbuf = smem + wid * kCopyWarpWords;
+    CopyTileRef cur = copy_tile_ref(tasks, n_tasks, next_tile(sync, lane), total_tiles);
+    if (cur.t.task < 0) return;
+    CopyTileRef nxt = copy_tile_ref(tasks, n_tasks, next_tile(sync, lane), total_tiles);
     int cur_task = -1;
     u64 acc_h = 0, acc_l = 0;
     u32 buf = 0;
-    constexpr int kAhead = kV3Stages - 1;
+    constexpr int kAhead = kCopyStages - 1;
 #pragma unroll
     for (int s = 0; s < kAhead; ++s) copy_issue(wbuf + s * kV3StageWords, cur, s, lane);
     while (cur.t.task >= 0) {
@@ -882,21 +970,33 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
             cur_task = cur.t.task;
             acc_h = acc_l = 0;
         }
+        const bool writes = cur.dst != nullptr;
+        if (writes && cur.gate >= 0) {
+            if (lane == 0) {
+                const u64 want = need[cur.gate];
+                while (ld_acquire(sync + 1 + cur.gate) < want) __nanosleep(256);
+            }
+            __syncwarp();
+        }
         const u64 my_leaf = cur.t.leaf0 + lane;
         mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
+        // The line stores of stage s also read stage s - 1, so the ring slot
+        // it occupies is refilled (with stage s + 3) only after them.
         for (int s = 0; s < kStagesPerLeaf; ++s) {
-            const int ahead = s + kAhead;
-            u32 fill = buf + kAhead;
-            fill = fill >= kV3Stages ? fill - kV3Stages : fill;
-            if (ahead < kStagesPerLeaf) copy_issue(wbuf + fill * kV3StageWords, cur, ahead, lane);
-            else copy_issue(wbuf + fill * kV3StageWords, nxt, ahead - kStagesPerLeaf, lane);
-            cp_async_wait<kV3Stages - 1>();
+            cp_async_wait<kAhead - 1>();
             __syncwarp();
+            const u32 prev = (buf + kCopyStages - 1) % kCopyStages;
             const uint4* sb = wbuf + buf * kV3StageWords;
-            if (cur.t.nfull) write_stage_dispatch(sb, cur, s, lane);
+            const uint4* sp = wbuf + prev * kV3StageWords;
+            if (writes && cur.t.nfull) write_lines_dispatch(sb, sp, cur, s, true, s > 0, lane);
             if (lane < cur.t.nfull) v4_hash(sb, cur.t, lane, h1, h2);
+            if (s == kStagesPerLeaf - 1 && writes && cur.t.nfull && cur.k)
+                write_lines_dispatch(nullptr, sb, cur, kStagesPerLeaf, false, true, lane);
             __syncwarp();
-            buf = buf + 1 == kV3Stages ? 0 : buf + 1;
+            const int ahead = s + kAhead;
+            if (ahead < kStagesPerLeaf) copy_issue(wbuf + prev * kV3StageWords, cur, ahead, lane);
+            else copy_issue(wbuf + prev * kV3StageWords, nxt, ahead - kStagesPerLeaf, lane);
+            buf = (buf + 1) % kCopyStages;
         }
         if (lane < cur.t.nfull) {
             u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
@@ -911,14 +1011,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
             acc_l += d2;
         }
         // the tensor's last tile also copies the head and tail bytes
-        if (cur.t.leaf0 + 32 >= (cur.t.n + kLeafBytes - 1) / kLeafBytes) {
+        if (writes && cur.t.leaf0 + 32 >= (cur.t.n + kLeafBytes - 1) / kLeafBytes) {
             const std::uint8_t* src = cur.t.base;
             for (u64 b = lane; b < cur.x_first && b < cur.t.n; b += 32) cur.dst[b] = src[b];
             for (u64 b = cur.x_end + lane; b < cur.t.n; b += 32) cur.dst[b] = src[b];
         }
-        t += nwarps;
+        if (cur.wave >= 0) {  // this tile's source bytes are all read
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                atomicAdd(sync + 1 + cur.wave, 1ull);
+            }
+        }
         cur = nxt;
-        nxt = copy_tile_ref(tasks, n_tasks, t + nwarps, total_tiles);
+        nxt = copy_tile_ref(tasks, n_tasks, next_tile(sync, lane), total_tiles);
     }
     cp_async_wait<0>();
     if (cur_task >= 0) {
@@ -943,48 +1049,75 @@ __global__ void copy_fp_finalize_kernel(const CopyFpTask* __restrict__ tasks, u3
 
 }  // namespace
 
-void copy_fp_launch(const CopyFpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests,
-                    int sm_count, cudaStream_t s) {
+std::uint64_t copy_fp_resident_warps(int sm_count) { return static_cast<u64>(sm_count) * 2 * kCopyWarps; }
+
+namespace {
+template <class Task>
+void load_kernel_launch(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_sync,
+                        const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s) {
+    static const bool attr = [] {
+        return cudaFuncSetAttribute(copy_fp_kernel<Task>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kCopySmemBytes) == cudaSuccess;
+    }();
+    (void)attr;
+    cudaMemsetAsync(d_sync, 0, (1 + n_waves) * sizeof(u64), s);
+    const u64 want = (total_tiles + kCopyWarps - 1) / kCopyWarps;
+    const u64 cap = static_cast<u64>(sm_count) * 2;
+    const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
+    copy_fp_kernel<Task><<<blocks, kCopyWarps * 32, kCopySmemBytes, s>>>(
+        d_tasks, n_tasks, total_tiles, d_sums, reinterpret_cast<unsigned long long*>(d_sync), d_need);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
+}  // namespace
+
+void copy_fp_launch(const CopyFpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, u64* d_sync,
+                    const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s) {
     if (n_tasks == 0) return;
-    if (total_tiles > 0) {
-        static const bool attr = [] {
-            return cudaFuncSetAttribute(copy_fp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV3SmemBytes) ==
-                   cudaSuccess;
-        }();
-        (void)attr;
-        const u64 want = (total_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
-        const u64 cap = static_cast<u64>(sm_count) * 2;
-        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
-        copy_fp_kernel<<<blocks, kWarpsPerCta * 32, kV3SmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
-        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-    }
+    if (total_tiles > 0) load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves, sm_count, s);
     copy_fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, int sm_count,
-               cudaStream_t s) {
+void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, u64* d_sync,
+               int sm_count, cudaStream_t s) {
     if (n_tasks == 0) return;
-    // TANGRAM_FP_KERNEL=v0..v3 selects the earlier variants (A/B runs); v4 is the default.
+    // Default: the load kernel with fingerprint-only tasks.  TANGRAM_FP_KERNEL=
+    // v0..v5 selects the earlier dedicated K1 variants (A/B runs).
     static const int variant = [] {
         const char* e = std::getenv("TANGRAM_FP_KERNEL");
         if (e && std::strcmp(e, "v0") == 0) return 0;
         if (e && std::strcmp(e, "v1") == 0) return 1;
         if (e && std::strcmp(e, "v2") == 0) return 2;
         if (e && std::strcmp(e, "v3") == 0) return 3;
-        return 4;
+        if (e && std::strcmp(e, "v4") == 0) return 4;
+        if (e && std::strcmp(e, "v5") == 0) return 5;
+        return 6;
     }();
     const bool v0 = variant == 0;
-    if (total_tiles > 0 && variant == 4) {
+    if (total_tiles > 0 && variant == 6) {
+        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, nullptr, 0, sm_count, s);
+    } else if (total_tiles > 0 && variant == 4) {
         static const bool attr = [] {
-            return cudaFuncSetAttribute(fp_v4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV3SmemBytes) ==
-                   cudaSuccess;
+            return cudaFuncSetAttribute(fp_v4_kernel<kV3Stages, kWarpsPerCta>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kV3SmemBytes) == cudaSuccess;
         }();
         (void)attr;
         const u64 want = (total_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
         const u64 cap = static_cast<u64>(sm_count) * 2;
         const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
-        fp_v4_kernel<<<blocks, kWarpsPerCta * 32, kV3SmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
+        fp_v4_kernel<kV3Stages, kWarpsPerCta>
+            <<<blocks, kWarpsPerCta * 32, kV3SmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
+    } else if (total_tiles > 0 && variant == 5) {
+        static const bool attr = [] {
+            return cudaFuncSetAttribute(fp_v4_kernel<kCopyStages, kCopyWarps>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kCopySmemBytes) == cudaSuccess;
+        }();
+        (void)attr;
+        const u64 want = (total_tiles + kCopyWarps - 1) / kCopyWarps;
+        const u64 cap = static_cast<u64>(sm_count) * 2;
+        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
+        fp_v4_kernel<kCopyStages, kCopyWarps>
+            <<<blocks, kCopyWarps * 32, kCopySmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
         g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     } else if (total_tiles > 0 && variant == 3) {
         static const bool attr = [] {

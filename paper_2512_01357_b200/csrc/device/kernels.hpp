@@ -24,22 +24,36 @@ struct FpTask {
     std::uint64_t tile0;       // first tile index of this task (prefix over tasks)
 };
 
-// sums: 2 u64 per task (must be zeroed), digests: 2 u64 per task.
+// sums: 2 u64 per task (must be zeroed), digests: 2 u64 per task, sync: one
+// u64 of device scratch private to this launch (zeroed by it).  Runs the load
+// kernel below with fingerprint-only tasks.
 void fp_launch(const FpTask* d_tasks, std::uint32_t n_tasks, std::uint64_t total_tiles, std::uint64_t* d_sums,
-               std::uint64_t* d_digests, int sm_count, cudaStream_t s);
+               std::uint64_t* d_digests, std::uint64_t* d_sync, int sm_count, cudaStream_t s);
 
-// ---- K3F: copy + fingerprint in one pass ----------------------------------
-// Moves every task's n bytes src -> dst (any alignments; the tasks of one
-// launch must be hazard-free, e.g. one WAR wave) and produces the tgfp1
-// digest of the moved bytes, reading them once.
+// ---- K3F: copy + fingerprint in one pass — the load kernel ---------------
+// Moves every task's n bytes src -> dst (any alignments) and produces the
+// tgfp1 digest of the moved bytes, reading them once; dst == nullptr only
+// fingerprints (a reused tensor verified in place).  One persistent launch
+// runs a whole load: warps take 128 KiB tiles in task order from a counter,
+// and a task with gate >= 0 writes nothing before every tile of WAR wave
+// `gate` has finished (its sources read) — so relocation waves, the
+// placements gated on them and the in-place verification share one launch.
 struct CopyFpTask {
     const std::uint8_t* src;
-    std::uint8_t* dst;
+    std::uint8_t* dst;    // nullptr: fingerprint only
     std::uint64_t n;
     std::uint64_t tile0;  // tile prefix (32 leaves per tile), relative to the launch
+    std::int32_t gate;    // wave that must be complete before this task writes (-1: none)
+    std::int32_t wave;    // wave this task belongs to (its tiles count towards need[wave]; -1: none)
 };
+// sync: 1 + n_waves u64 of device scratch (zeroed by the launch); need[w] =
+// tiles of wave w's tasks.  sums: 2 u64 per task (zeroed by the caller).
 void copy_fp_launch(const CopyFpTask* d_tasks, std::uint32_t n_tasks, std::uint64_t total_tiles, std::uint64_t* d_sums,
-                    std::uint64_t* d_digests, int sm_count, cudaStream_t s);
+                    std::uint64_t* d_digests, std::uint64_t* d_sync, const std::uint64_t* d_need,
+                    std::uint32_t n_waves, int sm_count, cudaStream_t s);
+// Warps one load-kernel launch keeps resident (tile-count sizing of the
+// independent work placed between gated waves).
+std::uint64_t copy_fp_resident_warps(int sm_count);
 
 // ---- K3: relocation wave (batched misaligned memcpy) ---------------------
 constexpr int kMaxMovesPerLaunch = 96;

@@ -301,8 +301,13 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     constexpr std::size_t kNone = ~std::size_t{0};
 
     // ---- descriptor tables (one H2D) ---------------------------------------------
-    // FpTask:     [K1 placements...][untouched hits...][relocated hits (unfused)...]
-    // CopyFpTask: [wave 0 moves...][wave 1 moves...]...[device-source placements...] (fused)
+    // FpTask (K1): [K1 placements...][unfused: untouched hits..., relocated hits...]
+    // CopyFpTask (fused: one load-kernel launch), in tile order, for g = 0..waves:
+    //   [wave g moves, gate g-1][device-source placements gated on wave g-1]
+    //   [a share of the in-place verifications of untouched hits]
+    // The verification share behind each gate keeps the warps that run out of
+    // gated work streaming while the wave's last tiles finish; the rest of the
+    // verifications follow the last group.
     std::vector<FpTask> tasks;
     std::vector<std::size_t> fp_of_placement(np, kNone);
     std::vector<u64> new_tiles;
@@ -314,75 +319,97 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
         new_tiles.push_back(tiles_of(tasks.back().n));
     }
     const std::size_t hit_base = tasks.size();
-    std::vector<FpTask> still, moved_hits;
-    if (fp_reuse)
+    u64 still_tiles = 0, moved_tiles = 0;
+    if (fp_reuse && !fused) {
+        std::vector<FpTask> still, moved_hits;
         for (std::size_t h = 0; h < hit_keys.size(); ++h) {
             const Entry* e = store_.entry(hit_keys[h]);
             (h < n_still ? still : moved_hits).push_back(FpTask{arena_ + e->off, e->size, 0});
         }
-    const u64 still_tiles = build_tasks(still), moved_tiles = build_tasks(moved_hits);
-    tasks.insert(tasks.end(), still.begin(), still.end());
-    if (!fused) tasks.insert(tasks.end(), moved_hits.begin(), moved_hits.end());
+        still_tiles = build_tasks(still);
+        moved_tiles = build_tasks(moved_hits);
+        tasks.insert(tasks.end(), still.begin(), still.end());
+        tasks.insert(tasks.end(), moved_hits.begin(), moved_hits.end());
+    }
     std::vector<CopyFpTask> ctasks;
-    std::vector<std::size_t> ctask_of_reloc(rel.size(), kNone), ctask_of_placement(np, kNone);
-    std::vector<std::size_t> wave_first(waves + 1, 0);
-    std::vector<u64> wave_tiles(waves, 0);
+    std::vector<std::size_t> ctask_of_reloc(rel.size(), kNone), ctask_of_placement(np, kNone),
+        ctask_of_still(hit_keys.size(), kNone);
+    std::vector<u64> need(waves, 0);
+    u64 ctiles = 0;
     if (fused) {
-        for (u32 w = 0; w < waves; ++w) {
-            wave_first[w] = ctasks.size();
-            u64 tl = 0;
-            for (std::size_t j = 0; j < rel.size(); ++j) {
-                if (rep->reloc_wave[j] != w) continue;
+        auto push = [&](const std::uint8_t* from, std::uint8_t* to, u64 n, int gate, int wave) {
+            ctasks.push_back(CopyFpTask{from, to, n, ctiles, gate, wave});
+            ctiles += tiles_of(n);
+            if (wave >= 0) need[static_cast<std::size_t>(wave)] += tiles_of(n);
+        };
+        const u64 share = 2 * copy_fp_resident_warps(sm_count_);
+        const std::size_t n_verify = fp_reuse ? n_still : 0;
+        std::size_t next_verify = 0;
+        for (u32 g = 0; g <= waves; ++g) {
+            const int gate = static_cast<int>(g) - 1;
+            for (std::size_t j = 0; g < waves && j < rel.size(); ++j) {
+                if (rep->reloc_wave[j] != g) continue;
                 ctask_of_reloc[j] = ctasks.size();
-                ctasks.push_back(CopyFpTask{arena_ + rel[j].from, arena_ + rel[j].to, rel[j].size, tl});
-                tl += tiles_of(rel[j].size);
+                push(arena_ + rel[j].from, arena_ + rel[j].to, rel[j].size, gate, static_cast<int>(g));
             }
-            wave_tiles[w] = tl;
-        }
-        wave_first[waves] = ctasks.size();
-        for (std::size_t i = 0; i < np; ++i) {
-            if (rep->placement_src[i] == 0) continue;
-            const auto& pl = D.plan.placements[i];
-            ctask_of_placement[i] = ctasks.size();
-            ctasks.push_back(CopyFpTask{peer_src[i], arena_ + pl.off, D.miss_desc[pl.tensor].size, 0});
+            for (std::size_t i = 0; i < np; ++i) {
+                if (rep->placement_src[i] == 0 || dep[i] != gate) continue;
+                ctask_of_placement[i] = ctasks.size();
+                push(peer_src[i], arena_ + D.plan.placements[i].off, D.miss_desc[D.plan.placements[i].tensor].size,
+                     gate, -1);
+            }
+            for (u64 got = 0; next_verify < n_verify && (g == waves || got < share); ++next_verify) {
+                const Entry* e = store_.entry(hit_keys[next_verify]);
+                ctask_of_still[next_verify] = ctasks.size();
+                push(arena_ + e->off, nullptr, e->size, -1, -1);
+                got += tiles_of(e->size);
+            }
         }
     }
     const std::size_t nf = tasks.size(), nc = ctasks.size();
     std::size_t n_fp_launch = 2;
     for (std::size_t i = 0; i < np; ++i) n_fp_launch += fp_of_placement[i] != kNone;
     ensure_events(ev_fp + 2 * n_fp_launch);
-    const std::size_t fdesc = nf * sizeof(FpTask), cdesc = nc * sizeof(CopyFpTask);
-    const std::size_t desc_bytes = (fdesc + cdesc + 15) & ~std::size_t{15};
+    // stage: [FpTask...][CopyFpTask...][need...] (H2D) | sums | digests | sync
+    const std::size_t fdesc = nf * sizeof(FpTask), cdesc = nc * sizeof(CopyFpTask), ndesc = waves * sizeof(u64);
+    const std::size_t desc_bytes = (fdesc + cdesc + ndesc + 15) & ~std::size_t{15};
     const std::size_t sums_bytes = (nf + nc) * 2 * sizeof(u64);
-    ensure_stage(desc_bytes + 2 * sums_bytes + 64);
+    ensure_stage(desc_bytes + 2 * sums_bytes + (1 + waves + n_fp_launch) * sizeof(u64) + 64);
     auto* h = static_cast<std::uint8_t*>(h_stage_);
     auto* dptr = static_cast<std::uint8_t*>(d_stage_);
     if (nf) std::memcpy(h, tasks.data(), fdesc);
     if (nc) std::memcpy(h + fdesc, ctasks.data(), cdesc);
+    if (waves) std::memcpy(h + fdesc + cdesc, need.data(), ndesc);
     const auto* d_tasks = reinterpret_cast<const FpTask*>(dptr);
     const auto* d_ctasks = reinterpret_cast<const CopyFpTask*>(dptr + fdesc);
+    const auto* d_need = reinterpret_cast<const u64*>(dptr + fdesc + cdesc);
     auto* d_sums = reinterpret_cast<u64*>(dptr + desc_bytes);
     auto* d_dig = reinterpret_cast<u64*>(dptr + desc_bytes + sums_bytes);
+    auto* d_sync = reinterpret_cast<u64*>(dptr + desc_bytes + 2 * sums_bytes);
+    u64* d_fp_sync = d_sync + 1 + waves;  // one tile counter per K1 launch
     if (nf + nc) {
         TG_CUDA(cudaMemcpyAsync(dptr, h, desc_bytes, cudaMemcpyHostToDevice, s_main_));
         TG_CUDA(cudaMemsetAsync(d_sums, 0, sums_bytes, s_main_));
     }
 
-    // ---- relocation waves on the main stream (K3F, or K3 unfused) ----------------
+    // ---- device work on the main stream: the load kernel (fused) or the K3
+    // relocation waves (unfused) ----------------------------------------------------
     TG_CUDA(cudaEventRecord(ev(1), s_main_));
-    for (u32 w = 0; w < waves; ++w) {
-        if (fused) {
-            const std::size_t c0 = wave_first[w], cn = wave_first[w + 1] - c0;
-            copy_fp_launch(d_ctasks + c0, static_cast<u32>(cn), wave_tiles[w], d_sums + 2 * (nf + c0),
-                           d_dig + 2 * (nf + c0), sm_count_, s_main_);
-        } else {
-            std::vector<MoveDesc> mv;
-            for (std::size_t j = 0; j < rel.size(); ++j)
-                if (rep->reloc_wave[j] == w)
-                    mv.push_back(MoveDesc{reinterpret_cast<u64>(arena_ + rel[j].from),
-                                          reinterpret_cast<u64>(arena_ + rel[j].to), rel[j].size});
-            relocate_launch(mv.data(), static_cast<int>(mv.size()), sm_count_, s_main_);
-        }
+    if (fused) {
+        copy_fp_launch(d_ctasks, static_cast<u32>(nc), ctiles, d_sums + 2 * nf, d_dig + 2 * nf, d_sync, d_need, waves,
+                       sm_count_, s_main_);
+        TG_CUDA(cudaGetLastError());
+        for (u32 w = 0; w < waves; ++w) TG_CUDA(cudaEventRecord(ev(ev_wave + w), s_main_));
+        for (std::size_t i = 0; i < np; ++i)
+            if (ctask_of_placement[i] != kNone) TG_CUDA(cudaEventRecord(ev(ev_land + i), s_main_));
+    }
+    for (u32 w = 0; !fused && w < waves; ++w) {
+        std::vector<MoveDesc> mv;
+        for (std::size_t j = 0; j < rel.size(); ++j)
+            if (rep->reloc_wave[j] == w)
+                mv.push_back(MoveDesc{reinterpret_cast<u64>(arena_ + rel[j].from), reinterpret_cast<u64>(arena_ + rel[j].to),
+                                      rel[j].size});
+        relocate_launch(mv.data(), static_cast<int>(mv.size()), sm_count_, s_main_);
         TG_CUDA(cudaGetLastError());
         TG_CUDA(cudaEventRecord(ev(ev_wave + w), s_main_));
     }
@@ -410,9 +437,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             waited = dep[i];
         }
         if (dev_src && fused) {
-            const std::size_t c = ctask_of_placement[i];
-            copy_fp_launch(d_ctasks + c, 1, tiles_of(sz), d_sums + 2 * (nf + c), d_dig + 2 * (nf + c), sm_count_, s);
-            TG_CUDA(cudaGetLastError());
+            continue;  // in the load kernel
         } else if (dev_src) {
             MoveDesc md{reinterpret_cast<u64>(peer_src[i]), reinterpret_cast<u64>(arena_ + pl.off), sz};
             relocate_launch(&md, 1, sm_count_, s);
@@ -439,7 +464,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
         if (k == kNone) continue;
         TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(ev_land + i)));
         TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s_fp_));
-        fp_launch(d_tasks + k, 1, new_tiles[k], d_sums + 2 * k, d_dig + 2 * k, sm_count_, s_fp_);
+        fp_launch(d_tasks + k, 1, new_tiles[k], d_sums + 2 * k, d_dig + 2 * k, d_fp_sync + fp_i, sm_count_, s_fp_);
         TG_CUDA(cudaGetLastError());
         TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s_fp_));
         ++fp_i;
@@ -453,15 +478,17 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             if (!count) return;
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s));
             fp_launch(d_tasks + first, static_cast<u32>(count), tiles, d_sums + 2 * first, d_dig + 2 * first,
-                      sm_count_, s);
+                      d_fp_sync + fp_i, sm_count_, s);
             TG_CUDA(cudaGetLastError());
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s));
             ++fp_i;
             ++fp_reuse_launches;
         };
         TG_CUDA(cudaStreamWaitEvent(s_verify_, ev(1)));
-        launch(s_verify_, hit_base, n_still, still_tiles);
-        if (!fused) launch(s_main_, hit_base + n_still, hit_keys.size() - n_still, moved_tiles);
+        if (!fused) {
+            launch(s_verify_, hit_base, n_still, still_tiles);
+            launch(s_main_, hit_base + n_still, hit_keys.size() - n_still, moved_tiles);
+        }
         TG_CUDA(cudaEventRecord(ev(8), s_verify_));
         TG_CUDA(cudaStreamWaitEvent(s_main_, ev(8)));
     }
@@ -478,7 +505,8 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     TG_CUDA(cudaStreamSynchronize(s_main_));
 
     rep->t.total_ms = ms_between(ev(0), ev(3));
-    rep->t.relocate_ms = waves ? ms_between(ev(1), ev(2)) : 0.0;
+    // fused: the whole load kernel (waves, device-source placements, verification)
+    rep->t.relocate_ms = (waves || (fused && nc)) ? ms_between(ev(1), ev(2)) : 0.0;
     rep->t.h2d_ms = rep->pcie_bytes ? ms_between(ev(4), ev(5)) : 0.0;
     rep->t.peer_ms = (rep->peer_bytes || rep->device_src_bytes) ? ms_between(ev(6), ev(7)) : 0.0;
     for (std::size_t f = 0; f < fp_i; ++f) {
@@ -524,7 +552,9 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     }
     for (std::size_t hix = 0; fp_reuse && hix < hit_keys.size(); ++hix) {
         const Key& k = hit_keys[hix];
-        const std::size_t slot = (hix < n_still || !fused) ? hit_base + hix : nf + ctask_of_reloc[reloc_of.at(k)];
+        const std::size_t slot = !fused          ? hit_base + hix
+                                 : hix < n_still ? nf + ctask_of_still[hix]
+                                                 : nf + ctask_of_reloc[reloc_of.at(k)];
         const Digest g = digest_at(slot);
         Entry* e = store_.entry(k);
         rep->digests[pos[k]] = g;
@@ -699,11 +729,11 @@ void fingerprint_device(const void* ptr, u64 n, int device, Digest* out) {
     cudaStream_t s;
     TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     void* d = nullptr;
-    TG_CUDA(cudaMallocAsync(&d, sizeof(FpTask) + 4 * sizeof(u64), s));
+    TG_CUDA(cudaMallocAsync(&d, sizeof(FpTask) + 5 * sizeof(u64), s));
     TG_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(FpTask), cudaMemcpyHostToDevice, s));
     auto* sums = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(d) + sizeof(FpTask));
     TG_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(u64), s));
-    fp_launch(static_cast<const FpTask*>(d), 1, tiles, sums, sums + 2, sms, s);
+    fp_launch(static_cast<const FpTask*>(d), 1, tiles, sums, sums + 2, sums + 4, sms, s);
     TG_CUDA(cudaGetLastError());
     u64 h[2];
     TG_CUDA(cudaMemcpyAsync(h, sums + 2, sizeof h, cudaMemcpyDeviceToHost, s));
@@ -729,18 +759,19 @@ double bench_fingerprint(const std::vector<std::pair<const void*, u64>>& bufs, i
     TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     void* d = nullptr;
     const std::size_t per = 4 * sizeof(u64) * nt;  // sums + digests per rep
-    TG_CUDA(cudaMalloc(&d, sizeof(FpTask) * nt + per * (reps + 1)));
+    TG_CUDA(cudaMalloc(&d, sizeof(FpTask) * nt + per * (reps + 1) + sizeof(u64)));
     TG_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(FpTask) * nt, cudaMemcpyHostToDevice, s));
     auto* sums = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(d) + sizeof(FpTask) * nt);
     TG_CUDA(cudaMemsetAsync(sums, 0, per * (reps + 1), s));
     auto rep_sums = [&](int r) { return sums + static_cast<std::size_t>(r) * 4 * nt; };
-    fp_launch(static_cast<const FpTask*>(d), nt, tiles, rep_sums(0), rep_sums(0) + 2 * nt, sms, s);  // warm-up
+    u64* sync = rep_sums(reps + 1);
+    fp_launch(static_cast<const FpTask*>(d), nt, tiles, rep_sums(0), rep_sums(0) + 2 * nt, sync, sms, s);  // warm-up
     cudaEvent_t a, b;
     TG_CUDA(cudaEventCreate(&a));
     TG_CUDA(cudaEventCreate(&b));
     TG_CUDA(cudaEventRecord(a, s));
     for (int r = 1; r <= reps; ++r)
-        fp_launch(static_cast<const FpTask*>(d), nt, tiles, rep_sums(r), rep_sums(r) + 2 * nt, sms, s);
+        fp_launch(static_cast<const FpTask*>(d), nt, tiles, rep_sums(r), rep_sums(r) + 2 * nt, sync, sms, s);
     TG_CUDA(cudaEventRecord(b, s));
     TG_CUDA(cudaGetLastError());
     std::vector<u64> h(2 * nt);
@@ -769,7 +800,7 @@ double bench_copy_fp(const std::vector<MoveDesc>& moves, int device, int reps, s
     u64 tiles = 0;
     for (const MoveDesc& m : moves) {
         t.push_back(CopyFpTask{reinterpret_cast<const std::uint8_t*>(m.src), reinterpret_cast<std::uint8_t*>(m.dst),
-                               m.len, tiles});
+                               m.len, tiles, -1, -1});
         tiles += ((m.len + kLeafBytes - 1) / kLeafBytes + kLeavesPerTile - 1) / kLeavesPerTile;
     }
     const u32 nt = static_cast<u32>(t.size());
@@ -777,18 +808,20 @@ double bench_copy_fp(const std::vector<MoveDesc>& moves, int device, int reps, s
     TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     void* d = nullptr;
     const std::size_t per = 4 * sizeof(u64) * nt;
-    TG_CUDA(cudaMalloc(&d, sizeof(CopyFpTask) * nt + per * (reps + 1)));
+    TG_CUDA(cudaMalloc(&d, sizeof(CopyFpTask) * nt + per * (reps + 1) + sizeof(u64)));
     TG_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(CopyFpTask) * nt, cudaMemcpyHostToDevice, s));
     auto* sums = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(d) + sizeof(CopyFpTask) * nt);
     TG_CUDA(cudaMemsetAsync(sums, 0, per * (reps + 1), s));
     auto rep_sums = [&](int r) { return sums + static_cast<std::size_t>(r) * 4 * nt; };
+    u64* sync = rep_sums(reps + 1);
     const auto* dt = static_cast<const CopyFpTask*>(d);
-    copy_fp_launch(dt, nt, tiles, rep_sums(0), rep_sums(0) + 2 * nt, sms, s);
+    copy_fp_launch(dt, nt, tiles, rep_sums(0), rep_sums(0) + 2 * nt, sync, nullptr, 0, sms, s);
     cudaEvent_t a, b;
     TG_CUDA(cudaEventCreate(&a));
     TG_CUDA(cudaEventCreate(&b));
     TG_CUDA(cudaEventRecord(a, s));
-    for (int r = 1; r <= reps; ++r) copy_fp_launch(dt, nt, tiles, rep_sums(r), rep_sums(r) + 2 * nt, sms, s);
+    for (int r = 1; r <= reps; ++r)
+        copy_fp_launch(dt, nt, tiles, rep_sums(r), rep_sums(r) + 2 * nt, sync, nullptr, 0, sms, s);
     TG_CUDA(cudaEventRecord(b, s));
     TG_CUDA(cudaGetLastError());
     std::vector<u64> h(2 * nt);

@@ -89,13 +89,13 @@ struct RemoteEntry {
 constexpr u32 kLoadVerifyReuse = 1u;     // fingerprint reused tensors, compare to the recorded digest
 constexpr u32 kLoadFingerprintNew = 2u;  // fingerprint placed tensors and record the digest
 constexpr u32 kLoadPeer = 4u;            // pull misses from peer pools that hold them
-// Opt-in: move + fingerprint relocated / device-sourced tensors in one pass
-// (K3F).  It reads those bytes once instead of twice, but per-lane hashing
-// makes it issue-bound (4.9 TB/s r+w alone vs 6.2 for K3 and 6.0 for K1), and
-// in the C2 step it measured 9.9 ms against 9.4 ms for the separate passes,
-// so the separate passes stay the default.
+// Default: the whole device side of a load is one load-kernel launch —
+// relocation waves, device-source placements and in-place verification, each
+// moved tensor fingerprinted from the copy's own read (C2 step: 8.8 ms, vs
+// 9.4 ms for the separate K3 waves + K1 passes, which remain available by
+// leaving this flag out).
 constexpr u32 kLoadFused = 8u;
-constexpr u32 kLoadDefault = kLoadVerifyReuse | kLoadFingerprintNew;
+constexpr u32 kLoadDefault = kLoadVerifyReuse | kLoadFingerprintNew | kLoadFused;
 
 struct LoadTimings {
     double plan_us = 0;          // host planning (decide)

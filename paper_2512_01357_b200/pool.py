@@ -259,7 +259,7 @@ class PackingStrictness(enum.IntEnum):
     LiteralGuard = 1
 
 
-LOAD_VERIFY_REUSE, LOAD_FINGERPRINT_NEW, LOAD_PEER = 1, 2, 4
+LOAD_VERIFY_REUSE, LOAD_FINGERPRINT_NEW, LOAD_PEER, LOAD_FUSED = 1, 2, 4, 8
 
 
 @dataclass
@@ -268,7 +268,7 @@ class LoadPolicy:
     strictness: PackingStrictness = PackingStrictness.Functional
     random_eviction: bool = False
     rng: Optional[Rng] = None
-    flags: int = LOAD_VERIFY_REUSE | LOAD_FINGERPRINT_NEW
+    flags: int = LOAD_VERIFY_REUSE | LOAD_FINGERPRINT_NEW | LOAD_FUSED
 
     def c(self):
         return N.LoadPolicyC(int(self.merge), int(self.strictness), int(self.random_eviction),

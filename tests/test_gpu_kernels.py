@@ -95,25 +95,27 @@ def test_relocation_kernel_random_alignments(tg):
 
 @pytest.mark.parametrize("n", [0, 1, 15, 17, 4095, 4096, 4097, 8192, 4096 * 31 + 7, 4096 * 32, 4096 * 33 + 1,
                                (1 << 21) + 4093, 131072 * 5 + 999])
-@pytest.mark.parametrize("so,do", [(0, 0), (0, 5), (5, 0), (3, 11), (11, 3), (7, 7), (15, 1), (1, 15)])
-def test_copy_fingerprint_fused(tg, cpu, n, so, do):
+@pytest.mark.parametrize("so,do", [(0, 0), (0, 5), (5, 0), (3, 11), (11, 3), (7, 7), (15, 1), (1, 15), (0, 8)])
+@pytest.mark.parametrize("pad", [16, 32, 64, 112])
+def test_copy_fingerprint_fused(tg, cpu, n, so, do, pad):
     """K3F moves the bytes exactly (including head/tail bytes, neighbours
-    untouched) and returns the same digest as tgfp1 on the CPU."""
+    untouched) and returns the same digest as tgfp1 on the CPU.  `pad` moves
+    the destination across the 128-byte line phases the line stores use."""
     from paper_2512_01357_b200 import _native as N
     from paper_2512_01357_b200.checkpoint import DeviceBuffer
     rng = np.random.default_rng(n * 131 + so * 17 + do)
     data = rng.integers(0, 256, size=n + 64, dtype=np.uint8)
-    src, dst = DeviceBuffer(n + 128), DeviceBuffer(n + 128)
+    src, dst = DeviceBuffer(n + 128), DeviceBuffer(n + 256)
     N.lib.tg_memcpy(C.c_void_p(src.ptr), data.ctypes.data_as(C.c_void_p), n + 64)
-    guard = np.full(n + 128, 0x5A, dtype=np.uint8)
-    N.lib.tg_memcpy(C.c_void_p(dst.ptr), guard.ctypes.data_as(C.c_void_p), n + 128)
-    mv = (C.c_uint64 * 3)(src.ptr + so, dst.ptr + 32 + do, n)
+    guard = np.full(n + 256, 0x5A, dtype=np.uint8)
+    N.lib.tg_memcpy(C.c_void_p(dst.ptr), guard.ctypes.data_as(C.c_void_p), n + 256)
+    mv = (C.c_uint64 * 3)(src.ptr + so, dst.ptr + pad + do, n)
     dig = (N.DigestC * 1)()
     assert N.lib.tg_copy_fingerprint(mv, 1, 0, 0, None, dig) == 0, N.lib.tg_last_error_detail()
-    out = np.empty(n + 128, dtype=np.uint8)
-    N.lib.tg_memcpy(out.ctypes.data_as(C.c_void_p), C.c_void_p(dst.ptr), n + 128)
-    assert np.array_equal(out[32 + do:32 + do + n], data[so:so + n])
-    assert np.all(out[:32 + do] == 0x5A) and np.all(out[32 + do + n:] == 0x5A)
+    out = np.empty(n + 256, dtype=np.uint8)
+    N.lib.tg_memcpy(out.ctypes.data_as(C.c_void_p), C.c_void_p(dst.ptr), n + 256)
+    assert np.array_equal(out[pad + do:pad + do + n], data[so:so + n])
+    assert np.all(out[:pad + do] == 0x5A) and np.all(out[pad + do + n:] == 0x5A)
     assert (dig[0].hi, dig[0].lo) == cpu.content_fingerprint(data[so:so + n].copy(), threads=4)[0]
 
 

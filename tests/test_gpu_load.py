@@ -335,3 +335,53 @@ def test_model_store_file_sources(tg, cpu, tmp_path):
     for t in m.tensors:
         N.lib.tg_host_unregister(t.id.c())
     pool.close()
+
+
+@pytest.mark.parametrize("source", ["hbm", "host"])
+@pytest.mark.parametrize("seed", [52, 51, 13])
+def test_fused_load_kernel_fuzz(tg, cpu, seed, source):
+    """Odd-sized models rotating through a small pool: loads with up to 8 WAR
+    waves, device-source placements gated on them and in-place verification,
+    all in one load-kernel launch (TG_LOAD_FUSED).  Decisions and digests
+    equal the unfused path (K3 waves + K1) load by load, and every resident
+    tensor's bytes equal the CPU restatement's.  (Seeds chosen on the control
+    plane for their wave counts.)"""
+    import random
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    mb = 1 << 20
+    rng = random.Random(seed)
+    models = [tg.make_model(f"m{seed}_{k}", rng.randrange(40 * mb, 90 * mb) | 1, rng.randrange(2, 6), 64)
+              for k in range(4)]
+    size = rng.randrange(120 * mb, 170 * mb)
+    seq = [rng.randrange(4) for _ in range(12)]
+    src = HbmCache(tg, models) if source == "hbm" else HostCheckpoint(models).__enter__()
+    pools = {f: tg.ReuseStore(tg.GpuSpec(pool_size=size), device=0) for f in (False, True)}
+    stats = {f: tg.ModelStatsTable() for f in pools}
+    expected, waves = {}, 0
+    try:
+        for i, k in enumerate(seq):
+            m = models[k]
+            res = {}
+            for f, pool in pools.items():
+                stats[f].record_request(m.model_id, 10.0 * i)
+                stats[f].set_load_bandwidth(m.model_id, 55e9)
+                res[f] = pool.load_model(m, stats[f], 10.0 * i, tg.LoadPolicy(merge=i % 2, flags=1 | 2 | (8 if f else 0)))
+            assert result_json(res[True]) == result_json(res[False]), f"load {i}"
+            if not res[True].ok():
+                continue
+            o, u = res[True].value(), res[False].value()
+            waves = max(waves, o.waves)
+            assert o.digests == u.digests, f"load {i}"
+            assert o.verify_mismatches == 0 and o.repaired_bytes == 0
+            _check_pooled_bytes(tg, cpu, pools[True], expected)
+            for pool in pools.values():
+                pool.end_instance(m.model_id)
+        assert pools[True].dump() == pools[False].dump()
+        assert waves >= 4
+    finally:
+        for pool in pools.values():
+            pool.close()
+        if source == "hbm":
+            src.close()
+        else:
+            src.__exit__(None, None, None)

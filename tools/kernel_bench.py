@@ -37,7 +37,7 @@ def main():
         buf = DeviceBuffer(n + 64, dev)
         lib.tg_synth_fill_device(tg.TensorId(1, 2).c(), 0, n + 64, C.c_void_p(buf.ptr), dev)
         res = {}
-        for shift in (0, 3, 8, 13):
+        for shift in (3, 0, 8, 13, 0):
             ms = C.c_double()
             d = N.DigestC()
             ptrs = (C.c_void_p * 1)(buf.ptr + shift)
@@ -59,12 +59,18 @@ def main():
             res[f"src{so}_dst{do}"] = {"ms": ms.value, "GBps_rw": 2 * size / ms.value / 1e6}
         out["reloc"] = {"bytes_per_launch": size, **res}
         res = {}
-        for so, do in ((0, 0), (3, 11), (13, 2)):
+        for so, do in ((0, 0), (3, 3), (0, 8), (3, 11), (13, 2)):
             ms = C.c_double()
             mv = (C.c_uint64 * 3)(a.ptr + so, b.ptr + do, size)
             dg = (N.DigestC * 1)()
             N.check_runtime(lib.tg_copy_fingerprint(mv, 1, dev, args.reps, C.byref(ms), dg), "bench K3F")
             res[f"src{so}_dst{do}"] = {"ms": ms.value, "GBps_rw": 2 * size / ms.value / 1e6}
+        for so in (0, 3):  # in-place verification through the load kernel (dst = nullptr)
+            ms = C.c_double()
+            mv = (C.c_uint64 * 3)(a.ptr + so, 0, size)
+            dg = (N.DigestC * 1)()
+            N.check_runtime(lib.tg_copy_fingerprint(mv, 1, dev, args.reps, C.byref(ms), dg), "bench K3F verify")
+            res[f"verify_src{so}"] = {"ms": ms.value, "GBps_read": size / ms.value / 1e6}
         out["copy_fp"] = {"bytes_per_launch": size, **res}
         a.free()
         b.free()

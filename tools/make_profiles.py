@@ -41,6 +41,34 @@ def launch_shares(path):
                           for k, v in sorted(per.items(), key=lambda kv: -kv[1][1])}}
 
 
+def _bytes(v):
+    val, unit = v
+    return float(val.replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
+
+
+def traffic(rep, out_path):
+    """DRAM traffic of the bench step's load-kernel launch against the step's
+    algorithmic bytes (printed by the same bench --profile run)."""
+    launches = summarise(rep)
+    algo = None
+    log = os.path.join(OUT, "prof_load.log")
+    if os.path.exists(log):
+        for ln in open(log):
+            if ln.startswith("{"):
+                algo = json.loads(ln).get("roofline_step", {}).get("algorithmic_bytes_per_step")
+    per = [{"ms": float(r["gpu__time_duration.sum"][0]) / (1e3 if r["gpu__time_duration.sum"][1] == "usecond" else 1),
+            "dram_read_bytes": _bytes(r["dram__bytes_read.sum"]),
+            "dram_write_bytes": _bytes(r["dram__bytes_write.sum"]),
+            "dram_pct_of_peak": r["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"][0]} for r in launches]
+    t = sum(x["dram_read_bytes"] + x["dram_write_bytes"] for x in per)
+    with open(out_path, "w") as f:
+        json.dump({"traffic_bytes_per_launch": t, "algorithmic_bytes": algo,
+                   "ratio": t / algo if algo else None,
+                   "source": "ncu --set full --clock-control none of the bench step's load-kernel launch "
+                             "(bench.py --profile --steps 1 --warmup 0); dram__bytes_read.sum + dram__bytes_write.sum",
+                   "per_launch": per}, f, indent=1)
+
+
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(PROF, exist_ok=True)
@@ -57,6 +85,9 @@ def main():
         with open(os.path.join(PROF, f"{tag}_launches_summary.json"), "w") as f:
             json.dump(launch_shares(lp), f, indent=1)
         subprocess.run(["cp", lp, os.path.join(PROF, f"{tag}_launches.csv")])
+    lk = os.path.join(OUT, "prof_load.ncu-rep")
+    if os.path.exists(lk):
+        traffic(lk, os.path.join(PROF, "load_kernel_traffic.json"))
     for extra in ("kernel_bench.json", "bench.json"):
         p = os.path.join(OUT, extra)
         if os.path.exists(p):
