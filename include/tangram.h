@@ -237,6 +237,35 @@ int tg_validate(const tg_pool* p);                                         /* :2
 int tg_dump(const tg_pool* p, char* buf, uint64_t cap, uint64_t* needed);  /* :270 (JSON) */
 int tg_regions(const tg_pool* p, tg_region* buf, uint64_t cap, uint64_t* n); /* RegionList::snapshot */
 int tg_tensor_info_get(const tg_pool* p, tg_tensor_id id, tg_tensor_info* out);
+/* ---- device tensor index -------------------------------------
+ * The pool's tensor map (ReuseStore::tensors_ reuse_store.hpp:338, TensorEntry
+ * :26-32) mirrored in HBM as an open-addressing table for device-side
+ * consumers: capacity a power of two >= 2 x entries (>= 1024), home slot
+ * key.lo & (capacity - 1), linear probing, one 64-byte slot per probe.  Every
+ * mutating call (load_model, end_instance, evict_*, move_tensor, restore)
+ * re-publishes it on the pool stream; include/tangram_index.cuh probes it. */
+typedef struct {
+    uint64_t key_hi, key_lo;
+    uint64_t offset, size;
+    double last_access;
+    uint64_t model; /* murmur3_x64_128(model id, seed 0).lo of the owning model */
+    uint32_t flags; /* TG_INDEX_OCCUPIED | TG_INDEX_PINNED */
+    uint32_t reserved0;
+    uint64_t reserved1;
+} tg_index_slot;
+#define TG_INDEX_OCCUPIED 1u
+#define TG_INDEX_PINNED 2u
+typedef struct {
+    uint64_t offset, size;
+    uint32_t found, flags;
+} tg_index_hit;
+/* Host image of the table (any pool, device or not): writes min(capacity,
+ * cap_slots) slots to buf (nullable) and the capacity to *capacity. */
+int tg_pool_index_image(const tg_pool* p, tg_index_slot* buf, uint64_t cap_slots, uint64_t* capacity);
+/* The published device table (device pools). */
+int tg_pool_device_index(tg_pool* p, const tg_index_slot** table, uint64_t* capacity);
+/* Batch lookup through the device table (one thread per key, K6), results to host. */
+int tg_index_lookup(tg_pool* p, const tg_tensor_id* ids, uint32_t n, tg_index_hit* out);
 int tg_fingerprint_tensor(tg_pool* p, tg_tensor_id id, tg_digest* out);    /* K1 over resident bytes */
 int tg_pool_add_peer(tg_pool* p, tg_pool* peer);                           /* NVLink peer pool (K5) */
 /* Peers in other processes (one process per GPU): export the

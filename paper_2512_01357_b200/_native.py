@@ -99,6 +99,15 @@ class IndexEntryC(C.Structure):
     _fields_ = [("id", TensorIdC), ("offset", u64), ("size", u64), ("digest", DigestC)]
 
 
+class IndexSlotC(C.Structure):
+    _fields_ = [("key_hi", u64), ("key_lo", u64), ("offset", u64), ("size", u64), ("last_access", dbl),
+                ("model", u64), ("flags", u32), ("reserved0", u32), ("reserved1", u64)]
+
+
+class IndexHitC(C.Structure):
+    _fields_ = [("offset", u64), ("size", u64), ("found", u32), ("flags", u32)]
+
+
 class GpuSnapshotC(C.Structure):
     _fields_ = [("gpu_id", cp), ("available", i32), ("pool_size", u64), ("free_bytes", u64),
                 ("pcie_bandwidth", dbl), ("store_bandwidth", dbl), ("nvlink_bandwidth", dbl)]
@@ -154,6 +163,9 @@ _SIGS = {
     "tg_dump": (C.c_int, [vp, C.c_char_p, u64, P(u64)]),
     "tg_regions": (C.c_int, [vp, P(RegionC), u64, P(u64)]),
     "tg_tensor_info_get": (C.c_int, [vp, TensorIdC, P(TensorInfoC)]),
+    "tg_pool_index_image": (C.c_int, [vp, P(IndexSlotC), u64, P(u64)]),
+    "tg_pool_device_index": (C.c_int, [vp, P(vp), P(u64)]),
+    "tg_index_lookup": (C.c_int, [vp, P(TensorIdC), u32, P(IndexHitC)]),
     "tg_fingerprint_tensor": (C.c_int, [vp, TensorIdC, P(DigestC)]),
     "tg_pool_add_peer": (C.c_int, [vp, vp]),
     "tg_pool_export_ipc": (C.c_int, [vp, vp]),

@@ -100,6 +100,12 @@ void kv_release_launch(const std::uint64_t* table_row, std::uint64_t blocks, std
 void synth_launch(std::uint64_t hi, std::uint64_t lo, std::uint64_t begin, std::uint64_t len, std::uint8_t* dst,
                   cudaStream_t s);
 
+// ---- K6: device tensor index lookup ------------------------------------------
+// table: tg_index_slot[capacity] (include/tangram.h); keys: (hi, lo) pairs;
+// out: 3 u64 per key = offset, size, found | flags << 32 (offset ~0 when absent).
+void index_lookup_launch(const void* table, std::uint64_t capacity, const std::uint64_t* d_keys, std::uint32_t n,
+                         std::uint64_t* d_out, cudaStream_t s);
+
 // ---- K5: peer pull (SM copy over NVLink peer mappings) -----------------------
 // Reuses the relocation kernel: the source address is a peer arena pointer.
 

@@ -14,6 +14,7 @@
 #include "../device/common.cuh"
 #include "../device/kernels.hpp"
 #include "kv.hpp"
+#include "index.hpp"
 #include "pool.hpp"
 #include "sched.hpp"
 
@@ -408,16 +409,32 @@ uint32_t tg_last_digests(const tg_pool* p, tg_digest* buf, uint32_t cap) {
 }
 
 int tg_end_instance(tg_pool* p, const char* m) {
-    p->pool->store().end_instance(m);
-    return 0;
+    return guard([&] {
+        p->pool->store().end_instance(m);
+        p->pool->publish_index();
+        return 0;
+    });
 }
-int tg_evict_tensor(tg_pool* p, tg_tensor_id id) { return code_of(p->pool->store().evict_tensor(key_of(id))); }
+int tg_evict_tensor(tg_pool* p, tg_tensor_id id) {
+    return guard([&] {
+        const int rc = code_of(p->pool->store().evict_tensor(key_of(id)));
+        p->pool->publish_index();
+        return rc;
+    });
+}
 int tg_evict_model(tg_pool* p, const char* m) {
-    p->pool->store().evict_model(m);
-    return 0;
+    return guard([&] {
+        p->pool->store().evict_model(m);
+        p->pool->publish_index();
+        return 0;
+    });
 }
 int tg_move_tensor(tg_pool* p, tg_tensor_id id, uint64_t to) {
-    return guard([&] { return code_of(p->pool->move_tensor(key_of(id), to)); });
+    return guard([&] {
+        const int rc = code_of(p->pool->move_tensor(key_of(id), to));
+        p->pool->publish_index();
+        return rc;
+    });
 }
 int tg_alloc_kv_region(tg_pool* p, uint64_t size, uint64_t block_id, uint64_t* off) {
     auto r = p->pool->store().alloc_kv_region(size, block_id);
@@ -490,6 +507,40 @@ int tg_tensor_info_get(const tg_pool* p, tg_tensor_id id, tg_tensor_info* o) {
     return 0;
 }
 
+int tg_pool_index_image(const tg_pool* p, tg_index_slot* buf, uint64_t cap_slots, uint64_t* capacity) {
+    return guard([&] {
+        if (!p || !capacity) return TG_ERR_BAD_ARG;
+        static_assert(sizeof(tg_index_slot) == sizeof(IndexSlot), "index slot layout");
+        const std::vector<IndexSlot> img = build_index_image(p->pool->store());
+        *capacity = img.size();
+        if (buf) std::memcpy(buf, img.data(), std::min<uint64_t>(cap_slots, img.size()) * sizeof(IndexSlot));
+        return 0;
+    });
+}
+int tg_pool_device_index(tg_pool* p, const tg_index_slot** table, uint64_t* capacity) {
+    return guard([&] {
+        if (!p || !table || !capacity) return TG_ERR_BAD_ARG;
+        if (!p->pool->has_device()) return TG_ERR_NO_DEVICE;
+        p->pool->publish_index();
+        *table = static_cast<const tg_index_slot*>(p->pool->device_index(capacity));
+        return 0;
+    });
+}
+int tg_index_lookup(tg_pool* p, const tg_tensor_id* ids, uint32_t n, tg_index_hit* out) {
+    return guard([&] {
+        if (!p || (n && (!ids || !out))) return TG_ERR_BAD_ARG;
+        if (!p->pool->has_device()) return TG_ERR_NO_DEVICE;
+        std::vector<Key> keys(n);
+        for (uint32_t i = 0; i < n; ++i) keys[i] = key_of(ids[i]);
+        std::vector<u64> r;
+        p->pool->index_lookup(keys, &r);
+        for (uint32_t i = 0; i < n; ++i)
+            out[i] = tg_index_hit{r[3 * i], r[3 * i + 1], static_cast<uint32_t>(r[3 * i + 2] & 1),
+                                  static_cast<uint32_t>(r[3 * i + 2] >> 32)};
+        return 0;
+    });
+}
+
 int tg_fingerprint_tensor(tg_pool* p, tg_tensor_id id, tg_digest* out) {
     return guard([&] {
         if (!p->pool->store().tensors().count(key_of(id))) return code_of(Err::NotFound);
@@ -559,6 +610,7 @@ int tg_pool_snapshot(tg_pool* p, tg_snapshot** out) {
 int tg_pool_restore(tg_pool* p, const tg_snapshot* s) {
     return guard([&] {
         p->pool->restore(s->s);
+        p->pool->publish_index();
         return 0;
     });
 }
@@ -737,6 +789,7 @@ int tg_kv_ensure_capacity(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t rid
         if (n_granted) *n_granted = n;
         if (want)
             for (u64 i = 0; i < g.size() && i < cap; ++i) granted[i] = g[i];
+        p->pool->publish_index();  // a contended grant may have evicted tensors
         return code_of(st);
     });
 }
@@ -758,6 +811,7 @@ int tg_kv_batch_allocate(tg_kv* kv, tg_pool* p, const tg_stats* s, const uint64_
         if (total) *total = t;
         if (want)
             for (u64 i = 0; i < g.size() && i < cap; ++i) pbns[i] = g[i];
+        p->pool->publish_index();
         return code_of(st);
     });
 }
@@ -775,7 +829,9 @@ int tg_kv_teardown(tg_kv* kv, tg_pool* p) {
 int tg_kv_urgent_reclaim(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t blocks) {
     return guard([&] {
         if (int rc = bind_kv(kv, p)) return rc;
-        return code_of(kv->a->urgent_reclaim(p->pool->store(), s->s_view(), blocks));
+        const int rc = code_of(kv->a->urgent_reclaim(p->pool->store(), s->s_view(), blocks));
+        p->pool->publish_index();
+        return rc;
     });
 }
 int tg_kv_table(const tg_kv* kv, uint64_t rid, uint64_t* pbns, uint64_t cap, uint64_t* n, uint64_t* token_count) {

@@ -5,12 +5,14 @@
 #include <fcntl.h>
 #include <unistd.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <unordered_set>
 
 #include "../device/common.cuh"
 #include "../device/kernels.hpp"
+#include "index.hpp"
 
 namespace tg {
 
@@ -138,6 +140,57 @@ Pool::~Pool() {
     if (arena_) cudaFree(arena_);
     if (d_stage_) cudaFree(d_stage_);
     if (h_stage_) cudaFreeHost(h_stage_);
+    if (d_index_) cudaFree(d_index_);
+    if (h_index_) cudaFreeHost(h_index_);
+    if (ev_index_) cudaEventDestroy(ev_index_);
+}
+
+void Pool::publish_index() {
+    if (!has_device() || store_.epoch() == published_epoch_) return;
+    DeviceScope ds(device_);
+    const std::vector<IndexSlot> img = build_index_image(store_);
+    const u64 cap = img.size(), bytes = cap * sizeof(IndexSlot);
+    if (ev_index_) TG_CUDA(cudaEventSynchronize(ev_index_));  // the previous image has been read
+    else TG_CUDA(cudaEventCreateWithFlags(&ev_index_, cudaEventDisableTiming));
+    if (cap > h_index_cap_) {
+        if (h_index_) TG_CUDA(cudaFreeHost(h_index_));
+        TG_CUDA(cudaHostAlloc(&h_index_, bytes, cudaHostAllocDefault));
+        h_index_cap_ = cap;
+    }
+    if (cap != index_cap_) {  // the table grew: consumers re-query tg_pool_device_index
+        if (d_index_) {
+            TG_CUDA(cudaStreamSynchronize(s_main_));
+            TG_CUDA(cudaFree(d_index_));
+        }
+        TG_CUDA(cudaMalloc(&d_index_, bytes));
+        index_cap_ = cap;
+    }
+    std::memcpy(h_index_, img.data(), bytes);
+    TG_CUDA(cudaMemcpyAsync(d_index_, h_index_, bytes, cudaMemcpyHostToDevice, s_main_));
+    TG_CUDA(cudaEventRecord(ev_index_, s_main_));
+    published_epoch_ = store_.epoch();
+}
+
+void Pool::index_lookup(const std::vector<Key>& keys, std::vector<u64>* out) {
+    if (!has_device()) throw DeviceError(kErrNoDevice, "index lookup on a control-plane pool");
+    publish_index();
+    DeviceScope ds(device_);
+    const std::size_t n = keys.size();
+    out->assign(3 * n, 0);
+    if (!n) return;
+    ensure_stage(n * 5 * sizeof(u64) + 64);
+    auto* h = static_cast<u64*>(h_stage_);
+    auto* d = static_cast<u64*>(d_stage_);
+    for (std::size_t i = 0; i < n; ++i) {
+        h[2 * i] = keys[i].hi;
+        h[2 * i + 1] = keys[i].lo;
+    }
+    TG_CUDA(cudaMemcpyAsync(d, h, 2 * n * sizeof(u64), cudaMemcpyHostToDevice, s_main_));
+    index_lookup_launch(d_index_, index_cap_, d, static_cast<u32>(n), d + 2 * n, s_main_);
+    TG_CUDA(cudaGetLastError());
+    TG_CUDA(cudaMemcpyAsync(h + 2 * n, d + 2 * n, 3 * n * sizeof(u64), cudaMemcpyDeviceToHost, s_main_));
+    TG_CUDA(cudaStreamSynchronize(s_main_));
+    std::memcpy(out->data(), h + 2 * n, 3 * n * sizeof(u64));
 }
 
 void Pool::ensure_events(std::size_t n) {
@@ -342,7 +395,11 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             ctiles += tiles_of(n);
             if (wave >= 0) need[static_cast<std::size_t>(wave)] += tiles_of(n);
         };
-        const u64 share = 2 * copy_fp_resident_warps(sm_count_);
+        static const u64 rounds = [] {
+            const char* e = std::getenv("TANGRAM_VERIFY_ROUNDS");  // A/B knob
+            return e ? std::strtoull(e, nullptr, 10) : 2ull;
+        }();
+        const u64 share = rounds * copy_fp_resident_warps(sm_count_);
         const std::size_t n_verify = fp_reuse ? n_still : 0;
         std::size_t next_verify = 0;
         for (u32 g = 0; g <= waves; ++g) {
@@ -492,6 +549,8 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
         TG_CUDA(cudaEventRecord(ev(8), s_verify_));
         TG_CUDA(cudaStreamWaitEvent(s_main_, ev(8)));
     }
+    // ---- device index: the committed map, published behind the data plane ------
+    publish_index();
     // ---- join, read digests, end ------------------------------------------------
     TG_CUDA(cudaStreamWaitEvent(s_main_, ev(5)));
     TG_CUDA(cudaStreamWaitEvent(s_main_, ev(7)));

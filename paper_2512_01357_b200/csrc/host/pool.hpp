@@ -164,6 +164,17 @@ public:
 
     std::unique_ptr<KvDevice> make_kv_device();
 
+    // Device tensor index: republish the store's tensor map to
+    // HBM on the pool stream when it changed since the last publish (no-op on
+    // control-plane pools).  device_index() is the published table.
+    void publish_index();
+    const void* device_index(u64* capacity) const {
+        *capacity = index_cap_;
+        return d_index_;
+    }
+    // One device lookup per key (K6); out: 3 u64 per key (offset, size, found | flags << 32).
+    void index_lookup(const std::vector<Key>& keys, std::vector<u64>* out);
+
 private:
     void ensure_events(std::size_t n);
     void fetch(const HostSource& hs, std::uint8_t* dst, u64 size, cudaStream_t s);
@@ -188,6 +199,13 @@ private:
     void* d_stage_ = nullptr;
     std::size_t stage_cap_ = 0;
     void ensure_stage(std::size_t bytes);
+    // device index
+    void* d_index_ = nullptr;
+    u64 index_cap_ = 0;
+    void* h_index_ = nullptr;  // pinned image being uploaded
+    u64 h_index_cap_ = 0;
+    cudaEvent_t ev_index_ = nullptr;
+    u64 published_epoch_ = ~u64{0};
 };
 
 std::unique_ptr<KvDevice> make_kv_device(int device, cudaStream_t stream);

@@ -1,6 +1,7 @@
 #include "store.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 
 #include "json_out.hpp"
@@ -68,7 +69,13 @@ Res<LoadDecision> Store::decide(const ModelDesc& m, const StatsView& stats, cons
     return d;
 }
 
+void Store::touch() {
+    static std::atomic<u64> next{0};
+    epoch_ = ++next;
+}
+
 void Store::commit(const ModelDesc& m, LoadDecision& d, double clock) {
+    touch();
     if (!d.misses.empty()) {
         for (const auto& ev : d.plan.evictions) {
             tensors_.erase(ev.tensor);
@@ -101,6 +108,7 @@ void Store::commit(const ModelDesc& m, LoadDecision& d, double clock) {
 }
 
 void Store::end_instance(const std::string& model) {
+    touch();
     for (auto& [k, e] : tensors_)
         if (e.model == model && e.pinned) {
             e.pinned = false;
@@ -115,10 +123,12 @@ St Store::evict_tensor(const Key& k) {
     map_.release(it->second.off);
     tensors_.erase(it);
     ++evictions_total_;
+    touch();
     return ok();
 }
 
 void Store::evict_model(const std::string& model) {
+    touch();
     std::vector<Key> ids;
     for (const auto& [k, e] : tensors_)
         if (e.model == model) ids.push_back(k);
@@ -141,6 +151,7 @@ St Store::move_tensor(const Key& k, u64 to) {
     if (!st) return st;
     it->second.off = to;
     merged_total_ += it->second.size;
+    touch();
     return ok();
 }
 

@@ -110,6 +110,10 @@ public:
     u64 evictions_total() const { return evictions_total_; }
     const PoolMap& map() const { return map_; }
     const std::unordered_map<Key, Entry, KeyHash>& tensors() const { return tensors_; }
+    // Changes whenever the tensor map's offsets, sizes, pins or access times
+    // change; values are unique process-wide, so copies and restores compare
+    // unequal to any other state.  (Drives the device index republish.)
+    u64 epoch() const { return epoch_; }
     Entry* entry(const Key& k) {
         auto it = tensors_.find(k);
         return it == tensors_.end() ? nullptr : &it->second;
@@ -144,6 +148,8 @@ public:
     std::string dump_json() const;
 
 private:
+    void touch();
+    u64 epoch_ = 0;
     double alpha_of(const std::string& m) const {
         auto it = alpha_.find(m);
         return it == alpha_.end() ? 1.0 : it->second;

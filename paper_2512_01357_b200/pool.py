@@ -485,6 +485,32 @@ class ReuseStore:
                 "has_digest": bool(i.has_digest), "digest": (i.digest.hi, i.digest.lo),
                 "device_ptr": i.device_ptr}
 
+    # -- device tensor index ------------------------------------------
+    def index_image(self):
+        """(capacity, [slot dicts]) of the open-addressing table the device holds
+        (built on the host; available on control-plane pools too)."""
+        cap = C.c_uint64()
+        N.check_runtime(lib.tg_pool_index_image(self._h, None, 0, C.byref(cap)), "tg_pool_index_image")
+        buf = (N.IndexSlotC * cap.value)()
+        N.check_runtime(lib.tg_pool_index_image(self._h, buf, cap.value, C.byref(cap)), "tg_pool_index_image")
+        return cap.value, [{"key": (b.key_hi, b.key_lo), "offset": b.offset, "size": b.size,
+                            "last_access": b.last_access, "model": b.model, "flags": b.flags} for b in buf]
+
+    def device_index(self):
+        """(device pointer, capacity) of the published table (tg_index_slot[capacity])."""
+        ptr, cap = C.c_void_p(), C.c_uint64()
+        N.check_runtime(lib.tg_pool_device_index(self._h, C.byref(ptr), C.byref(cap)), "tg_pool_device_index")
+        return ptr.value, cap.value
+
+    def index_lookup(self, ids):
+        """Device lookups (K6): [None | {"offset", "size", "pinned"}] per TensorId."""
+        n = len(ids)
+        keys = (N.TensorIdC * max(1, n))(*[t.c() for t in ids])
+        out = (N.IndexHitC * max(1, n))()
+        N.check_runtime(lib.tg_index_lookup(self._h, keys, n, out), "tg_index_lookup")
+        return [{"offset": h.offset, "size": h.size, "pinned": bool(h.flags & 2)} if h.found else None
+                for h in out[:n]]
+
     def fingerprint_tensor(self, tid: TensorId):
         d = N.DigestC()
         rc = lib.tg_fingerprint_tensor(self._h, tid.c(), C.byref(d))
