@@ -405,6 +405,8 @@ def run_ours(args):
         lib.tg_host_clear()
         extras["c1"] = run_c1(tg, local)
         extras["c3"] = run_c3(tg, local)
+        if local == 0:
+            extras["c5"] = run_c5(local)
     if not args.no_cpu_baseline and world == 1 and not args.profile:
         cpu_base = cpu_baseline(args)
 
@@ -678,6 +680,45 @@ def run_c3(tg, dev):
     pool.close()
     return {"workload": "C3 Llama-2-13B (26 GB) in a 120 GiB pool; KV blocks of 16 tokens x 819,200 B/token; "
                         "host+device time per batch incl. kernel completion, best of 3", "bursts": out}
+
+
+def run_c5(dev):
+    """C5: the reference's own Simulator (unmodified
+    simulator.hpp) replays the Zipf trace over the drop-in bindings; pool gpu0
+    lives on this GPU and really moves and fingerprints bytes (every catalog
+    tensor's source synthesised in HBM), the other seven pools are
+    control-plane only.  RunMetrics must equal the pure-reference build's."""
+    import time
+    build = os.path.join(ROOT, "integration", "_build")
+    ref_bin, tg_bin = os.path.join(build, "sim_reference"), os.path.join(build, "sim_tangram")
+    if not (os.path.exists(ref_bin) and os.path.exists(tg_bin)):
+        return {"unavailable": "integration/_build binaries absent (built by build() where the reference exists)"}
+    args = ["reuse_odkv", "8", "48", "4", "2", "2000", "42", "0", "0", "L3"]
+    a = subprocess.run([ref_bin] + args, capture_output=True, timeout=600)
+    env = dict(os.environ, TANGRAM_DEVICE="auto", TANGRAM_SYNTH_SOURCES="1")  # gpu0 -> device 0
+    t0 = time.perf_counter()
+    b = subprocess.run([tg_bin] + args, capture_output=True, timeout=600, env=env)
+    wall = time.perf_counter() - t0
+    try:
+        pools = json.loads(b.stderr.decode().strip().splitlines()[-1])["pools"]
+        g0 = [p for p in pools if p["gpu_id"] == "gpu0"][0]
+    except Exception as e:  # pragma: no cover
+        return {"unavailable": f"replay failed: {e}"}
+    moved = g0["relocated_bytes"] + g0["device_src_bytes"] + g0["pcie_bytes"]
+    ms = g0["data_plane_ms"]
+    return {"workload": "C5 Zipf trace (2,000 requests, seed 42, L3) on 8 x 48 GiB pools, ReuseOdkv, batch 4, "
+                        "keep-alive 2 s; reference Simulator over the drop-in bindings; gpu0 on this GPU with real "
+                        "bytes (HBM-resident sources), gpu1..7 control-plane only",
+            "run_metrics_equal_reference": a.returncode == 0 and b.returncode == 0 and a.stdout == b.stdout,
+            "gpu0_loads": g0["loads"], "gpu0_relocated_bytes": g0["relocated_bytes"],
+            "gpu0_placed_bytes": g0["device_src_bytes"] + g0["pcie_bytes"],
+            "gpu0_fingerprint_bytes": g0["fingerprint_bytes"], "gpu0_data_plane_ms": ms,
+            "gpu0_moved_GBps": moved / ms / 1e6 if ms > 0 else None,
+            "gpu0_hbm_rw_GBps": (2 * moved + g0["fingerprint_bytes"] - g0["device_src_bytes"]
+                                 - g0["relocated_bytes"]) / ms / 1e6 if ms > 0 else None,
+            "replay_wall_s": wall,
+            "note": "data_plane_ms = sum over gpu0's loads of the CUDA-event span of each synchronous load; "
+                    "hbm_rw counts moves r+w plus fingerprint reads not already covered by a move's read"}
 
 
 def check_parity(tg, pool, target, host, cache, dev):

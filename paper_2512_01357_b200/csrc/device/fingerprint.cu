@@ -783,18 +783,26 @@ __device__ __forceinline__ CopyFpTask as_copy_task(const FpTask& t) {
     return CopyFpTask{t.base, nullptr, t.n, t.tile0, -1, -1};
 }
 
+// Task of tile t: the last task with tile0 <= t.  A warp takes its tiles in
+// increasing order, so the search starts at the task of its previous tile
+// (`hint`, tile0 <= t) and scans 32 tasks per round with one load per lane —
+// one dependent L2 round trip per tile instead of log2(n_tasks).
+template <class Task>
+__device__ __forceinline__ u32 find_task(const Task* __restrict__ tasks, u32 n_tasks, u64 t, u32 hint, u32 lane) {
+    for (u32 base = hint;; base += 31) {
+        const u32 i = base + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, i < n_tasks && tasks[i].tile0 <= t);
+        if (m != 0xffffffffu || base + 32 >= n_tasks) return base + 31 - __clz(m);  // lane 0 always set
+    }
+}
+
 template <class Task>
 __device__ __forceinline__ CopyTileRef copy_tile_ref(const Task* __restrict__ tasks, u32 n_tasks, u64 t,
-                                                     u64 total_tiles) {
+                                                     u64 total_tiles, u32 hint, u32 lane) {
     CopyTileRef r{};
     r.t.task = -1;
     if (t >= total_tiles) return r;
-    u32 lo = 0, hi = n_tasks - 1;
-    while (lo < hi) {
-        const u32 mid = (lo + hi + 1) >> 1;
-        if (tasks[mid].tile0 <= t) lo = mid;
-        else hi = mid - 1;
-    }
+    const u32 lo = find_task(tasks, n_tasks, t, hint, lane);
     const CopyFpTask tk = as_copy_task(tasks[lo]);
     r.t.task = static_cast<int>(lo);
     r.t.base = tk.src;
@@ -917,6 +925,12 @@ __device__ __forceinline__ void copy_issue(uint4* stage_buf, const CopyTileRef& 
     cp_async_commit();
 }
 
+// Release-ordered add: the warp's reads and stores before it (ordered by the
+// preceding __syncwarp) are visible to whoever acquires the counter.
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+
 __device__ __forceinline__ u64 ld_acquire(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
@@ -949,9 +963,10 @@ __global__ void __launch_bounds__(kCopyWarps * 32, 2)
     const u32 lane = threadIdx.x & 31;
     const u32 wid = threadIdx.x >> 5;
     uint4* wbuf = smem + wid * kCopyWarpWords;
-    CopyTileRef cur = copy_tile_ref(tasks, n_tasks, next_tile(sync, lane), total_tiles);
+    CopyTileRef cur = copy_tile_ref(tasks, n_tasks, next_tile(sync, lane), total_tiles, 0u, lane);
     if (cur.t.task < 0) return;
-    CopyTileRef nxt = copy_tile_ref(tasks, n_tasks, next_tile(sync, lane), total_tiles);
+    CopyTileRef nxt = copy_tile_ref(tasks, n_tasks, next_tile(sync, lane), total_tiles, static_cast<u32>(cur.t.task),
+                                    lane);
     int cur_task = -1;
     u64 acc_h = 0, acc_l = 0;
     u32 buf = 0;
@@ -989,9 +1004,9 @@ __global__ void __launch_bounds__(kCopyWarps * 32, 2)
             const uint4* sb = wbuf + buf * kV3StageWords;
             const uint4* sp = wbuf + prev * kV3StageWords;
             if (writes && cur.t.nfull) write_lines_dispatch(sb, sp, cur, s, true, s > 0, lane);
-            if (lane < cur.t.nfull) v4_hash(sb, cur.t, lane, h1, h2);
             if (s == kStagesPerLeaf - 1 && writes && cur.t.nfull && cur.k)
                 write_lines_dispatch(nullptr, sb, cur, kStagesPerLeaf, false, true, lane);
+            if (lane < cur.t.nfull) v4_hash(sb, cur.t, lane, h1, h2);
             __syncwarp();
             const int ahead = s + kAhead;
             if (ahead < kStagesPerLeaf) copy_issue(wbuf + prev * kV3StageWords, cur, ahead, lane);
@@ -1018,13 +1033,11 @@ __global__ void __launch_bounds__(kCopyWarps * 32, 2)
         }
         if (cur.wave >= 0) {  // this tile's source bytes are all read
             __syncwarp();
-            if (lane == 0) {
-                __threadfence();
-                atomicAdd(sync + 1 + cur.wave, 1ull);
-            }
+            if (lane == 0) red_release_add(sync + 1 + cur.wave, 1ull);
         }
+        const u32 hint = static_cast<u32>(nxt.t.task >= 0 ? nxt.t.task : cur.t.task);
         cur = nxt;
-        nxt = copy_tile_ref(tasks, n_tasks, next_tile(sync, lane), total_tiles);
+        nxt = copy_tile_ref(tasks, n_tasks, next_tile(sync, lane), total_tiles, hint, lane);
     }
     cp_async_wait<0>();
     if (cur_task >= 0) {

@@ -295,14 +295,26 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     }
 
     // Relocation waves: wave(k) = 1 + max wave(j), j < k, dst_k ∩ src_j ≠ ∅.
+    // The planner moves each tensor at most once and only into free space
+    // (packing.hpp:412-456), so write-after-read is the only hazard it
+    // produces.  Read-after-write / write-after-write edges (a tensor moved
+    // twice) also raise the wave, and route the load through the separately
+    // launched waves: the load kernel prefetches a gated tile's sources
+    // before its gate opens, which is only safe for WAR.
     // (copy: the decision is moved into the report below)
     const std::vector<Move> rel = d.plan.relocations;
     rep->reloc_wave.assign(rel.size(), 0);
     u32 waves = 0;
+    bool raw_edges = false;
     for (std::size_t k = 0; k < rel.size(); ++k) {
         u32 w = 0;
-        for (std::size_t j = 0; j < k; ++j)
-            if (overlaps(rel[k].to, rel[k].size, rel[j].from, rel[j].size)) w = std::max(w, rep->reloc_wave[j] + 1);
+        for (std::size_t j = 0; j < k; ++j) {
+            const bool war = overlaps(rel[k].to, rel[k].size, rel[j].from, rel[j].size);
+            const bool raw = overlaps(rel[k].from, rel[k].size, rel[j].to, rel[j].size) ||
+                             overlaps(rel[k].to, rel[k].size, rel[j].to, rel[j].size);
+            raw_edges = raw_edges || raw;
+            if (war || raw) w = std::max(w, rep->reloc_wave[j] + 1);
+        }
         rep->reloc_wave[k] = w;
         waves = std::max(waves, w + 1);
     }
@@ -332,7 +344,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     // ---- event layout -----------------------------------------------------------
     // 0 t0 | 1 reloc start | 2 reloc end | 3 end | 4 h2d start | 5 h2d end | 6 peer start | 7 peer end
     // 8 verify joined | 9.. wave ends (waves) | then per placement "bytes landed" | then fp start/end pairs
-    const bool fused = (flags & kLoadFused) != 0;
+    const bool fused = (flags & kLoadFused) != 0 && !raw_edges;
     const std::size_t ev_wave = 9, ev_land = ev_wave + waves, ev_fp = ev_land + np;
     const bool fp_new = flags & kLoadFingerprintNew, fp_reuse = (flags & kLoadVerifyReuse) && !hit_keys.empty();
     // Reused tensors no relocation touches are verified right away on the
