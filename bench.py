@@ -403,10 +403,12 @@ def run_ours(args):
         for b in host.values():
             b.free()
         lib.tg_host_clear()
-        extras["c1"] = run_c1(tg, local)
-        extras["c3"] = run_c3(tg, local)
-        if local == 0:
-            extras["c5"] = run_c5(local)
+        for key, fn in (("c1", lambda: run_c1(tg, local, h2d_peak, hbm_peak)), ("c3", lambda: run_c3(tg, local)),
+                        ("c5", lambda: run_c5(local))):
+            try:  # a secondary config never takes the headline line down
+                extras[key] = fn()
+            except Exception as e:  # pragma: no cover
+                extras[key] = {"error": f"{type(e).__name__}: {e}"}
     if not args.no_cpu_baseline and world == 1 and not args.profile:
         cpu_base = cpu_baseline(args)
 
@@ -583,7 +585,7 @@ def _event_ms(stream_ptr, dev, fn):
     return a.elapsed_time(b), r
 
 
-def run_c1(tg, dev, reps=3):
+def run_c1(tg, dev, h2d_peak, hbm_peak, reps=3):
     """C1: OPT-1.3B cold load (PCIe) and 100 % reuse reload (HBM verify)."""
     from paper_2512_01357_b200.checkpoint import HostCheckpoint
     m = {x.model_id: x for x in tg.default_catalog()}["opt1.3B"]
@@ -612,7 +614,12 @@ def run_c1(tg, dev, reps=3):
             "cold_h2d_bytes": oc.pcie_bytes, "cold_h2d_ms": oc.timings["h2d_ms"],
             "warm_ms": mw, "warm_effective_GBps": m.total_size / mw / 1e6,
             "warm_fingerprint_bytes": ow.fingerprint_bytes, "warm_verify_mismatches": ow.verify_mismatches,
-            "plan_us_cold": oc.timings["plan_us"], "plan_us_warm": ow.timings["plan_us"]}
+            "plan_us_cold": oc.timings["plan_us"], "plan_us_warm": ow.timings["plan_us"],
+            "cold_frac_of_h2d_peak": m.total_size / mc / 1e6 / h2d_peak,
+            "warm_frac_of_hbm_peak": ow.fingerprint_bytes / mw / 1e6 / hbm_peak,
+            "roofline_note": "cold: whole-load latency vs the measured pinned-H2D peak; warm: fingerprint bytes "
+                             "read once / whole-load latency (plan, launch, digest readback included) vs the "
+                             "measured HBM copy peak"}
 
 
 def run_c3(tg, dev):
@@ -666,6 +673,33 @@ def run_c3(tg, dev):
         row = {"requests": len(reqs), "blocks": blocks, "blocks_match_reference": blocks == sum(
                    len(g) for g in case["burst"]),
                "burst_us": best_b * 1e6, "decode_step_us": best_d * 1e6, "blocks_per_us": blocks / (best_b * 1e6)}
+        # K4D: decode steps decided on the device (no host round trip per
+        # step): S steps in which every request crosses a block boundary
+        kv.batch_allocate(pool, stats, reqs, want_pbns=False).value()
+        steps = 8
+        slots = torch.tensor([kv.request_slot(r) for r, _ in reqs], dtype=torch.int64, device=f"cuda:{dev}")
+        same = torch.tensor([p for _, p in reqs], dtype=torch.int64, device=f"cuda:{dev}")
+        kv.device_arm(pool, 8192 // 16 + steps + 2, len(reqs), 1).value()  # warm-up: a no-grant batch
+        kv.batch_allocate_device(slots.data_ptr(), same.data_ptr(), len(reqs))
+        kv.device_sync(pool, stats).value()
+        kv.device_arm(pool, 8192 // 16 + steps + 2, len(reqs), steps).value()
+        toks = [torch.tensor([(p + 15) // 16 * 16 + 1 + 16 * k for _, p in reqs], dtype=torch.int64,
+                             device=f"cuda:{dev}") for k in range(steps)]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cs = torch.cuda.current_stream()
+        e0.record(cs)
+        for k in range(steps):
+            kv.batch_allocate_device(slots.data_ptr(), toks[k].data_ptr(), len(reqs), stream=cs.cuda_stream)
+        e1.record(cs)
+        torch.cuda.synchronize()
+        applied, replayed = kv.device_sync(pool, stats).value()
+        want_blocks = sum(((p + 15) // 16 * 16 + 1 + 16 * (steps - 1) + 15) // 16 for _, p in reqs)
+        row["device_decode_step_us"] = e0.elapsed_time(e1) * 1e3 / steps
+        row["device_decode_steps"] = steps
+        row["device_steps_applied_on_device"] = applied
+        row["device_blocks_match"] = sum(kv._blocks(r) for r, _ in reqs) == want_blocks
+        kv.instance_teardown(pool)
         if have_ref:
             r = ref.ReuseStore(120 * GIB)
             rs = ref.ModelStatsTable()
@@ -679,7 +713,10 @@ def run_c3(tg, dev):
         out[n] = row
     pool.close()
     return {"workload": "C3 Llama-2-13B (26 GB) in a 120 GiB pool; KV blocks of 16 tokens x 819,200 B/token; "
-                        "host+device time per batch incl. kernel completion, best of 3", "bursts": out}
+                        "host+device time per batch incl. kernel completion, best of 3; device_decode_step_us: "
+                        "K4D batches decided on the GPU (tg_kv_batch_allocate_device), CUDA-event time per step "
+                        "over 8 back-to-back steps in which every request crosses a block boundary",
+            "bursts": out}
 
 
 def run_c5(dev):

@@ -35,6 +35,8 @@ extern "C" {
 #define TG_ERR_BAD_ARG 104        /* null handle / malformed argument */
 #define TG_ERR_VERIFY 105         /* reused bytes fail their fingerprint and cannot be repaired */
 #define TG_ERR_INTERNAL 106
+#define TG_ERR_KV_ARMED 107       /* pool layout / host KV call while an engine is armed (tg_kv_device_sync first) */
+#define TG_ERR_KV_LOG 108         /* the device batch log overflowed between arm and sync: batches were dropped */
 
 #define TG_POOL_NO_DEVICE (-1)    /* device argument: control plane only, moves no bytes */
 
@@ -343,6 +345,37 @@ int tg_kv_table(const tg_kv* kv, uint64_t request_id, uint64_t* pbns, uint64_t c
 int tg_kv_address_table(const tg_kv* kv, uint64_t* triples /*pbn,off,size*/, uint64_t cap, uint64_t* n); /* :63 */
 int tg_kv_stats_get(const tg_kv* kv, tg_kv_stats* out);
 int tg_kv_device_tables(const tg_kv* kv, void** tables, uint64_t* stride, void** addr); /* for paged attention */
+
+/* ---- device-decided KV batches (K4D; new, no reference counterpart) ------------
+ * The allocator decision of batch_allocate (:107-161) taken by a kernel, for
+ * requests the engine already knows, with no host round trip per batch:
+ *   tg_kv_request_slot     table row of a request (ensure_capacity(rid, 0)
+ *                          makes a new request known, as in the reference);
+ *   tg_kv_device_arm       upload the allocator state and the pool's free runs;
+ *                          from here until sync the pool layout is frozen
+ *                          (layout-changing pool calls and host KV calls on any
+ *                          engine of that pool return TG_ERR_KV_ARMED);
+ *   tg_kv_batch_allocate_device
+ *                          enqueue one batch on `stream` (null: the engine's
+ *                          stream): request table slots and token counts in
+ *                          DEVICE memory, n <= max_requests; capturable in a
+ *                          CUDA graph (every pointer is read at run time);
+ *                          batches of one session must be stream-ordered;
+ *   tg_kv_device_sync      wait, fold the device decisions into the host state,
+ *                          replay on the reference path every batch the device
+ *                          left to it (contended pool, unknown slot, shrinking
+ *                          token count, duplicate request, ...), and disarm.
+ * After sync, tables, address table, counters and pool regions equal running
+ * the same batches through tg_kv_batch_allocate.  Errors of replayed batches
+ * are reported by sync (the first one); TG_ERR_KV_LOG if more than
+ * max_batches batches were enqueued. */
+int tg_kv_request_slot(const tg_kv* kv, uint64_t request_id, uint32_t* slot);
+int tg_kv_device_arm(tg_kv* kv, tg_pool* p, uint64_t max_blocks_per_request, uint32_t max_requests,
+                     uint32_t max_batches);
+int tg_kv_batch_allocate_device(tg_kv* kv, const uint64_t* d_slots, const uint64_t* d_tokens, uint32_t n,
+                                void* cuda_stream);
+int tg_kv_device_sync(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t* applied_batches,
+                      uint64_t* replayed_batches);
 
 /* ---- planner (plan_allocation, packing.hpp:311-483) ----------------------------
  * Pure two-stage plan over an address-ordered region tiling.  new_tensors are

@@ -202,6 +202,10 @@ _SIGS = {
     "tg_kv_address_table": (C.c_int, [vp, P(u64), u64, P(u64)]),
     "tg_kv_stats_get": (C.c_int, [vp, P(KvStatsC)]),
     "tg_kv_device_tables": (C.c_int, [vp, P(vp), P(u64), P(vp)]),
+    "tg_kv_request_slot": (C.c_int, [vp, u64, P(C.c_uint32)]),
+    "tg_kv_device_arm": (C.c_int, [vp, vp, u64, C.c_uint32, C.c_uint32]),
+    "tg_kv_batch_allocate_device": (C.c_int, [vp, vp, vp, C.c_uint32, vp]),
+    "tg_kv_device_sync": (C.c_int, [vp, vp, vp, P(u64), P(u64)]),
     "tg_plan_allocation": (C.c_int, [P(RegionC), u64, P(TensorSpecC), u32, P(EvictionC), u32, P(TensorIdC), u32,
                                      i32, i32, i32, P(vp)]),
     "tg_plan_evictions": (u32, [vp, P(EvictionC), u32]),

@@ -93,6 +93,63 @@ struct KvBatchArgs {
     std::uint64_t* out;   // optional: granted pbns in order
 };
 void kv_batch_launch(const KvBatchArgs& a, cudaStream_t s);
+
+// ---- K4D: device-decided KV batches (the allocator decision on the GPU) -----
+// Control block of an armed engine, resident in HBM.  The host writes the
+// first part at arm time (pointers and limits, a mirror of the pool's free
+// runs of at least one block in ascending (size, offset) order, the per-slot
+// block and token counts); kv_device_batch_kernel advances the second part.
+// Every pointer is read at run time, so a captured CUDA graph of batches stays
+// valid across arms.
+constexpr std::uint32_t kKvDevMaxRequests = 8192;  // per batch
+constexpr std::uint32_t kKvDevMaxPieces = 64;      // carved pieces per batch
+struct KvDevCtl {
+    std::uint64_t* tables;
+    std::uint64_t stride;
+    std::uint64_t* free_list;
+    std::uint64_t* addr;
+    const std::uint64_t* run_off;
+    const std::uint64_t* run_blocks;
+    std::uint64_t n_runs;
+    std::uint64_t* slot_blocks;
+    std::uint64_t* slot_tokens;
+    std::uint64_t* slot_mark;  // batch that last touched the slot (+1): duplicate detection
+    std::uint64_t n_slots;
+    std::uint8_t* log;
+    std::uint64_t log_entry_bytes;
+    std::uint64_t max_batches;
+    std::uint64_t max_requests;
+    std::uint64_t block_bytes;
+    std::uint64_t block_tokens;
+    // advanced by the kernel
+    std::uint64_t free_top;
+    std::uint64_t next_pbn;
+    std::uint64_t run_cursor;
+    std::uint64_t run_used;
+    std::uint64_t blocks_left;
+    std::uint64_t batches;
+    std::uint64_t stalled;  // 0 ok, 1 a batch fell back to the host (later ones do nothing), 2 log overflow
+};
+// One log entry per batch: header, the batch's (slot, tokens) pairs
+// (max_requests of them), then up to kKvDevMaxPieces carved pieces.
+struct KvLogHeader {
+    std::uint64_t n;
+    std::uint64_t status;  // 0 applied on the device, 1 left to the host (replayed at sync)
+    std::uint64_t total;
+    std::uint64_t pops;
+    std::uint64_t n_pieces;
+    std::uint64_t pad[3];
+};
+struct KvPiece {
+    std::uint64_t off;
+    std::uint64_t count;
+    std::uint64_t first_pbn;
+};
+inline std::uint64_t kv_log_entry_bytes(std::uint64_t max_requests) {
+    return sizeof(KvLogHeader) + 16 * max_requests + sizeof(KvPiece) * kKvDevMaxPieces;
+}
+void kv_device_batch_launch(KvDevCtl* d_ctl, const std::uint64_t* d_slots, const std::uint64_t* d_tokens,
+                            std::uint32_t n, cudaStream_t s);
 void kv_release_launch(const std::uint64_t* table_row, std::uint64_t blocks, std::uint64_t* free_list_dst,
                        cudaStream_t s);
 

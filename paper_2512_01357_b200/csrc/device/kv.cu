@@ -8,8 +8,14 @@
 // 203-229) takes free_list[top-1-k] while k < pops, otherwise the next PBN
 // of its carve run; it writes the request's LBN→PBN table entry and, for
 // carved blocks, the PBN→offset address-table entry.
+//
+// K4D (kv_device_batch_kernel) takes the decision itself as well, for
+// batches enqueued between KvAllocator::arm and ::sync: no host round trip
+// per batch, so a decode loop can allocate its blocks inside a CUDA graph.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstring>
 #include <memory>
 #include <vector>
 
@@ -51,6 +57,193 @@ __global__ void kv_batch_kernel(const KvBatchArgs a) {
     }
     a.tables[static_cast<u64>(g.slot) * a.stride + lbn] = pbn;
     if (a.out) a.out[k] = pbn;
+}
+
+// K4D: one batch decided and applied on the device (one CTA).  The decision
+// is the reference's certainly-fits path (kv_engine.hpp:127-141): for each
+// request in order, blocks ceil(tokens / B) - have, the LIFO free list first
+// (kv_engine.hpp:205-210), then best-fit carving — which for equal blocks is
+// a walk over the free runs in ascending (size, offset) order, each run
+// carved from its start until it holds less than one block (SURVEY §7 hard
+// part 5; the control block keeps the cursor of that walk).  A batch that
+// would need the contended path (not certainly fitting: urgent reclaim), or
+// that the device cannot decide alone (unknown slot, shrinking token count,
+// a request twice, a table row too short, too many pieces) is left untouched
+// and flagged; the host replays it, and every later batch of the session, on
+// the reference path at sync time.
+constexpr int kKvThreads = 1024;
+
+__device__ __forceinline__ u32 block_excl_scan(u32 v, u32* s_warp, u32* total) {
+    const u32 lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    u32 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= static_cast<u32>(o)) x += y;
+    }
+    if (lane == 31) s_warp[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        u32 t = lane < kKvThreads / 32 ? s_warp[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= static_cast<u32>(o)) t += y;
+        }
+        s_warp[lane] = t;  // inclusive over warps
+    }
+    __syncthreads();
+    const u32 before = (w ? s_warp[w - 1] : 0) + x - v;
+    *total = s_warp[kKvThreads / 32 - 1];
+    __syncthreads();
+    return before;
+}
+
+__global__ void __launch_bounds__(kKvThreads) kv_device_batch_kernel(KvDevCtl* __restrict__ c,
+                                                                     const u64* __restrict__ slots,
+                                                                     const u64* __restrict__ tokens, u32 n) {
+    __shared__ u32 s_pref[kKvDevMaxRequests + 1];
+    __shared__ KvPiece s_piece[kKvDevMaxPieces];
+    __shared__ u64 s_pstart[kKvDevMaxPieces + 1];
+    __shared__ u32 s_warp[32];
+    __shared__ u64 s_b, s_pops, s_npieces;
+    __shared__ int s_fallback;
+    const u32 tid = threadIdx.x;
+    if (tid == 0) s_b = c->batches++;
+    __syncthreads();
+    const u64 b = s_b;
+    if (b >= c->max_batches) {  // log full: the batch is lost, reported at sync
+        if (tid == 0) c->stalled = 2;
+        return;
+    }
+    std::uint8_t* entry = c->log + b * c->log_entry_bytes;
+    auto* hdr = reinterpret_cast<KvLogHeader*>(entry);
+    u64* req = reinterpret_cast<u64*>(entry + sizeof(KvLogHeader));
+    auto* pcs = reinterpret_cast<KvPiece*>(entry + sizeof(KvLogHeader) + 16 * c->max_requests);
+    for (u32 i = tid; i < n && i < c->max_requests; i += kKvThreads) {
+        req[2 * i] = slots[i];
+        req[2 * i + 1] = tokens[i];
+    }
+    const bool stalled = c->stalled != 0;
+    if (stalled) {
+        if (tid == 0) {
+            hdr->n = n;
+            hdr->status = 1;
+            hdr->total = hdr->pops = hdr->n_pieces = 0;
+        }
+        return;
+    }
+    // need per request, and whether the device can decide the batch alone
+    const u64 bs = c->block_tokens;
+    int bad = n > c->max_requests;
+    const u32 per = (n + kKvThreads - 1) / kKvThreads;  // contiguous chunk per thread
+    u32 local = 0;
+    for (u32 q = 0; q < per; ++q) {
+        const u32 i = tid * per + q;
+        if (i >= n) break;
+        const u64 slot = slots[i], tok = tokens[i];
+        u32 need = 0;
+        if (slot >= c->n_slots) {
+            bad = 1;
+        } else {
+            if (atomicExch(reinterpret_cast<unsigned long long*>(c->slot_mark + slot), b + 1) == b + 1) bad = 1;
+            if (tok < c->slot_tokens[slot]) bad = 1;
+            const u64 want = (tok + bs - 1) / bs, have = c->slot_blocks[slot];
+            if (want > c->stride) bad = 1;
+            else if (want > have) need = static_cast<u32>(want - have);
+        }
+        s_pref[i] = need;
+        local += need;
+    }
+    bad = __syncthreads_or(bad);
+    u32 total = 0;
+    u32 run = block_excl_scan(local, s_warp, &total);
+    for (u32 q = 0; q < per; ++q) {
+        const u32 i = tid * per + q;
+        if (i >= n) break;
+        const u32 v = s_pref[i];
+        s_pref[i] = run;
+        run += v;
+    }
+    if (tid == 0) {
+        s_pref[n] = total;
+        int fb = bad || total > c->free_top + c->blocks_left;
+        u64 pops = total < c->free_top ? total : c->free_top;
+        u64 rem = total - pops, cur = c->run_cursor, used = c->run_used, np = 0, carved = 0;
+        while (!fb && rem > 0) {
+            if (np == kKvDevMaxPieces || cur >= c->n_runs) {
+                fb = 1;
+                break;
+            }
+            const u64 k = min(c->run_blocks[cur] - used, rem);
+            s_piece[np] = KvPiece{c->run_off[cur] + used * c->block_bytes, k, c->next_pbn + carved};
+            s_pstart[np] = carved;
+            ++np;
+            carved += k;
+            rem -= k;
+            used += k;
+            if (used == c->run_blocks[cur]) {
+                ++cur;
+                used = 0;
+            }
+        }
+        s_pstart[np] = carved;
+        s_fallback = fb;
+        s_pops = pops;
+        s_npieces = np;
+        if (fb) {
+            hdr->n = n;
+            hdr->status = 1;
+            hdr->total = hdr->pops = hdr->n_pieces = 0;
+            c->stalled = 1;
+        } else {
+            hdr->n = n;
+            hdr->status = 0;
+            hdr->total = total;
+            hdr->pops = pops;
+            hdr->n_pieces = np;
+            for (u64 p = 0; p < np; ++p) pcs[p] = s_piece[p];
+            c->run_cursor = cur;
+            c->run_used = used;
+        }
+    }
+    __syncthreads();
+    if (s_fallback) return;
+    const u64 pops = s_pops, np = s_npieces, top = c->free_top;
+    // expand: block k of the batch -> (request, LBN) and its PBN
+    for (u32 k = tid; k < total; k += kKvThreads) {
+        u32 lo = 0, hi = n - 1;
+        while (lo < hi) {
+            const u32 mid = (lo + hi + 1) >> 1;
+            if (s_pref[mid] <= k) lo = mid;
+            else hi = mid - 1;
+        }
+        const u64 slot = slots[lo];
+        const u64 lbn = c->slot_blocks[slot] + (k - s_pref[lo]);
+        u64 pbn;
+        if (k < pops) {
+            pbn = c->free_list[top - 1 - k];
+        } else {
+            const u64 j = k - pops;
+            u32 p = 0;
+            while (p + 1 < np && s_pstart[p + 1] <= j) ++p;
+            pbn = s_piece[p].first_pbn + (j - s_pstart[p]);
+            c->addr[pbn] = s_piece[p].off + (j - s_pstart[p]) * c->block_bytes;
+        }
+        c->tables[slot * c->stride + lbn] = pbn;
+    }
+    __syncthreads();
+    for (u32 i = tid; i < n; i += kKvThreads) {
+        const u64 slot = slots[i];
+        c->slot_blocks[slot] += s_pref[i + 1] - s_pref[i];
+        c->slot_tokens[slot] = tokens[i];
+    }
+    if (tid == 0) {
+        const u64 carved = total - pops;
+        c->free_top = top - pops;
+        c->next_pbn += carved;
+        c->blocks_left -= carved;
+    }
 }
 
 __global__ void kv_copy_kernel(const u64* __restrict__ src, u64 n, u64* __restrict__ dst) {
@@ -176,6 +369,113 @@ public:
         return c;
     }
 
+    int arm(const KvArmSpec& a, u64 block_bytes) override {
+        DeviceScope ds(dev_);
+        u64 carvable = 0;
+        for (u64 b : a.run_blocks) carvable += b;
+        const u64 slots = a.slot_blocks.size();
+        grow(static_cast<u32>(slots), a.max_blocks_per_request, a.free_top, a.next_pbn + carvable + 1);
+        const u64 nr = a.run_off.size();
+        const u64 entry = kv_log_entry_bytes(a.max_requests);
+        // buffers are kept across arms when large enough (captured graphs
+        // read every pointer from the control block, so a reallocation only
+        // costs a re-upload)
+        reserve_buf(&d_runs_, &runs_cap_, 2 * std::max<u64>(nr, 1));
+        reserve_buf(&d_slots_, &slots_cap_, 3 * std::max<u64>(slots, 1));
+        reserve_bytes(&d_log_, &log_cap_, entry * a.max_batches);
+        if (!d_ctl_) TG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_ctl_), sizeof(KvDevCtl), s_));
+        std::vector<u64> h(2 * nr + 2 * slots);
+        std::copy(a.run_off.begin(), a.run_off.end(), h.begin());
+        std::copy(a.run_blocks.begin(), a.run_blocks.end(), h.begin() + nr);
+        std::copy(a.slot_blocks.begin(), a.slot_blocks.end(), h.begin() + 2 * nr);
+        std::copy(a.slot_tokens.begin(), a.slot_tokens.end(), h.begin() + 2 * nr + slots);
+        if (nr) TG_CUDA(cudaMemcpyAsync(d_runs_, h.data(), 2 * nr * sizeof(u64), cudaMemcpyHostToDevice, s_));
+        if (slots) {
+            TG_CUDA(cudaMemcpyAsync(d_slots_, h.data() + 2 * nr, 2 * slots * sizeof(u64), cudaMemcpyHostToDevice, s_));
+            TG_CUDA(cudaMemsetAsync(d_slots_ + 2 * slots, 0, slots * sizeof(u64), s_));
+        }
+        KvDevCtl c{};
+        c.tables = tables_;
+        c.stride = stride_;
+        c.free_list = free_;
+        c.addr = addr_;
+        c.run_off = d_runs_;
+        c.run_blocks = d_runs_ + nr;
+        c.n_runs = nr;
+        c.slot_blocks = d_slots_;
+        c.slot_tokens = d_slots_ + slots;
+        c.slot_mark = d_slots_ + 2 * slots;
+        c.n_slots = slots;
+        c.log = d_log_;
+        c.log_entry_bytes = entry;
+        c.max_batches = a.max_batches;
+        c.max_requests = a.max_requests;
+        c.block_bytes = block_bytes;
+        c.block_tokens = a.block_tokens;
+        c.free_top = a.free_top;
+        c.next_pbn = a.next_pbn;
+        c.blocks_left = carvable;
+        h_ctl_ = c;
+        TG_CUDA(cudaMemcpyAsync(d_ctl_, &h_ctl_, sizeof(KvDevCtl), cudaMemcpyHostToDevice, s_));
+        TG_CUDA(cudaStreamSynchronize(s_));
+        max_requests_ = a.max_requests;
+        max_batches_ = a.max_batches;
+        log_entry_ = entry;
+        captured_ = false;
+        pending_ = false;
+        return 0;
+    }
+
+    int enqueue(const u64* d_slots, const u64* d_tokens, u32 n, void* stream) override {
+        DeviceScope ds(dev_);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s_;
+        kv_device_batch_launch(d_ctl_, d_slots, d_tokens, n, st);
+        TG_CUDA(cudaGetLastError());
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        TG_CUDA(cudaStreamIsCapturing(st, &cs));
+        if (cs != cudaStreamCaptureStatusNone) {
+            captured_ = true;  // replays run outside our view: sync waits for the device
+        } else {
+            if (!done_) TG_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
+            TG_CUDA(cudaEventRecord(done_, st));
+            pending_ = true;
+        }
+        return 0;
+    }
+
+    int read_log(KvLog* out) override {
+        DeviceScope ds(dev_);
+        if (captured_) TG_CUDA(cudaDeviceSynchronize());
+        else if (pending_) TG_CUDA(cudaEventSynchronize(done_));
+        KvDevCtl c{};
+        TG_CUDA(cudaMemcpyAsync(&c, d_ctl_, sizeof(KvDevCtl), cudaMemcpyDeviceToHost, s_));
+        TG_CUDA(cudaStreamSynchronize(s_));
+        const u64 nb = std::min(c.batches, max_batches_);
+        std::vector<std::uint8_t> log(nb * log_entry_);
+        if (nb) {
+            TG_CUDA(cudaMemcpyAsync(log.data(), d_log_, log.size(), cudaMemcpyDeviceToHost, s_));
+            TG_CUDA(cudaStreamSynchronize(s_));
+        }
+        out->stalled = c.stalled;
+        out->batches.clear();
+        for (u64 b = 0; b < nb; ++b) {
+            const std::uint8_t* e = log.data() + b * log_entry_;
+            KvLogHeader hd;
+            std::memcpy(&hd, e, sizeof hd);
+            KvLogBatch lb;
+            lb.status = hd.status;
+            lb.total = hd.total;
+            lb.pops = hd.pops;
+            const u64* rq = reinterpret_cast<const u64*>(e + sizeof(KvLogHeader));
+            for (u64 i = 0; i < hd.n; ++i) lb.reqs.push_back({rq[2 * i], rq[2 * i + 1]});
+            const auto* pc = reinterpret_cast<const KvPiece*>(e + sizeof(KvLogHeader) + 16 * max_requests_);
+            for (u64 p = 0; p < hd.n_pieces; ++p) lb.pieces.push_back(KvRun{pc[p].off, pc[p].count, pc[p].first_pbn});
+            out->batches.push_back(std::move(lb));
+        }
+        captured_ = pending_ = false;
+        return 0;
+    }
+
     void reset() override {}
     void* table_ptr() const override { return tables_; }
     u64 table_stride() const override { return stride_; }
@@ -233,6 +533,19 @@ private:
         stage_cap_ = n;
     }
 
+    void reserve_buf(u64** p, u64* cap, u64 n) {
+        if (n <= *cap) return;
+        if (*p) TG_CUDA(cudaFreeAsync(*p, s_));
+        *cap = grow_to(*cap, n);
+        TG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), *cap * sizeof(u64), s_));
+    }
+    void reserve_bytes(std::uint8_t** p, u64* cap, u64 n) {
+        if (n <= *cap) return;
+        if (*p) TG_CUDA(cudaFreeAsync(*p, s_));
+        *cap = n;
+        TG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), n, s_));
+    }
+
     void ensure_out(u64 n) {
         if (n <= out_cap_) return;
         if (d_out_) TG_CUDA(cudaFreeAsync(d_out_, s_));
@@ -243,8 +556,11 @@ private:
     void release_all() {
         DeviceScope ds(dev_);
         cudaStreamSynchronize(s_);
-        for (u64* p : {tables_, free_, addr_, d_out_})
+        for (u64* p : {tables_, free_, addr_, d_out_, d_runs_, d_slots_})
             if (p) cudaFree(p);
+        if (d_log_) cudaFree(d_log_);
+        if (d_ctl_) cudaFree(d_ctl_);
+        if (done_) cudaEventDestroy(done_);
         if (d_stage_) cudaFree(d_stage_);
         if (h_stage_) cudaFreeHost(h_stage_);
         if (stage_done_) cudaEventDestroy(stage_done_);
@@ -264,6 +580,17 @@ private:
     std::uint8_t* d_stage_ = nullptr;
     std::size_t stage_cap_ = 0;
     cudaEvent_t stage_done_ = nullptr;
+    // K4D
+    KvDevCtl* d_ctl_ = nullptr;
+    KvDevCtl h_ctl_{};
+    u64* d_runs_ = nullptr;
+    u64 runs_cap_ = 0;
+    u64* d_slots_ = nullptr;
+    u64 slots_cap_ = 0;
+    std::uint8_t* d_log_ = nullptr;
+    u64 log_cap_ = 0, log_entry_ = 0, max_requests_ = 0, max_batches_ = 0;
+    cudaEvent_t done_ = nullptr;
+    bool captured_ = false, pending_ = false;
 };
 
 }  // namespace
@@ -272,6 +599,11 @@ void kv_batch_launch(const KvBatchArgs& a, cudaStream_t s) {
     if (a.total == 0) return;
     const unsigned blocks = static_cast<unsigned>((a.total + 255) / 256);
     kv_batch_kernel<<<blocks, 256, 0, s>>>(a);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void kv_device_batch_launch(KvDevCtl* d_ctl, const u64* d_slots, const u64* d_tokens, u32 n, cudaStream_t s) {
+    kv_device_batch_kernel<<<1, kKvThreads, 0, s>>>(d_ctl, d_slots, d_tokens, n);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

@@ -106,6 +106,10 @@ LoadOptions options_of(const tg_load_policy* p, std::unique_ptr<UniformCallback>
 // Bind a KV engine to the pool's device on first use (KvEngine takes the
 // store per call, kv_engine.hpp:75, so binding is lazy).
 int bind_kv(tg_kv* kv, tg_pool* p) {
+    if (p->pool->store().kv_armed() || kv->a->armed()) {
+        g_detail = "a KV engine is armed on this pool: tg_kv_device_sync first";
+        return TG_ERR_KV_ARMED;
+    }
     const int dev = p->pool->device();
     if (kv->device == -2) {
         kv->device = dev;
@@ -311,6 +315,7 @@ int tg_load_model(tg_pool* p, const tg_model_spec* ms, const tg_stats* s, double
                   tg_load_outcome* out) {
     return guard([&] {
         if (!p || !ms || !s) return TG_ERR_BAD_ARG;
+        if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         const ModelDesc m = model_of(ms);
         const u32 flags = (pol && pol->flags) ? pol->flags : static_cast<u32>(TG_LOAD_DEFAULT);
         LoadReport& r = p->last;
@@ -417,6 +422,7 @@ int tg_end_instance(tg_pool* p, const char* m) {
 }
 int tg_evict_tensor(tg_pool* p, tg_tensor_id id) {
     return guard([&] {
+        if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         const int rc = code_of(p->pool->store().evict_tensor(key_of(id)));
         p->pool->publish_index();
         return rc;
@@ -424,6 +430,7 @@ int tg_evict_tensor(tg_pool* p, tg_tensor_id id) {
 }
 int tg_evict_model(tg_pool* p, const char* m) {
     return guard([&] {
+        if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         p->pool->store().evict_model(m);
         p->pool->publish_index();
         return 0;
@@ -431,18 +438,23 @@ int tg_evict_model(tg_pool* p, const char* m) {
 }
 int tg_move_tensor(tg_pool* p, tg_tensor_id id, uint64_t to) {
     return guard([&] {
+        if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         const int rc = code_of(p->pool->move_tensor(key_of(id), to));
         p->pool->publish_index();
         return rc;
     });
 }
 int tg_alloc_kv_region(tg_pool* p, uint64_t size, uint64_t block_id, uint64_t* off) {
+    if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
     auto r = p->pool->store().alloc_kv_region(size, block_id);
     if (!r) return code_of(r.error());
     *off = r.value();
     return 0;
 }
-int tg_free_kv_region(tg_pool* p, uint64_t off) { return code_of(p->pool->store().free_kv_region(off)); }
+int tg_free_kv_region(tg_pool* p, uint64_t off) {
+    if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
+    return code_of(p->pool->store().free_kv_region(off));
+}
 
 int tg_lookup(const tg_pool* p, const tg_model_spec* ms, uint8_t* mask, uint64_t* reuse) {
     const ModelDesc m = model_of(ms);
@@ -603,12 +615,14 @@ int tg_pool_update_remote(tg_pool* p, int32_t peer_id, const tg_index_entry* idx
 
 int tg_pool_snapshot(tg_pool* p, tg_snapshot** out) {
     return guard([&] {
+        if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         *out = new tg_snapshot{p->pool->snapshot()};
         return 0;
     });
 }
 int tg_pool_restore(tg_pool* p, const tg_snapshot* s) {
     return guard([&] {
+        if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         p->pool->restore(s->s);
         p->pool->publish_index();
         return 0;
@@ -772,6 +786,7 @@ int tg_kv_create(const char* model_id, uint64_t bs, uint64_t bpt, tg_kv** out) {
 }
 void tg_kv_destroy(tg_kv* kv) { delete kv; }
 int tg_kv_clone(const tg_kv* kv, tg_kv** out) {
+    if (kv->a->armed()) return TG_ERR_KV_ARMED;
     return guard([&] {
         *out = new tg_kv{std::make_unique<KvAllocator>(*kv->a), kv->device};
         return 0;
@@ -817,6 +832,7 @@ int tg_kv_batch_allocate(tg_kv* kv, tg_pool* p, const tg_stats* s, const uint64_
 }
 
 int tg_kv_release_request(tg_kv* kv, uint64_t rid) {
+    if (kv->a->armed()) return TG_ERR_KV_ARMED;
     return guard([&] { return code_of(kv->a->release_request(rid)); });
 }
 int tg_kv_teardown(tg_kv* kv, tg_pool* p) {
@@ -835,6 +851,7 @@ int tg_kv_urgent_reclaim(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t bloc
     });
 }
 int tg_kv_table(const tg_kv* kv, uint64_t rid, uint64_t* pbns, uint64_t cap, uint64_t* n, uint64_t* token_count) {
+    if (kv->a->armed()) return TG_ERR_KV_ARMED;
     return guard([&] {
         if (!kv->a->has_request(rid)) return code_of(Err::NotFound);
         if (token_count) *token_count = kv->a->request_tokens(rid);
@@ -878,6 +895,49 @@ int tg_kv_device_tables(const tg_kv* kv, void** tables, uint64_t* stride, void**
     *stride = d->table_stride();
     *addr = d->addr_ptr();
     return 0;
+}
+
+int tg_kv_request_slot(const tg_kv* kv, uint64_t rid, uint32_t* slot) {
+    if (!slot) return TG_ERR_BAD_ARG;
+    if (!kv->a->has_request(rid)) return code_of(Err::NotFound);
+    *slot = kv->a->request_slot(rid);
+    return 0;
+}
+int tg_kv_device_arm(tg_kv* kv, tg_pool* p, uint64_t max_blocks_per_request, uint32_t max_requests,
+                     uint32_t max_batches) {
+    return guard([&] {
+        if (max_requests > kKvDevMaxRequests) {
+            g_detail = "max_requests above the per-batch limit";
+            return TG_ERR_BAD_ARG;
+        }
+        if (int rc = bind_kv(kv, p)) return rc;
+        return code_of(kv->a->arm(p->pool->store(), max_blocks_per_request, max_requests, max_batches));
+    });
+}
+int tg_kv_batch_allocate_device(tg_kv* kv, const uint64_t* d_slots, const uint64_t* d_tokens, uint32_t n,
+                                void* stream) {
+    return guard([&] {
+        if (!kv->a->armed()) {
+            g_detail = "engine not armed (tg_kv_device_arm)";
+            return TG_ERR_BAD_ARG;
+        }
+        return kv->a->enqueue_device(d_slots, d_tokens, n, stream);
+    });
+}
+int tg_kv_device_sync(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t* applied, uint64_t* replayed) {
+    return guard([&] {
+        if (!kv->a->armed()) return TG_ERR_BAD_ARG;
+        KvAllocator::SyncReport r;
+        St st = kv->a->sync(p->pool->store(), s->s_view(), &r);
+        if (applied) *applied = r.applied;
+        if (replayed) *replayed = r.replayed;
+        p->pool->publish_index();  // a replayed contended batch may have evicted tensors
+        if (r.overflow) {
+            g_detail = "device KV batch log overflowed: batches were dropped";
+            return TG_ERR_KV_LOG;
+        }
+        return code_of(st);
+    });
 }
 
 // ---- planner ------------------------------------------------------------------------------------

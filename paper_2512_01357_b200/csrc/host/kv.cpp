@@ -12,6 +12,7 @@ KvAllocator::KvAllocator(const KvAllocator& o)
       free_count_(o.free_count_),
       reqs_(o.reqs_),
       free_slots_(o.free_slots_),
+      rid_of_slot_(o.rid_of_slot_),
       slots_used_(o.slots_used_),
       runs_(o.runs_),
       ctr_(o.ctr_),
@@ -46,7 +47,9 @@ KvAllocator::Req& KvAllocator::req(u64 rid) {
         free_slots_.pop_back();
     } else {
         r.slot = slots_used_++;
+        rid_of_slot_.resize(slots_used_);
     }
+    rid_of_slot_[r.slot] = rid;
     return reqs_.emplace(rid, r).first->second;
 }
 
@@ -218,6 +221,7 @@ void KvAllocator::teardown(Store& s) {
     runs_.clear();
     reqs_.clear();
     free_slots_.clear();
+    rid_of_slot_.clear();
     slots_used_ = 0;
     free_count_ = 0;
     if (dev_) dev_->reset();
@@ -233,6 +237,94 @@ St KvAllocator::urgent_reclaim(Store& s, const StatsView& st, u64 blocks) {
     }
     ++ctr_.reclaim_events;
     return ok();
+}
+
+// ---- K4D -----------------------------------------------------------------------------
+St KvAllocator::arm(Store& s, u64 max_blocks_per_request, u32 max_requests, u32 max_batches) {
+    if (!dev_) throw DeviceError(101, "kv: device-decided batches need a device pool");
+    if (armed_ || max_requests == 0 || max_batches == 0) return Err::InvalidArgument;
+    KvArmSpec a;
+    s.map().for_each_free_by_size(block_bytes_, [&](u64 off, u64 len) {
+        a.run_off.push_back(off);
+        a.run_blocks.push_back(len / block_bytes_);
+    });
+    a.slot_blocks.assign(slots_used_, 0);
+    a.slot_tokens.assign(slots_used_, 0);
+    u64 longest = 0;
+    for (const auto& [rid, r] : reqs_) {
+        a.slot_blocks[r.slot] = r.blocks;
+        a.slot_tokens[r.slot] = r.tokens;
+        longest = std::max(longest, r.blocks);
+    }
+    a.free_top = free_count_;
+    a.next_pbn = next_pbn_;
+    a.max_blocks_per_request = std::max(max_blocks_per_request, longest);
+    a.max_requests = max_requests;
+    a.max_batches = max_batches;
+    a.block_tokens = block_tokens_;
+    if (int rc = dev_->arm(a, block_bytes_)) throw DeviceError(rc, "kv: arm failed");
+    armed_ = true;
+    arm_max_requests_ = max_requests;
+    s.set_kv_armed(+1);
+    return ok();
+}
+
+int KvAllocator::enqueue_device(const u64* d_slots, const u64* d_tokens, u32 n, void* stream) {
+    if (!armed_ || n > arm_max_requests_) return 104;  // TG_ERR_BAD_ARG
+    return dev_->enqueue(d_slots, d_tokens, n, stream);
+}
+
+St KvAllocator::sync(Store& s, const StatsView& st, SyncReport* rep) {
+    if (!armed_) return Err::InvalidArgument;
+    KvLog log;
+    if (int rc = dev_->read_log(&log)) throw DeviceError(rc, "kv: device log read failed");
+    armed_ = false;
+    s.set_kv_armed(-1);
+    rep->overflow = log.stalled == 2;
+    St first = ok();
+    for (const KvLogBatch& b : log.batches) {
+        if (b.status == 0) {
+            // the device's decisions, folded in exactly as batch_allocate's
+            // certainly-fits path books them (kv_engine.hpp:127-141)
+            u64 total = 0;
+            for (const auto& [slot, tok] : b.reqs) {
+                Req& r = reqs_.at(rid_of_slot_.at(slot));
+                const u64 want = blocks_for(tok, block_tokens_);
+                const u64 need = want > r.blocks ? want - r.blocks : 0;
+                r.blocks += need;
+                r.tokens = tok;
+                total += need;
+            }
+            if (total != b.total) throw DeviceError(106, "kv: device batch disagrees with the host replay");
+            if (total == 0) continue;
+            free_count_ -= b.pops;
+            ctr_.blocks_from_free_list += b.pops;
+            u64 carved = 0;
+            for (const KvRun& p : b.pieces) {
+                if (p.first_pbn != next_pbn_) throw DeviceError(106, "kv: device PBNs out of sequence");
+                s.carve_kv_run(p.off, p.count, block_bytes_, p.first_pbn);
+                runs_.push_back(p);
+                next_pbn_ += p.count;
+                carved += p.count;
+            }
+            ctr_.blocks_from_pool += carved;
+            ++ctr_.alloc_batches;
+            if (carved) ++ctr_.pool_invocations;
+            ++rep->applied;
+        } else {
+            std::vector<std::pair<u64, u64>> reqs;
+            bool known = true;
+            for (const auto& [slot, tok] : b.reqs) {
+                if (slot >= rid_of_slot_.size() || !reqs_.count(rid_of_slot_[slot])) known = false;
+                else reqs.push_back({rid_of_slot_[slot], tok});
+            }
+            ++rep->replayed;
+            std::vector<u64> counts;
+            St r = known ? batch_allocate(s, st, reqs, &counts, nullptr) : St(Err::InvalidArgument);
+            if (!r && first) first = r;
+        }
+    }
+    return first;
 }
 
 St KvAllocator::table(u64 rid, std::vector<u64>* lbn_to_pbn, u64* tokens) const {

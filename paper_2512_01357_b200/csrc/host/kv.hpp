@@ -57,9 +57,36 @@ struct KvBatchWork {
     std::vector<KvRun> carved;  // the rest, in order
 };
 
+// K4D: what arming an engine uploads (KvAllocator::arm).
+struct KvArmSpec {
+    std::vector<u64> run_off, run_blocks;       // free runs >= 1 block, ascending (size, offset)
+    std::vector<u64> slot_blocks, slot_tokens;  // per table slot
+    u64 free_top = 0, next_pbn = 1;
+    u64 max_blocks_per_request = 0;
+    u32 max_requests = 0, max_batches = 0;
+    u64 block_tokens = 0;
+};
+// One batch of the device log, as read back at sync.
+struct KvLogBatch {
+    u64 status = 0;  // 0 decided and applied on the device, 1 left to the host
+    u64 total = 0, pops = 0;
+    std::vector<std::pair<u64, u64>> reqs;  // (slot, tokens)
+    std::vector<KvRun> pieces;              // carved, in order
+};
+struct KvLog {
+    std::vector<KvLogBatch> batches;
+    u64 stalled = 0;  // 2: the log overflowed and batches were dropped
+};
+
 // Device half (device/kv.cu); null for control-plane-only pools.
 class KvDevice {
 public:
+    // K4D: arm (synchronous), enqueue one batch (asynchronous, graph-capturable;
+    // `stream` null = the engine's stream), read the log back (waits for the
+    // enqueued batches).
+    virtual int arm(const KvArmSpec& a, u64 block_bytes) = 0;
+    virtual int enqueue(const u64* d_slots, const u64* d_tokens, u32 n, void* stream) = 0;
+    virtual int read_log(KvLog* out) = 0;
     virtual ~KvDevice() = default;
     virtual int apply_batch(const KvBatchWork& w, u64 block_bytes, u64* out_pbns /*nullable, w.total*/) = 0;
     // append the request's table (LBN order) to the free list
@@ -113,6 +140,24 @@ public:
     void teardown(Store& s);
     St urgent_reclaim(Store& s, const StatsView& st, u64 blocks);
 
+    // ---- K4D: device-decided batches ------------------------------------------
+    // arm: upload the allocator state and a mirror of the pool's free runs;
+    // until sync, batches of the engine's known requests (by table slot) are
+    // decided and applied by kv_device_batch_kernel with no host round trip,
+    // and the pool must not change (Store::kv_armed).  sync: fold the device's
+    // decisions into the host state (pool regions, tables, counters — equal to
+    // running the same batches through batch_allocate) and replay on the host
+    // path every batch the device left to it; disarms.
+    St arm(Store& s, u64 max_blocks_per_request, u32 max_requests, u32 max_batches);
+    int enqueue_device(const u64* d_slots, const u64* d_tokens, u32 n, void* stream);
+    struct SyncReport {
+        u64 applied = 0, replayed = 0;
+        bool overflow = false;
+    };
+    St sync(Store& s, const StatsView& st, SyncReport* rep);
+    bool armed() const { return armed_; }
+    u32 max_device_requests() const { return arm_max_requests_; }
+
     // table(rid) / address_table() readers.
     St table(u64 rid, std::vector<u64>* lbn_to_pbn, u64* tokens) const;
     void address_table(std::vector<KvRun>* runs) const { *runs = runs_; }
@@ -139,7 +184,10 @@ private:
     u64 free_count_ = 0;
     std::map<u64, Req> reqs_;
     std::vector<u32> free_slots_;
+    std::vector<u64> rid_of_slot_;
     u32 slots_used_ = 0;
+    bool armed_ = false;
+    u32 arm_max_requests_ = 0;
     std::vector<KvRun> runs_;
     KvCounters ctr_;
     std::unique_ptr<KvDevice> dev_;

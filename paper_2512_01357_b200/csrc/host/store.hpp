@@ -147,7 +147,13 @@ public:
     St validate() const;
     std::string dump_json() const;
 
+    // Engines armed for device-decided KV batches (K4D) hold a mirror of the
+    // free runs: while any is armed, nothing may change the layout.
+    u32 kv_armed() const { return kv_armed_; }
+    void set_kv_armed(int delta) { kv_armed_ = static_cast<u32>(static_cast<int>(kv_armed_) + delta); }
+
 private:
+    u32 kv_armed_ = 0;
     void touch();
     u64 epoch_ = 0;
     double alpha_of(const std::string& m) const {

@@ -679,6 +679,35 @@ class KvEngine:
         N.check_runtime(lib.tg_kv_table(self._h, request_id, buf, n.value, C.byref(n), C.byref(tok)), "tg_kv_table")
         return KvBlockTable(request_id, self._bs, {i: buf[i] for i in range(n.value)}, tok.value)
 
+    # ---- device-decided batches (K4D; include/tangram.h) ---------------------------
+    def request_slot(self, request_id) -> int:
+        """Table row of a known request (its LBN->PBN row in the device tables)."""
+        s = C.c_uint32()
+        N.check_runtime(lib.tg_kv_request_slot(self._h, request_id, C.byref(s)), "tg_kv_request_slot")
+        return s.value
+
+    def device_arm(self, store: ReuseStore, max_blocks_per_request, max_requests, max_batches):
+        rc = lib.tg_kv_device_arm(self._h, store._h, max_blocks_per_request, max_requests, max_batches)
+        N.check_runtime(rc, "tg_kv_device_arm")
+        return Result(None) if rc == 0 else Result(error=Error(rc - 1))
+
+    def batch_allocate_device(self, slots_ptr, tokens_ptr, n, stream=None):
+        """Enqueue one batch: `slots_ptr`/`tokens_ptr` are device pointers to n
+        u64 each (e.g. torch int64 tensors' data_ptr()); no host round trip."""
+        N.check_runtime(lib.tg_kv_batch_allocate_device(self._h, C.c_void_p(slots_ptr), C.c_void_p(tokens_ptr), n,
+                                                        C.c_void_p(stream) if stream else None),
+                        "tg_kv_batch_allocate_device")
+
+    def device_sync(self, store: ReuseStore, stats: ModelStatsTable) -> Result:
+        """Fold the device's decisions into the host state; replay the batches
+        the device left to the host.  Value: (applied, replayed) batch counts."""
+        a, r = C.c_uint64(), C.c_uint64()
+        rc = lib.tg_kv_device_sync(self._h, store._h, stats._h, C.byref(a), C.byref(r))
+        N.check_runtime(rc, "tg_kv_device_sync")
+        if rc:
+            return Result(error=Error(rc - 1))
+        return Result((a.value, r.value))
+
     def address_table(self) -> dict:
         n = C.c_uint64()
         lib.tg_kv_address_table(self._h, None, 0, C.byref(n))

@@ -1,0 +1,200 @@
+"""K4D — device-decided KV batches (tg_kv_batch_allocate_device) on a B200.
+
+Batches enqueued between arm and sync are decided by the kernel alone; after
+sync the engine must be indistinguishable from the reference KvEngine
+(kv_engine.hpp:107-161) driven with the same batches: block tables (read back
+from HBM), address table, counters, free list, and the pool dump.  Batches
+the device cannot decide alone (contended pool -> urgent reclaim, a request
+twice, a shrinking token count) are replayed on the host path at sync, with
+the reference's error semantics.
+"""
+import random
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+BS, BPT = 8, 100  # 8 tokens x 100 B = 800 B blocks
+
+
+def _dev(values):
+    import torch
+    return torch.tensor(values, dtype=torch.int64, device="cuda:0")
+
+
+def _fragment(rnd, mine, theirs, n_ops):
+    """Identical random alloc/free sequences on both pools -> holes of mixed sizes."""
+    held = []
+    for i in range(n_ops):
+        if held and rnd.random() < 0.45:
+            off = held.pop(rnd.randrange(len(held)))
+            assert mine.free_kv_region(off).ok() == (theirs.free_kv_region(off) == 0)
+        else:
+            size = rnd.randint(300, 5000)
+            a = mine.alloc_kv_region(size, 10_000 + i)
+            rc, off = theirs.alloc_kv_region(size, 10_000 + i)
+            assert a.ok() == (rc == 0)
+            if a.ok():
+                assert a.value() == off
+                held.append(off)
+    assert mine.dump() == theirs.dump()
+
+
+def _same_engine(kvm, kvr, mine, theirs, live):
+    for rid in live:
+        t, rt = kvm.table(rid), kvr.table(rid)
+        assert rt, rid
+        assert t.token_count == rt["token_count"], rid
+        assert [[k, v] for k, v in sorted(t.lbn_to_pbn.items())] == rt["lbn_to_pbn"], rid
+    st = kvr.state()
+    assert sorted([p, o, s] for p, (o, s) in kvm.address_table().items()) == st["address_table"]
+    s = kvm.stats()
+    assert [s.pool_invocations, s.alloc_batches, s.blocks_from_free_list, s.blocks_from_pool,
+            s.reclaim_events] == [st["stats"][k] for k in ("pool_invocations", "alloc_batches",
+                                                          "blocks_from_free_list", "blocks_from_pool",
+                                                          "reclaim_events")]
+    assert kvm.free_list_size() == st["free_list_size"]
+    assert mine.dump() == theirs.dump()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_device_batches_equal_reference(tg, ref, seed):
+    rnd = random.Random(seed)
+    pool_size = rnd.randint(150_000, 500_000)
+    mine = tg.ReuseStore(tg.GpuSpec(pool_size=pool_size), device=0)
+    theirs = ref.ReuseStore(pool_size)
+    sm, sr = tg.ModelStatsTable(), ref.ModelStatsTable()
+    _fragment(rnd, mine, theirs, 40)
+    kvm, kvr = tg.KvEngine("s", BS, BPT), ref.KvEngine("s", BS, BPT)
+    live, nxt = {}, 1
+    applied_total = replayed_total = 0
+    for session in range(6):
+        # host-path batch: new requests (prefill), releases
+        reqs = [(nxt + i, rnd.randint(0, 40)) for i in range(rnd.randint(1, 5))]
+        nxt += len(reqs)
+        a, b = kvm.batch_allocate(mine, sm, reqs), kvr.batch_allocate(theirs, sr, reqs)
+        assert a.ok() == b["ok"]
+        for rid, _ in reqs:
+            tb = kvr.table(rid)
+            if tb:
+                live[rid] = tb["token_count"]
+        for rid in [r for r in live if rnd.random() < 0.2]:
+            assert kvm.release_request(rid).ok() and kvr.release_request(rid) == 0
+            live.pop(rid)
+        if not live:
+            continue
+        # device session
+        assert kvm.device_arm(mine, 64, 32, 16).ok()
+        keep, first_err = [], None
+        for step in range(rnd.randint(1, 10)):
+            rids = [r for r in live if rnd.random() < 0.7] or [next(iter(live))]
+            batch = [(r, live[r] + rnd.choice([0, 1, 1, 2, 7, 15, 30])) for r in rids]
+            x = rnd.random()
+            if x < 0.08:  # a request twice: the device leaves the batch to the host
+                batch.append((batch[0][0], batch[0][1] + 3))
+            elif x < 0.12:  # shrinking token count: InvalidArgument (partial effects kept)
+                batch.append((batch[0][0], 0))
+            slots = _dev([kvm.request_slot(r) for r, _ in batch])
+            toks = _dev([t for _, t in batch])
+            keep += [slots, toks]
+            kvm.batch_allocate_device(slots.data_ptr(), toks.data_ptr(), len(batch))
+            rr = kvr.batch_allocate(theirs, sr, batch)
+            if not rr["ok"] and first_err is None:
+                first_err = rr["error"]
+            for r in rids:
+                tb = kvr.table(r)
+                live[r] = tb["token_count"]
+        res = kvm.device_sync(mine, sm)
+        if first_err is None:
+            assert res.ok(), res
+            applied, replayed = res.value()
+            applied_total += applied
+            replayed_total += replayed
+        else:
+            assert not res.ok() and res.error().value == first_err
+        _same_engine(kvm, kvr, mine, theirs, live)
+        assert mine.validate().ok()
+    assert applied_total > 0
+    mine.close()
+
+
+def test_device_batches_in_a_cuda_graph(tg, ref):
+    """A decode loop captured once (tokens += 1 per step on the device, then
+    the batch) and replayed: the sync'ed engine equals the reference fed the
+    same 4 x replays batches."""
+    import torch
+    rnd = random.Random(7)
+    pool_size = 800_000
+    mine = tg.ReuseStore(tg.GpuSpec(pool_size=pool_size), device=0)
+    theirs = ref.ReuseStore(pool_size)
+    sm, sr = tg.ModelStatsTable(), ref.ModelStatsTable()
+    _fragment(rnd, mine, theirs, 60)
+    kvm, kvr = tg.KvEngine("s", BS, BPT), ref.KvEngine("s", BS, BPT)
+    reqs = [(i + 1, rnd.randint(1, 60)) for i in range(24)]
+    assert kvm.batch_allocate(mine, sm, reqs).ok() and kvr.batch_allocate(theirs, sr, reqs)["ok"]
+    live = dict(reqs)
+    rids = [r for r, _ in reqs]
+    assert kvm.device_arm(mine, 256, 32, 64).ok()
+    slots = _dev([kvm.request_slot(r) for r in rids])
+    toks = _dev([live[r] for r in rids])
+    inc = _dev([rnd.randint(1, 3) for _ in rids])
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
+            for _ in range(4):
+                toks.add_(inc)
+                kvm.batch_allocate_device(slots.data_ptr(), toks.data_ptr(), len(rids),
+                                          stream=torch.cuda.current_stream().cuda_stream)
+    incs = inc.tolist()
+    replays = 5
+    for _ in range(replays):
+        g.replay()
+    for _ in range(replays * 4):
+        for i, r in enumerate(rids):
+            live[r] += incs[i]
+        assert kvr.batch_allocate(theirs, sr, [(r, live[r]) for r in rids])["ok"]
+    torch.cuda.synchronize()
+    applied, replayed = kvm.device_sync(mine, sm).value()
+    assert applied == replays * 4 and replayed == 0
+    _same_engine(kvm, kvr, mine, theirs, live)
+    mine.close()
+
+
+def test_armed_engine_freezes_the_pool(tg):
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=100_000), device=0)
+    st = tg.ModelStatsTable()
+    kv = tg.KvEngine("s", BS, BPT)
+    assert kv.batch_allocate(pool, st, [(1, 20)]).ok()
+    assert kv.device_arm(pool, 16, 8, 4).ok()
+    from paper_2512_01357_b200 import _native as N
+    with pytest.raises(N.TangramRuntimeError):
+        pool.alloc_kv_region(800, 5)
+    with pytest.raises(N.TangramRuntimeError):
+        kv.batch_allocate(pool, st, [(2, 8)])
+    other = tg.KvEngine("t", BS, BPT)
+    with pytest.raises(N.TangramRuntimeError):
+        other.batch_allocate(pool, st, [(9, 8)])
+    # unknown slot: the batch is left to the host, which cannot map it
+    bad = _dev([99])
+    t = _dev([8])
+    kv.batch_allocate_device(bad.data_ptr(), t.data_ptr(), 1)
+    r = kv.device_sync(pool, st)
+    assert not r.ok() and r.error().name == "InvalidArgument"
+    assert pool.alloc_kv_region(800, 5).ok()  # disarmed
+    # log overflow is reported
+    assert kv.device_arm(pool, 16, 8, 2).ok()
+    s1 = _dev([kv.request_slot(1)])
+    for k in range(3):
+        tk = _dev([24 + 8 * k])
+        kv.batch_allocate_device(s1.data_ptr(), tk.data_ptr(), 1)
+        torch_sync()
+    with pytest.raises(N.TangramRuntimeError):
+        kv.device_sync(pool, st)
+    pool.close()
+
+
+def torch_sync():
+    import torch
+    torch.cuda.synchronize()
