@@ -1067,13 +1067,13 @@ std::uint64_t copy_fp_resident_warps(int sm_count) { return static_cast<u64>(sm_
 namespace {
 template <class Task>
 void load_kernel_launch(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_sync,
-                        const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s) {
+                        const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed) {
     static const bool attr = [] {
         return cudaFuncSetAttribute(copy_fp_kernel<Task>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kCopySmemBytes) == cudaSuccess;
     }();
     (void)attr;
-    cudaMemsetAsync(d_sync, 0, (1 + n_waves) * sizeof(u64), s);
+    if (!sync_zeroed) cudaMemsetAsync(d_sync, 0, (1 + n_waves) * sizeof(u64), s);
     const u64 want = (total_tiles + kCopyWarps - 1) / kCopyWarps;
     const u64 cap = static_cast<u64>(sm_count) * 2;
     const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
@@ -1084,15 +1084,16 @@ void load_kernel_launch(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* 
 }  // namespace
 
 void copy_fp_launch(const CopyFpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, u64* d_sync,
-                    const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s) {
+                    const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed) {
     if (n_tasks == 0) return;
-    if (total_tiles > 0) load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves, sm_count, s);
+    if (total_tiles > 0)
+        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves, sm_count, s, sync_zeroed);
     copy_fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, u64* d_sync,
-               int sm_count, cudaStream_t s) {
+               int sm_count, cudaStream_t s, bool sync_zeroed) {
     if (n_tasks == 0) return;
     // Default: the load kernel with fingerprint-only tasks.  TANGRAM_FP_KERNEL=
     // v0..v5 selects the earlier dedicated K1 variants (A/B runs).
@@ -1108,7 +1109,7 @@ void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums,
     }();
     const bool v0 = variant == 0;
     if (total_tiles > 0 && variant == 6) {
-        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, nullptr, 0, sm_count, s);
+        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, nullptr, 0, sm_count, s, sync_zeroed);
     } else if (total_tiles > 0 && variant == 4) {
         static const bool attr = [] {
             return cudaFuncSetAttribute(fp_v4_kernel<kV3Stages, kWarpsPerCta>,

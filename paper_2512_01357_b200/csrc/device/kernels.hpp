@@ -25,10 +25,12 @@ struct FpTask {
 };
 
 // sums: 2 u64 per task (must be zeroed), digests: 2 u64 per task, sync: one
-// u64 of device scratch private to this launch (zeroed by it).  Runs the load
+// u64 of device scratch private to this launch (zeroed by it unless the caller
+// did, sync_zeroed).  Runs the load
 // kernel below with fingerprint-only tasks.
 void fp_launch(const FpTask* d_tasks, std::uint32_t n_tasks, std::uint64_t total_tiles, std::uint64_t* d_sums,
-               std::uint64_t* d_digests, std::uint64_t* d_sync, int sm_count, cudaStream_t s);
+               std::uint64_t* d_digests, std::uint64_t* d_sync, int sm_count, cudaStream_t s,
+               bool sync_zeroed = false);
 
 // ---- K3F: copy + fingerprint in one pass — the load kernel ---------------
 // Moves every task's n bytes src -> dst (any alignments) and produces the
@@ -46,11 +48,12 @@ struct CopyFpTask {
     std::int32_t gate;    // wave that must be complete before this task writes (-1: none)
     std::int32_t wave;    // wave this task belongs to (its tiles count towards need[wave]; -1: none)
 };
-// sync: 1 + n_waves u64 of device scratch (zeroed by the launch); need[w] =
+// sync: 1 + n_waves u64 of device scratch (zeroed by the launch unless
+// sync_zeroed); need[w] =
 // tiles of wave w's tasks.  sums: 2 u64 per task (zeroed by the caller).
 void copy_fp_launch(const CopyFpTask* d_tasks, std::uint32_t n_tasks, std::uint64_t total_tiles, std::uint64_t* d_sums,
                     std::uint64_t* d_digests, std::uint64_t* d_sync, const std::uint64_t* d_need,
-                    std::uint32_t n_waves, int sm_count, cudaStream_t s);
+                    std::uint32_t n_waves, int sm_count, cudaStream_t s, bool sync_zeroed = false);
 // Warps one load-kernel launch keeps resident (tile-count sizing of the
 // independent work placed between gated waves).
 std::uint64_t copy_fp_resident_warps(int sm_count);

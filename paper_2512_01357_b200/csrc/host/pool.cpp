@@ -443,30 +443,32 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     const std::size_t fdesc = nf * sizeof(FpTask), cdesc = nc * sizeof(CopyFpTask), ndesc = waves * sizeof(u64);
     const std::size_t desc_bytes = (fdesc + cdesc + ndesc + 15) & ~std::size_t{15};
     const std::size_t sums_bytes = (nf + nc) * 2 * sizeof(u64);
-    ensure_stage(desc_bytes + 2 * sums_bytes + (1 + waves + n_fp_launch) * sizeof(u64) + 64);
+    // stage: [descriptors][sums = 0][sync counters = 0][digests]; the first
+    // three go up in one H2D, so no memset precedes the kernels
+    const std::size_t sync_bytes = (1 + waves + n_fp_launch) * sizeof(u64);
+    ensure_stage(desc_bytes + 2 * sums_bytes + sync_bytes + 64);
     auto* h = static_cast<std::uint8_t*>(h_stage_);
     auto* dptr = static_cast<std::uint8_t*>(d_stage_);
     if (nf) std::memcpy(h, tasks.data(), fdesc);
     if (nc) std::memcpy(h + fdesc, ctasks.data(), cdesc);
     if (waves) std::memcpy(h + fdesc + cdesc, need.data(), ndesc);
+    std::memset(h + desc_bytes, 0, sums_bytes + sync_bytes);
     const auto* d_tasks = reinterpret_cast<const FpTask*>(dptr);
     const auto* d_ctasks = reinterpret_cast<const CopyFpTask*>(dptr + fdesc);
     const auto* d_need = reinterpret_cast<const u64*>(dptr + fdesc + cdesc);
     auto* d_sums = reinterpret_cast<u64*>(dptr + desc_bytes);
-    auto* d_dig = reinterpret_cast<u64*>(dptr + desc_bytes + sums_bytes);
-    auto* d_sync = reinterpret_cast<u64*>(dptr + desc_bytes + 2 * sums_bytes);
+    auto* d_sync = reinterpret_cast<u64*>(dptr + desc_bytes + sums_bytes);
+    auto* d_dig = reinterpret_cast<u64*>(dptr + desc_bytes + sums_bytes + sync_bytes);
     u64* d_fp_sync = d_sync + 1 + waves;  // one tile counter per K1 launch
-    if (nf + nc) {
-        TG_CUDA(cudaMemcpyAsync(dptr, h, desc_bytes, cudaMemcpyHostToDevice, s_main_));
-        TG_CUDA(cudaMemsetAsync(d_sums, 0, sums_bytes, s_main_));
-    }
+    if (nf + nc)
+        TG_CUDA(cudaMemcpyAsync(dptr, h, desc_bytes + sums_bytes + sync_bytes, cudaMemcpyHostToDevice, s_main_));
 
     // ---- device work on the main stream: the load kernel (fused) or the K3
     // relocation waves (unfused) ----------------------------------------------------
     TG_CUDA(cudaEventRecord(ev(1), s_main_));
     if (fused) {
         copy_fp_launch(d_ctasks, static_cast<u32>(nc), ctiles, d_sums + 2 * nf, d_dig + 2 * nf, d_sync, d_need, waves,
-                       sm_count_, s_main_);
+                       sm_count_, s_main_, /*sync_zeroed=*/true);
         TG_CUDA(cudaGetLastError());
         for (u32 w = 0; w < waves; ++w) TG_CUDA(cudaEventRecord(ev(ev_wave + w), s_main_));
         for (std::size_t i = 0; i < np; ++i)
@@ -533,7 +535,8 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
         if (k == kNone) continue;
         TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(ev_land + i)));
         TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s_fp_));
-        fp_launch(d_tasks + k, 1, new_tiles[k], d_sums + 2 * k, d_dig + 2 * k, d_fp_sync + fp_i, sm_count_, s_fp_);
+        fp_launch(d_tasks + k, 1, new_tiles[k], d_sums + 2 * k, d_dig + 2 * k, d_fp_sync + fp_i, sm_count_, s_fp_,
+                  /*sync_zeroed=*/true);
         TG_CUDA(cudaGetLastError());
         TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s_fp_));
         ++fp_i;
@@ -547,7 +550,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             if (!count) return;
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s));
             fp_launch(d_tasks + first, static_cast<u32>(count), tiles, d_sums + 2 * first, d_dig + 2 * first,
-                      d_fp_sync + fp_i, sm_count_, s);
+                      d_fp_sync + fp_i, sm_count_, s, /*sync_zeroed=*/true);
             TG_CUDA(cudaGetLastError());
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s));
             ++fp_i;
@@ -571,7 +574,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
         TG_CUDA(cudaStreamWaitEvent(s_main_, ev(3)));
     }
     TG_CUDA(cudaEventRecord(ev(3), s_main_));
-    auto* h_dig = reinterpret_cast<u64*>(h + desc_bytes + sums_bytes);
+    auto* h_dig = reinterpret_cast<u64*>(h + desc_bytes + sums_bytes + sync_bytes);
     if (nf + nc) TG_CUDA(cudaMemcpyAsync(h_dig, d_dig, sums_bytes, cudaMemcpyDeviceToHost, s_main_));
     TG_CUDA(cudaStreamSynchronize(s_main_));
 
