@@ -131,7 +131,8 @@ typedef struct {
 typedef struct {
     tg_tensor_id tensor;
     uint64_t offset, size;
-    uint32_t source; /* 0 host/PCIe, 1 peer pool/NVLink, 2 device-resident source (HBM) */
+    uint32_t source; /* 0 host/PCIe, 1 peer pool/NVLink, 2 device-resident source (HBM),
+                        3 re-shard: assembled over NVLink from peer shards of another layout */
 } tg_placement;
 
 /* warmsim::Region (region_pool.hpp:22-28) */
@@ -288,6 +289,17 @@ int tg_pool_update_remote(tg_pool* p, int32_t peer_id, const tg_index_entry* idx
 int tg_pool_snapshot(tg_pool* p, tg_snapshot** out);
 int tg_pool_restore(tg_pool* p, const tg_snapshot* s);
 void tg_snapshot_destroy(tg_snapshot* s);
+
+/* ---- shard lineage (re-shard pulls) -----------------
+ * tg_model_shard records, for every shard tensor, the byte range of its
+ * parent tensor it holds.  A load with TG_LOAD_PEER whose miss has no exact
+ * copy on a peer assembles it from resident shards of the same parent in any
+ * other layout on peer pools (in-process peers or attached remote pools):
+ * one NVLink piece per overlapping shard, then a fingerprint of the assembled
+ * tensor (placement source 3).  tg_lineage_register declares the relation
+ * for shards made elsewhere; tg_lineage_get reads it. */
+int tg_lineage_register(tg_tensor_id child, tg_tensor_id parent, uint64_t begin, uint64_t size);
+int tg_lineage_get(tg_tensor_id child, tg_tensor_id* parent, uint64_t* begin, uint64_t* size);
 
 /* ---- host checkpoint sources (data side-channel) --------------
  * ptr may be pinned host memory (placed over PCIe by the copy engine) or

@@ -4,7 +4,9 @@ Bytes of tensor t are the little-endian u64 stream
 splitmix64(t.hi ^ rotl(t.lo, 17) ^ (w * 0x9E3779B97F4A7C15)), truncated to
 t.size — content is a pure function of the TensorId, so "same content" and
 "same key" coincide and content-keyed reuse decisions equal the reference's
-key-based ones.  Buffers are pinned (cudaMallocHost) and registered with the
+key-based ones.  A tensor-parallel shard (shard_model) holds its byte range
+of the parent tensor's stream, so shards of one tensor in different layouts
+agree byte for byte where they overlap.  Buffers are pinned (cudaMallocHost) and registered with the
 library as the byte source of each tensor (tg_host_register).  Large
 checkpoints are generated on the GPU (synth kernel) and copied down once.
 """
@@ -13,7 +15,7 @@ import ctypes as C
 import numpy as np
 
 from . import _native as N
-from .pool import ModelSpec, TensorId
+from .pool import ModelSpec, TensorId, lineage
 
 lib = N.lib
 
@@ -58,6 +60,13 @@ class DeviceBuffer:
     __del__ = free
 
 
+def content_of(tid: TensorId):
+    """(stream id, offset) of a tensor's synthetic bytes: its own stream, or
+    its parent's at the shard's offset."""
+    lin = lineage(tid)
+    return (tid, 0) if lin is None else (lin[0], lin[1])
+
+
 def synth_host(tid: TensorId, n, begin=0, threads=8):
     out = np.empty(n, dtype=np.uint8)
     if n:
@@ -86,11 +95,12 @@ class HostCheckpoint:
         off = 0
         for t in tensors:
             ptr = self.slab.ptr + off
+            sid, begin = content_of(t.id)
             if fill == "device":
-                N.check_runtime(lib.tg_synth_fill_device(t.id.c(), 0, t.size, C.c_void_p(scratch.ptr), device))
+                N.check_runtime(lib.tg_synth_fill_device(sid.c(), begin, t.size, C.c_void_p(scratch.ptr), device))
                 N.check_runtime(lib.tg_memcpy(C.c_void_p(ptr), C.c_void_p(scratch.ptr), t.size), "tg_memcpy")
             else:
-                lib.tg_synth_fill_host(t.id.c(), 0, t.size, C.c_void_p(ptr), 8)
+                lib.tg_synth_fill_host(sid.c(), begin, t.size, C.c_void_p(ptr), 8)
             if register:
                 N.check_runtime(lib.tg_host_register(t.id.c(), C.c_void_p(ptr), t.size, None), "tg_host_register")
             self.entries[t.id] = (ptr, t.size)

@@ -220,6 +220,7 @@ int tg_model_shard(const tg_model* m, uint32_t rank, uint32_t world, tg_model** 
         d.size = e - b;
         const std::int64_t elems = static_cast<std::int64_t>(d.size / 2);
         d.id = tensor_key(d.model_id, d.name, &elems, 1, Dtype::F16);
+        ShardLineage::get().put(d.id, ShardOf{t.id, b, d.size});
         s->m.tensors.push_back(d);
         s->m.total_size += d.size;
     }
@@ -227,6 +228,19 @@ int tg_model_shard(const tg_model* m, uint32_t rank, uint32_t world, tg_model** 
               [](const TensorDesc& a, const TensorDesc& b) { return a.name < b.name; });
     s->refresh();
     *out = s;
+    return 0;
+}
+
+int tg_lineage_register(tg_tensor_id child, tg_tensor_id parent, uint64_t begin, uint64_t size) {
+    ShardLineage::get().put(key_of(child), ShardOf{key_of(parent), begin, size});
+    return 0;
+}
+int tg_lineage_get(tg_tensor_id child, tg_tensor_id* parent, uint64_t* begin, uint64_t* size) {
+    ShardOf s;
+    if (!ShardLineage::get().find(key_of(child), &s)) return code_of(Err::NotFound);
+    if (parent) *parent = id_of(s.parent);
+    if (begin) *begin = s.begin;
+    if (size) *size = s.size;
     return 0;
 }
 

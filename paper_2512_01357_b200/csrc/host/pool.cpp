@@ -36,6 +36,32 @@ void SourceRegistry::erase(const Key& k) {
     std::lock_guard<std::mutex> g(mu_);
     map_.erase(k);
 }
+ShardLineage& ShardLineage::get() {
+    static ShardLineage r;
+    return r;
+}
+void ShardLineage::put(const Key& child, const ShardOf& s) {
+    std::lock_guard<std::mutex> g(mu_);
+    if (of_.count(child)) return;
+    of_[child] = s;
+    kids_[s.parent].push_back(child);
+}
+bool ShardLineage::find(const Key& child, ShardOf* out) const {
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = of_.find(child);
+    if (it == of_.end()) return false;
+    *out = it->second;
+    return true;
+}
+std::vector<std::pair<Key, ShardOf>> ShardLineage::children(const Key& parent) const {
+    std::lock_guard<std::mutex> g(mu_);
+    std::vector<std::pair<Key, ShardOf>> out;
+    auto it = kids_.find(parent);
+    if (it == kids_.end()) return out;
+    for (const Key& c : it->second) out.push_back({c, of_.at(c)});
+    return out;
+}
+
 void SourceRegistry::clear() {
     std::lock_guard<std::mutex> g(mu_);
     map_.clear();
@@ -260,6 +286,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     std::vector<HostSource> src(np);
     std::vector<const std::uint8_t*> peer_src(np, nullptr);
     std::vector<Digest> peer_digest(np);  // what the peer's index says the bytes fingerprint to
+    std::vector<std::vector<MoveDesc>> pieces(np);  // re-shard pulls: src, dst offset in the tensor, len
     rep->placement_src.assign(np, 0);
     if (has_device()) {
         for (std::size_t i = 0; i < np; ++i) {
@@ -283,7 +310,8 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
                     }
                 }
             }
-            if (peer_src[i]) continue;
+            if (!peer_src[i] && (flags & kLoadPeer) && assemble_shard(t, &pieces[i])) rep->placement_src[i] = 3;
+            if (peer_src[i] || rep->placement_src[i] == 3) continue;
             if (!SourceRegistry::get().find(t.id, &src[i]) || src[i].size != t.size)
                 throw DeviceError(kErrNoSource, "no host source registered for tensor " + t.id.hex() + " (" +
                                                     t.model_id + "/" + t.name + ")");
@@ -338,7 +366,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     for (std::size_t i = 0; i < np; ++i) {
         const u64 sz = D.miss_desc[D.plan.placements[i].tensor].size;
         const std::uint8_t k = rep->placement_src[i];
-        (k == 0 ? rep->pcie_bytes : k == 1 ? rep->peer_bytes : rep->device_src_bytes) += sz;
+        (k == 0 ? rep->pcie_bytes : (k == 1 || k == 3) ? rep->peer_bytes : rep->device_src_bytes) += sz;
     }
 
     // ---- event layout -----------------------------------------------------------
@@ -361,7 +389,10 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     }
     // K1 after landing: host-sourced placements always; device-sourced ones
     // only when unfused (fused: K3F hashes them while it copies)
-    auto k1_placement = [&](std::size_t i) { return fp_new && (!fused || rep->placement_src[i] == 0); };
+    // (re-shard pulls, kind 3, are assembled from several pieces: K1 after the last lands)
+    auto k1_placement = [&](std::size_t i) {
+        return fp_new && (!fused || rep->placement_src[i] == 0 || rep->placement_src[i] == 3);
+    };
     auto tiles_of = [](u64 n) { return ((n + kLeafBytes - 1) / kLeafBytes + kLeavesPerTile - 1) / kLeavesPerTile; };
     constexpr std::size_t kNone = ~std::size_t{0};
 
@@ -422,7 +453,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
                 push(arena_ + rel[j].from, arena_ + rel[j].to, rel[j].size, gate, static_cast<int>(g));
             }
             for (std::size_t i = 0; i < np; ++i) {
-                if (rep->placement_src[i] == 0 || dep[i] != gate) continue;
+                if (rep->placement_src[i] == 0 || rep->placement_src[i] == 3 || dep[i] != gate) continue;
                 ctask_of_placement[i] = ctasks.size();
                 push(peer_src[i], arena_ + D.plan.placements[i].off, D.miss_desc[D.plan.placements[i].tensor].size,
                      gate, -1);
@@ -507,7 +538,15 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             TG_CUDA(cudaStreamWaitEvent(s, ev(ev_wave + dep[i])));
             waited = dep[i];
         }
-        if (dev_src && fused) {
+        if (rep->placement_src[i] == 3) {
+            std::vector<MoveDesc> mv = pieces[i];
+            for (MoveDesc& md : mv) md.dst += reinterpret_cast<u64>(arena_ + pl.off);
+            for (std::size_t at = 0; at < mv.size(); at += kMaxMovesPerLaunch) {
+                relocate_launch(mv.data() + at, static_cast<int>(std::min<std::size_t>(kMaxMovesPerLaunch, mv.size() - at)),
+                                sm_count_, s);
+                TG_CUDA(cudaGetLastError());
+            }
+        } else if (dev_src && fused) {
             continue;  // in the load kernel
         } else if (dev_src) {
             MoveDesc md{reinterpret_cast<u64>(peer_src[i]), reinterpret_cast<u64>(arena_ + pl.off), sz};
@@ -657,6 +696,48 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     totals_.fingerprint_bytes += rep->fingerprint_bytes;
     totals_.relocated_bytes += D.plan.total_merge_cost;
     return ok();
+}
+
+// Re-shard pull: cover tensor t's parent byte range with resident shards of
+// the same parent on peer pools (any TP layout); pieces hold the peer source,
+// the destination offset inside t, and the length.
+bool Pool::assemble_shard(const TensorDesc& t, std::vector<MoveDesc>* pieces) const {
+    ShardOf me;
+    if (!ShardLineage::get().find(t.id, &me) || me.size != t.size || t.size == 0) return false;
+    struct Cand {
+        u64 b, e;
+        const std::uint8_t* base;
+    };
+    std::vector<Cand> cands;
+    for (const auto& [kid, of] : ShardLineage::get().children(me.parent)) {
+        if (kid == t.id || of.begin >= me.begin + me.size || of.begin + of.size <= me.begin) continue;
+        const std::uint8_t* base = nullptr;
+        for (Pool* p : peers_) {
+            const Entry* e = p->store_.entry(kid);
+            if (e && e->size == of.size && e->has_digest) {
+                base = p->arena_ + e->off;
+                break;
+            }
+        }
+        for (std::size_t r = 0; !base && r < remotes_.size(); ++r) {
+            auto it = remotes_[r].index.find(kid);
+            if (it != remotes_[r].index.end() && it->second.size == of.size) base = remotes_[r].base + it->second.off;
+        }
+        if (base) cands.push_back(Cand{of.begin, of.begin + of.size, base});
+    }
+    std::vector<MoveDesc> out;
+    const u64 end = me.begin + me.size;
+    for (u64 pos = me.begin; pos < end;) {
+        const Cand* best = nullptr;
+        for (const Cand& c : cands)
+            if (c.b <= pos && pos < c.e && (!best || c.e > best->e)) best = &c;
+        if (!best) return false;
+        const u64 len = std::min(best->e, end) - pos;
+        out.push_back(MoveDesc{reinterpret_cast<u64>(best->base + (pos - best->b)), pos - me.begin, len});
+        pos += len;
+    }
+    *pieces = std::move(out);
+    return true;
 }
 
 // Bytes of a registered source into the arena (repair paths).

@@ -77,6 +77,30 @@ private:
     std::unordered_map<Key, HostSource, KeyHash> map_;
 };
 
+// Shard lineage (process-wide): tensor `child` holds bytes [begin, begin +
+// size) of tensor `parent` — what tg_model_shard produces for every shard.
+// A load may then assemble a missing shard from the resident shards of the
+// same parent in another layout on peer pools (re-shard pull, SURVEY §8(d)
+// C4 "shards resident on peers in a previous TP layout").
+struct ShardOf {
+    Key parent;
+    u64 begin = 0;
+    u64 size = 0;
+};
+class ShardLineage {
+public:
+    static ShardLineage& get();
+    void put(const Key& child, const ShardOf& s);
+    bool find(const Key& child, ShardOf* out) const;
+    // children of `parent` as (child, lineage)
+    std::vector<std::pair<Key, ShardOf>> children(const Key& parent) const;
+
+private:
+    mutable std::mutex mu_;
+    std::unordered_map<Key, ShardOf, KeyHash> of_;
+    std::unordered_map<Key, std::vector<Key>, KeyHash> kids_;
+};
+
 // A resident, fingerprinted tensor of a peer pool (what peers exchange).
 struct RemoteEntry {
     Key id;
@@ -111,7 +135,7 @@ struct LoadTimings {
 struct LoadReport {
     LoadDecision decision;           // hits / misses / plan (placements index miss_desc)
     std::vector<u32> reloc_wave;     // WAR wave of each relocation
-    std::vector<std::uint8_t> placement_src;  // 0 = host (PCIe), 1 = peer (NVLink)
+    std::vector<std::uint8_t> placement_src;  // 0 host (PCIe), 1 peer (NVLink), 2 HBM source, 3 re-shard pieces
     u32 waves = 0;
     u64 pcie_bytes = 0, peer_bytes = 0, device_src_bytes = 0, fingerprint_bytes = 0, repaired_bytes = 0;
     u32 verify_mismatches = 0, expected_mismatches = 0;
@@ -186,6 +210,7 @@ private:
     std::uint8_t* arena_ = nullptr;
     cudaStream_t s_main_ = nullptr, s_copy_ = nullptr, s_fp_ = nullptr, s_peer_ = nullptr, s_verify_ = nullptr;
     std::vector<cudaEvent_t> events_;
+    bool assemble_shard(const TensorDesc& t, std::vector<MoveDesc>* pieces) const;
     std::vector<Pool*> peers_;
     struct RemotePeer {
         std::uint8_t* base = nullptr;  // IPC-mapped peer arena

@@ -186,11 +186,20 @@ def shard_model(model: ModelSpec, rank: int, world: int) -> ModelSpec:
         if e <= b:
             continue
         name = t.name + suffix
-        ts.append(TensorSpec(tensor_key(model.model_id + suffix, name, [(e - b) // 2]),
-                             model.model_id + suffix, name, e - b))
+        tid = tensor_key(model.model_id + suffix, name, [(e - b) // 2])
+        lib.tg_lineage_register(tid.c(), t.id.c(), b, e - b)  # shard = bytes [b, e) of t
+        ts.append(TensorSpec(tid, model.model_id + suffix, name, e - b))
     ts.sort(key=lambda t: t.name)
     return ModelSpec(model.model_id + suffix, ts, sum(t.size for t in ts), model.latency_sensitivity,
                      model.location, model.bytes_per_token // world)
+
+
+def lineage(tid: TensorId):
+    """(parent TensorId, begin, size) if `tid` is a shard of another tensor, else None."""
+    p, b, n = N.TensorIdC(), C.c_uint64(), C.c_uint64()
+    if lib.tg_lineage_get(tid.c(), C.byref(p), C.byref(b), C.byref(n)) != 0:
+        return None
+    return TensorId(p.hi, p.lo), b.value, n.value
 
 
 def tensor_key(model_id, name, shape, dtype=1) -> TensorId:
@@ -298,7 +307,7 @@ class Placement:
     tensor: TensorId
     offset: int
     size: int
-    source: int = 0  # 0 host/PCIe, 1 peer/NVLink
+    source: int = 0  # 0 host/PCIe, 1 peer/NVLink, 2 HBM source, 3 re-shard pieces from peer shards
 
 
 @dataclass

@@ -1,0 +1,86 @@
+"""Re-shard pulls (SURVEY §8(d) C4 "shards resident on peers in a previous TP
+layout", §8(e)): a pool loading the TP4 shards of a model whose TP2 shards
+are resident on two peer pools assembles every tensor from the overlapping
+TP2 pieces device-to-device (on one GPU the peers are pools on the same
+device), with no host source registered.  Decisions equal the reference's
+for the TP4 shard ModelSpecs; every assembled tensor fingerprints equal to the
+CPU restatement of its byte range of the parent tensor.
+"""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _expected(cpu, tg, t):
+    parent, begin, size = tg.lineage(t.id)
+    assert size == t.size
+    return cpu.content_fingerprint(cpu.synth(parent.hi, parent.lo, size, begin), threads=8)[0]
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["K3+K1", "K3F"])
+def test_tp2_to_tp4_reshard_from_peers(tg, cpu, ref, fused):
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    m = tg.make_model("reshard", 60_000_011, 3, 8192)
+    tp2 = [tg.shard_model(m, r, 2) for r in range(2)]
+    tp4 = [tg.shard_model(m, r, 4) for r in range(4)]
+    peers = [tg.ReuseStore(tg.GpuSpec(f"gpu{r}", 40_000_000), device=0) for r in range(2)]
+    with HostCheckpoint(tp2):
+        for r, p in enumerate(peers):
+            st = tg.ModelStatsTable()
+            st.record_request(tp2[r].model_id, 0.0)
+            o = p.load_model(tp2[r], st, 0.0).value()
+            for i, t in enumerate(tp2[r].tensors):  # TP2 bytes = parent ranges
+                assert o.digests[i] == _expected(cpu, tg, t)
+    # sources unregistered: the TP4 bytes can only come from the peers
+    c = tg.ReuseStore(tg.GpuSpec("gpu2", 64_000_000), device=0)
+    for p in peers:
+        c.add_peer(p)
+    sc = tg.ModelStatsTable()
+    r_pool, r_stats = ref.ReuseStore(64_000_000, gpu_id="gpu2"), ref.ModelStatsTable()
+    for k, shard in enumerate(tp4):
+        sc.record_request(shard.model_id, float(k))
+        o = c.load_model(shard, sc, float(k), tg.LoadPolicy(flags=1 | 2 | 4 | (8 if fused else 0))).value()
+        assert o.peer_bytes == shard.total_size and o.pcie_bytes == 0
+        assert all(p.source == 3 for p in o.plan.placements)
+        for i, t in enumerate(shard.tensors):
+            assert o.digests[i] == _expected(cpu, tg, t), (shard.model_id, t.name)
+        c.end_instance(shard.model_id)
+        r_stats.record_request(shard.model_id, float(k))
+        r_pool.load_model(shard.to_json(), r_stats, float(k))
+        r_pool.end_instance(shard.model_id)
+        assert c.dump() == r_pool.dump()
+    # a warm reload of a TP4 shard reuses in place (no peer bytes)
+    sc.record_request(tp4[1].model_id, 9.0)
+    o = c.load_model(tp4[1], sc, 9.0).value()
+    assert o.bytes_transferred == 0 and o.verify_mismatches == 0
+    c.close()
+    for p in peers:
+        p.close()
+
+
+def test_reshard_needs_full_cover(tg):
+    """A TP4 shard straddling a TP2 boundary with only one TP2 peer resident
+    cannot be assembled: the load asks for a host source and, with none
+    registered, fails leaving the pool unchanged."""
+    from paper_2512_01357_b200 import _native as N
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    m = tg.make_model("reshard-gap", 20_000_003, 2, 8192)
+    tp2 = [tg.shard_model(m, r, 2) for r in range(2)]
+    tp4 = [tg.shard_model(m, r, 4) for r in range(4)]
+    a = tg.ReuseStore(tg.GpuSpec("gpu0", 20_000_000), device=0)
+    with HostCheckpoint([tp2[0]]):
+        st = tg.ModelStatsTable()
+        st.record_request(tp2[0].model_id, 0.0)
+        a.load_model(tp2[0], st, 0.0).value()
+    c = tg.ReuseStore(tg.GpuSpec("gpu1", 20_000_000), device=0)
+    c.add_peer(a)
+    sc = tg.ModelStatsTable()
+    sc.record_request(tp4[0].model_id, 0.0)
+    assert c.load_model(tp4[0], sc, 0.0, tg.LoadPolicy(flags=1 | 2 | 4 | 8)).value().peer_bytes == tp4[0].total_size
+    before = c.dump()
+    sc.record_request(tp4[2].model_id, 1.0)  # bytes [n/2, 3n/4): on no peer
+    with pytest.raises(N.TangramRuntimeError):
+        c.load_model(tp4[2], sc, 1.0, tg.LoadPolicy(flags=1 | 2 | 4 | 8))
+    assert c.dump() == before
+    a.close()
+    c.close()
