@@ -798,7 +798,8 @@ u64 Pool::peer_reuse_size(const ModelDesc& m) const {
             }
         for (const RemotePeer& r : remotes_)
             if (!found && r.index.count(t.id)) found = true;
-        if (found) s += t.size;
+        std::vector<MoveDesc> pieces;  // or assembled from peer shards of another layout
+        if (found || (has_device() && assemble_shard(t, &pieces))) s += t.size;
     }
     return s;
 }

@@ -38,6 +38,7 @@ def test_tp2_to_tp4_reshard_from_peers(tg, cpu, ref, fused):
     sc = tg.ModelStatsTable()
     r_pool, r_stats = ref.ReuseStore(64_000_000, gpu_id="gpu2"), ref.ModelStatsTable()
     for k, shard in enumerate(tp4):
+        assert c.peer_reuse_size(shard) == shard.total_size  # the scheduler's S'_peer term
         sc.record_request(shard.model_id, float(k))
         o = c.load_model(shard, sc, float(k), tg.LoadPolicy(flags=1 | 2 | 4 | (8 if fused else 0))).value()
         assert o.peer_bytes == shard.total_size and o.pcie_bytes == 0
