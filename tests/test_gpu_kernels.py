@@ -141,3 +141,28 @@ def test_copy_fingerprint_batched_moves(tg, cpu):
         N.lib.tg_memcpy(out.ctypes.data_as(C.c_void_p), C.c_void_p(moves[3 * k + 1]), n)
         assert np.array_equal(out, datas[k])
         assert (dig[k].hi, dig[k].lo) == cpu.content_fingerprint(datas[k], threads=4)[0]
+
+
+def test_tensor_beyond_4gib(tg, cpu):
+    """A 4.5 GB tensor (byte offsets, leaf and tile counts past 2^32): K1 and
+    the load kernel's move + fingerprint agree with the CPU restatement, and
+    the moved bytes match around the 4 GiB boundary and at both ends."""
+    from paper_2512_01357_b200 import _native as N
+    from paper_2512_01357_b200.checkpoint import DeviceBuffer
+    n = 4_500_000_007
+    tid = tg.TensorId(0xABCD, 0x4242)
+    src, dst = DeviceBuffer(n + 64), DeviceBuffer(n + 64)
+    assert N.lib.tg_synth_fill_device(tid.c(), 0, n, C.c_void_p(src.ptr + 5), 0) == 0
+    host = np.empty(n, dtype=np.uint8)
+    N.lib.tg_memcpy(host.ctypes.data_as(C.c_void_p), C.c_void_p(src.ptr + 5), n)
+    want = cpu.content_fingerprint(host, threads=16)[0]
+    assert _dev_fp(tg, src.ptr + 5, n) == want
+    mv = (C.c_uint64 * 3)(src.ptr + 5, dst.ptr + 14, n)
+    dig = (N.DigestC * 1)()
+    assert N.lib.tg_copy_fingerprint(mv, 1, 0, 0, None, dig) == 0, N.lib.tg_last_error_detail()
+    assert (dig[0].hi, dig[0].lo) == want
+    for lo in (0, (1 << 32) - 4099, n - 5000):
+        w = np.empty(4099, dtype=np.uint8)
+        N.lib.tg_memcpy(w.ctypes.data_as(C.c_void_p), C.c_void_p(dst.ptr + 14 + lo), 4099)
+        assert np.array_equal(w, host[lo:lo + 4099]), lo
+    assert _dev_fp(tg, dst.ptr + 14, n) == want
