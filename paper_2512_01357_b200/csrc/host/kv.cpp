@@ -18,6 +18,11 @@ KvAllocator::KvAllocator(const KvAllocator& o)
       ctr_(o.ctr_),
       dev_(o.dev_ ? o.dev_->clone() : nullptr) {}
 
+KvAllocator::~KvAllocator() {
+    if (armed_)
+        if (auto c = armed_on_.lock()) --*c;
+}
+
 KvAllocator& KvAllocator::operator=(const KvAllocator& o) {
     if (this == &o) return *this;
     KvAllocator tmp(o);
@@ -265,7 +270,8 @@ St KvAllocator::arm(Store& s, u64 max_blocks_per_request, u32 max_requests, u32 
     if (int rc = dev_->arm(a, block_bytes_)) throw DeviceError(rc, "kv: arm failed");
     armed_ = true;
     arm_max_requests_ = max_requests;
-    s.set_kv_armed(+1);
+    armed_on_ = s.kv_arm_handle();
+    if (auto c = armed_on_.lock()) ++*c;
     return ok();
 }
 
@@ -279,7 +285,8 @@ St KvAllocator::sync(Store& s, const StatsView& st, SyncReport* rep) {
     KvLog log;
     if (int rc = dev_->read_log(&log)) throw DeviceError(rc, "kv: device log read failed");
     armed_ = false;
-    s.set_kv_armed(-1);
+    if (auto c = armed_on_.lock()) --*c;
+    armed_on_.reset();
     rep->overflow = log.stalled == 2;
     St first = ok();
     for (const KvLogBatch& b : log.batches) {

@@ -105,7 +105,8 @@ class KvAllocator {
 public:
     KvAllocator(std::string model, u64 block_tokens, u64 bytes_per_token)
         : model_(std::move(model)), block_tokens_(block_tokens), block_bytes_(block_tokens * bytes_per_token) {}
-    KvAllocator(const KvAllocator& o);  // deep copy, device tables included
+    ~KvAllocator();
+    KvAllocator(const KvAllocator& o);  // deep copy, device tables included (never armed)
     KvAllocator& operator=(const KvAllocator& o);
     KvAllocator(KvAllocator&&) noexcept = default;
     KvAllocator& operator=(KvAllocator&&) noexcept = default;
@@ -187,6 +188,7 @@ private:
     std::vector<u64> rid_of_slot_;
     u32 slots_used_ = 0;
     bool armed_ = false;
+    std::weak_ptr<int> armed_on_;  // the store's arm count (Store::kv_arm_handle)
     u32 arm_max_requests_ = 0;
     std::vector<KvRun> runs_;
     KvCounters ctr_;

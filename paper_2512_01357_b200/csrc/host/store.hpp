@@ -6,6 +6,7 @@
 #pragma once
 
 #include <map>
+#include <memory>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -148,12 +149,26 @@ public:
     std::string dump_json() const;
 
     // Engines armed for device-decided KV batches (K4D) hold a mirror of the
-    // free runs: while any is armed, nothing may change the layout.
-    u32 kv_armed() const { return kv_armed_; }
-    void set_kv_armed(int delta) { kv_armed_ = static_cast<u32>(static_cast<int>(kv_armed_) + delta); }
+    // free runs: while any is armed, nothing may change the layout.  Engines
+    // hold a weak handle on the count, so an engine destroyed while armed
+    // releases its arm, and one outliving the store touches nothing; copies
+    // of a store (snapshots) start with a count of their own at zero.
+    class ArmCount {
+    public:
+        ArmCount() : c_(std::make_shared<int>(0)) {}
+        ArmCount(const ArmCount&) : ArmCount() {}
+        ArmCount& operator=(const ArmCount&) { return *this; }
+        int value() const { return *c_; }
+        std::weak_ptr<int> handle() const { return c_; }
+
+    private:
+        std::shared_ptr<int> c_;
+    };
+    u32 kv_armed() const { return static_cast<u32>(kv_armed_.value()); }
+    std::weak_ptr<int> kv_arm_handle() const { return kv_armed_.handle(); }
 
 private:
-    u32 kv_armed_ = 0;
+    ArmCount kv_armed_;
     void touch();
     u64 epoch_ = 0;
     double alpha_of(const std::string& m) const {

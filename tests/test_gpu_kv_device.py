@@ -198,3 +198,19 @@ def test_armed_engine_freezes_the_pool(tg):
 def torch_sync():
     import torch
     torch.cuda.synchronize()
+
+
+def test_destroying_an_armed_engine_releases_the_pool(tg):
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=50_000), device=0)
+    st = tg.ModelStatsTable()
+    kv = tg.KvEngine("s", BS, BPT)
+    assert kv.batch_allocate(pool, st, [(1, 20)]).ok()
+    assert kv.device_arm(pool, 16, 8, 4).ok()
+    from paper_2512_01357_b200 import _native as N
+    with pytest.raises(N.TangramRuntimeError):
+        pool.alloc_kv_region(800, 5)
+    del kv
+    import gc
+    gc.collect()
+    assert pool.alloc_kv_region(800, 5).ok()
+    pool.close()
