@@ -139,6 +139,8 @@ const char* tg_error_string(int code) {
         case TG_ERR_BUFFER: return "buffer too small";
         case TG_ERR_BAD_ARG: return "bad argument";
         case TG_ERR_VERIFY: return "fingerprint verification failed";
+        case TG_ERR_KV_ARMED: return "a KV engine is armed for device batches";
+        case TG_ERR_KV_LOG: return "device KV batch log overflowed";
         default: return "internal error";
     }
 }

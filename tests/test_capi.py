@@ -30,6 +30,21 @@ def test_version_and_errors(tg):
     assert N.lib.tg_error_string(1) == b"insufficient memory"
     assert N.lib.tg_error_string(10) == b"invalid argument"
     assert N.lib.tg_error_string(101) == b"no device"
+    assert N.lib.tg_error_string(107) == b"a KV engine is armed for device batches"
+
+
+def test_kv_device_path_needs_a_device(tg):
+    """K4D (device-decided KV batches) refuses control-plane-only pools."""
+    from paper_2512_01357_b200 import _native as N
+    import pytest
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=1 << 20), device=None)
+    st = tg.ModelStatsTable()
+    kv = tg.KvEngine("s", 8, 100)
+    assert kv.batch_allocate(pool, st, [(1, 20)]).ok()
+    assert kv.request_slot(1) == 0
+    with pytest.raises(N.TangramRuntimeError):
+        kv.device_arm(pool, 16, 8, 4)
+    assert pool.alloc_kv_region(800, 5).ok()  # not armed
 
 
 def test_data_plane_fails_loudly_without_device(tg):
