@@ -947,22 +947,39 @@ __device__ __forceinline__ u64 next_tile(unsigned long long* counter, u32 lane) 
     return __shfl_sync(0xffffffffu, t, 0);
 }
 
-// The load kernel keeps four stage slots per warp: stage s - 1 (still read
-// by the line stores), stage s, and two stages in flight.  Six warps per CTA
-// keep two CTAs (2 x 108 KiB) resident per SM.
-constexpr int kCopyStages = 4;
-constexpr int kCopyWarps = 6;
-constexpr int kCopyWarpWords = kCopyStages * kV3StageWords;
-constexpr int kCopySmemBytes = kCopyWarps * kCopyWarpWords * 16;
+// Stage ring of the load kernel: four slots per warp, six warps per CTA, two
+// CTAs (2 x 108 KiB) per SM.
+//  * Tasks that write (kPair): the stores of stages s - 1 and s go out
+//    together at odd s, so each leaf receives 256 contiguous bytes at a time.
+//    With single 128-byte lines 4 KiB apart DRAM write efficiency drops
+//    (B200, plain register copies: 4.94 TB/s r+w for 128-byte pieces, 5.87
+//    for 256-byte pieces, 6.0 contiguous — tools/store_pattern.cu).  A line
+//    of stage s reads stage s and the last words of stage s - 1, so a pair at
+//    odd s reads s - 2 .. s and one stage is in flight.
+//  * Fingerprint-only launches (K1), or TANGRAM_LOAD_RING=single: one line per
+//    stage; a line reads s - 1 and s, and two stages are in flight.
+template <int STAGES, int WARPS, bool PAIR>
+struct CopyCfg {
+    static constexpr int kStages = STAGES;
+    static constexpr int kWarps = WARPS;
+    static constexpr bool kPair = PAIR;
+    static constexpr int kAhead = STAGES - 1 - (PAIR ? 1 : 0);  // stages in flight + 1
+    static constexpr int kWarpWords = STAGES * kV3StageWords;
+    static constexpr int kSmemBytes = WARPS * kWarpWords * 16;
+};
+using CfgSingle = CopyCfg<4, 6, false>;
+using CfgPair = CopyCfg<4, 6, true>;
 
-template <class Task>
-__global__ void __launch_bounds__(kCopyWarps * 32, 2)
+template <class Task, class Cfg>
+__global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
     copy_fp_kernel(const Task* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums,
                    unsigned long long* __restrict__ sync, const u64* __restrict__ need) {
+    constexpr int kStagesRing = Cfg::kStages;
+    constexpr int kAhead = Cfg::kAhead;
     extern __shared__ uint4 smem[];
     const u32 lane = threadIdx.x & 31;
     const u32 wid = threadIdx.x >> 5;
-    uint4* wbuf = smem + wid * kCopyWarpWords;
+    uint4* wbuf = smem + wid * Cfg::kWarpWords;
     CopyTileRef cur = copy_tile_ref(tasks, n_tasks, next_tile(sync, lane), total_tiles, 0u, lane);
     if (cur.t.task < 0) return;
     CopyTileRef nxt = copy_tile_ref(tasks, n_tasks, next_tile(sync, lane), total_tiles, static_cast<u32>(cur.t.task),
@@ -970,7 +987,6 @@ __global__ void __launch_bounds__(kCopyWarps * 32, 2)
     int cur_task = -1;
     u64 acc_h = 0, acc_l = 0;
     u32 buf = 0;
-    constexpr int kAhead = kCopyStages - 1;
 #pragma unroll
     for (int s = 0; s < kAhead; ++s) copy_issue(wbuf + s * kV3StageWords, cur, s, lane);
     while (cur.t.task >= 0) {
@@ -995,23 +1011,32 @@ __global__ void __launch_bounds__(kCopyWarps * 32, 2)
         }
         const u64 my_leaf = cur.t.leaf0 + lane;
         mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
-        // The line stores of stage s also read stage s - 1, so the ring slot
-        // it occupies is refilled (with stage s + 3) only after them.
+        // The line stores of stage s also read stage s - 1 (pairs: s - 2 .. s),
+        // so the ring slot refilled with stage s + kAhead is the one no store
+        // reads any more: that of s - 1 (single lines) or s - 2 (pairs).
         for (int s = 0; s < kStagesPerLeaf; ++s) {
             cp_async_wait<kAhead - 1>();
             __syncwarp();
-            const u32 prev = (buf + kCopyStages - 1) % kCopyStages;
             const uint4* sb = wbuf + buf * kV3StageWords;
-            const uint4* sp = wbuf + prev * kV3StageWords;
-            if (writes && cur.t.nfull) write_lines_dispatch(sb, sp, cur, s, true, s > 0, lane);
+            const uint4* sp = wbuf + ((buf + kStagesRing - 1) % kStagesRing) * kV3StageWords;
+            if constexpr (Cfg::kPair) {
+                if ((s & 1) && writes && cur.t.nfull) {
+                    const uint4* spp = wbuf + ((buf + kStagesRing - 2) % kStagesRing) * kV3StageWords;
+                    write_lines_dispatch(sp, spp, cur, s - 1, true, s > 1, lane);
+                    write_lines_dispatch(sb, sp, cur, s, true, true, lane);
+                }
+            } else {
+                if (writes && cur.t.nfull) write_lines_dispatch(sb, sp, cur, s, true, s > 0, lane);
+            }
             if (s == kStagesPerLeaf - 1 && writes && cur.t.nfull && cur.k)
                 write_lines_dispatch(nullptr, sb, cur, kStagesPerLeaf, false, true, lane);
             if (lane < cur.t.nfull) v4_hash(sb, cur.t, lane, h1, h2);
             __syncwarp();
             const int ahead = s + kAhead;
-            if (ahead < kStagesPerLeaf) copy_issue(wbuf + prev * kV3StageWords, cur, ahead, lane);
-            else copy_issue(wbuf + prev * kV3StageWords, nxt, ahead - kStagesPerLeaf, lane);
-            buf = (buf + 1) % kCopyStages;
+            uint4* refill = wbuf + ((buf + kAhead) % kStagesRing) * kV3StageWords;
+            if (ahead < kStagesPerLeaf) copy_issue(refill, cur, ahead, lane);
+            else copy_issue(refill, nxt, ahead - kStagesPerLeaf, lane);
+            buf = (buf + 1) % kStagesRing;
         }
         if (lane < cur.t.nfull) {
             u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
@@ -1062,24 +1087,48 @@ __global__ void copy_fp_finalize_kernel(const CopyFpTask* __restrict__ tasks, u3
 
 }  // namespace
 
-std::uint64_t copy_fp_resident_warps(int sm_count) { return static_cast<u64>(sm_count) * 2 * kCopyWarps; }
+// Load-kernel configuration of launches with writing tasks (TANGRAM_LOAD_RING
+// = "single" selects the four-slot single-line ring for A/B runs).
+// Writing launches use the paired-store ring unless TANGRAM_LOAD_RING=single
+// (A/B runs).
+static bool pair_ring() {
+    static const bool pair = [] {
+        const char* e = std::getenv("TANGRAM_LOAD_RING");
+        return !(e && std::strcmp(e, "single") == 0);
+    }();
+    return pair;
+}
+
+std::uint64_t copy_fp_resident_warps(int sm_count) { return static_cast<u64>(sm_count) * 2 * CfgPair::kWarps; }
 
 namespace {
-template <class Task>
-void load_kernel_launch(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_sync,
-                        const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed) {
+template <class Task, class Cfg>
+void load_kernel_launch_cfg(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_sync,
+                            const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed) {
     static const bool attr = [] {
-        return cudaFuncSetAttribute(copy_fp_kernel<Task>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kCopySmemBytes) == cudaSuccess;
+        return cudaFuncSetAttribute(copy_fp_kernel<Task, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    Cfg::kSmemBytes) == cudaSuccess;
     }();
     (void)attr;
     if (!sync_zeroed) cudaMemsetAsync(d_sync, 0, (1 + n_waves) * sizeof(u64), s);
-    const u64 want = (total_tiles + kCopyWarps - 1) / kCopyWarps;
+    const u64 want = (total_tiles + Cfg::kWarps - 1) / Cfg::kWarps;
     const u64 cap = static_cast<u64>(sm_count) * 2;
     const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
-    copy_fp_kernel<Task><<<blocks, kCopyWarps * 32, kCopySmemBytes, s>>>(
+    copy_fp_kernel<Task, Cfg><<<blocks, Cfg::kWarps * 32, Cfg::kSmemBytes, s>>>(
         d_tasks, n_tasks, total_tiles, d_sums, reinterpret_cast<unsigned long long*>(d_sync), d_need);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+template <class Task>
+void load_kernel_launch(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_sync,
+                        const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed,
+                        bool writes) {
+    if (writes && pair_ring())
+        load_kernel_launch_cfg<Task, CfgPair>(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves,
+                                              sm_count, s, sync_zeroed);
+    else
+        load_kernel_launch_cfg<Task, CfgSingle>(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves,
+                                                sm_count, s, sync_zeroed);
 }
 }  // namespace
 
@@ -1087,7 +1136,8 @@ void copy_fp_launch(const CopyFpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64
                     const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed) {
     if (n_tasks == 0) return;
     if (total_tiles > 0)
-        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves, sm_count, s, sync_zeroed);
+        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves, sm_count, s, sync_zeroed,
+                           /*writes=*/true);
     copy_fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
@@ -1109,7 +1159,8 @@ void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums,
     }();
     const bool v0 = variant == 0;
     if (total_tiles > 0 && variant == 6) {
-        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, nullptr, 0, sm_count, s, sync_zeroed);
+        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, nullptr, 0, sm_count, s, sync_zeroed,
+                           /*writes=*/false);
     } else if (total_tiles > 0 && variant == 4) {
         static const bool attr = [] {
             return cudaFuncSetAttribute(fp_v4_kernel<kV3Stages, kWarpsPerCta>,
@@ -1123,15 +1174,15 @@ void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums,
             <<<blocks, kWarpsPerCta * 32, kV3SmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
     } else if (total_tiles > 0 && variant == 5) {
         static const bool attr = [] {
-            return cudaFuncSetAttribute(fp_v4_kernel<kCopyStages, kCopyWarps>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kCopySmemBytes) == cudaSuccess;
+            return cudaFuncSetAttribute(fp_v4_kernel<CfgSingle::kStages, CfgSingle::kWarps>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, CfgSingle::kSmemBytes) == cudaSuccess;
         }();
         (void)attr;
-        const u64 want = (total_tiles + kCopyWarps - 1) / kCopyWarps;
+        const u64 want = (total_tiles + CfgSingle::kWarps - 1) / CfgSingle::kWarps;
         const u64 cap = static_cast<u64>(sm_count) * 2;
         const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
-        fp_v4_kernel<kCopyStages, kCopyWarps>
-            <<<blocks, kCopyWarps * 32, kCopySmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
+        fp_v4_kernel<CfgSingle::kStages, CfgSingle::kWarps>
+            <<<blocks, CfgSingle::kWarps * 32, CfgSingle::kSmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
         g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
     } else if (total_tiles > 0 && variant == 3) {
         static const bool attr = [] {
