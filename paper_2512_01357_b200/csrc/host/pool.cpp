@@ -440,7 +440,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
         };
         static const u64 rounds = [] {
             const char* e = std::getenv("TANGRAM_VERIFY_ROUNDS");  // A/B knob
-            return e ? std::strtoull(e, nullptr, 10) : 2ull;
+            return e ? std::strtoull(e, nullptr, 10) : 8ull;
         }();
         const u64 share = rounds * copy_fp_resident_warps(sm_count_);
         const std::size_t n_verify = fp_reuse ? n_still : 0;
