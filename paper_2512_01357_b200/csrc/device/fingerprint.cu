@@ -955,7 +955,8 @@ __device__ __forceinline__ u64 next_tile(unsigned long long* counter, u32 lane) 
 //    (B200, plain register copies: 4.94 TB/s r+w for 128-byte pieces, 5.87
 //    for 256-byte pieces, 6.0 contiguous — tools/store_pattern.cu).  A line
 //    of stage s reads stage s and the last words of stage s - 1, so a pair at
-//    odd s reads s - 2 .. s and one stage is in flight.
+//    odd s reads s - 2 .. s; after it both s - 2 and s - 1 are refilled, so
+//    two or three stages are in flight.
 //  * Fingerprint-only launches (K1), or TANGRAM_LOAD_RING=single: one line per
 //    stage; a line reads s - 1 and s, and two stages are in flight.
 template <int STAGES, int WARPS, bool PAIR>
@@ -963,7 +964,7 @@ struct CopyCfg {
     static constexpr int kStages = STAGES;
     static constexpr int kWarps = WARPS;
     static constexpr bool kPair = PAIR;
-    static constexpr int kAhead = STAGES - 1 - (PAIR ? 1 : 0);  // stages in flight + 1
+    static constexpr int kAhead = STAGES - 1;  // single-line ring: stages in flight + 1
     static constexpr int kWarpWords = STAGES * kV3StageWords;
     static constexpr int kSmemBytes = WARPS * kWarpWords * 16;
 };
@@ -987,8 +988,9 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
     int cur_task = -1;
     u64 acc_h = 0, acc_l = 0;
     u32 buf = 0;
+    constexpr int kPrologue = Cfg::kPair ? 3 : kAhead;  // stages 0 .. kPrologue - 1 before the loop
 #pragma unroll
-    for (int s = 0; s < kAhead; ++s) copy_issue(wbuf + s * kV3StageWords, cur, s, lane);
+    for (int s = 0; s < kPrologue; ++s) copy_issue(wbuf + s * kV3StageWords, cur, s, lane);
     while (cur.t.task >= 0) {
         if (cur.t.task != cur_task) {
             if (cur_task >= 0) {
@@ -1014,28 +1016,46 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
         // The line stores of stage s also read stage s - 1 (pairs: s - 2 .. s),
         // so the ring slot refilled with stage s + kAhead is the one no store
         // reads any more: that of s - 1 (single lines) or s - 2 (pairs).
+        auto issue = [&](int stage, int slot) {
+            uint4* dst = wbuf + slot * kV3StageWords;
+            if (stage < kStagesPerLeaf) copy_issue(dst, cur, stage, lane);
+            else copy_issue(dst, nxt, stage - kStagesPerLeaf, lane);
+        };
         for (int s = 0; s < kStagesPerLeaf; ++s) {
-            cp_async_wait<kAhead - 1>();
-            __syncwarp();
             const uint4* sb = wbuf + buf * kV3StageWords;
-            const uint4* sp = wbuf + ((buf + kStagesRing - 1) % kStagesRing) * kV3StageWords;
+            const u32 b1 = (buf + kStagesRing - 1) % kStagesRing, b2 = (buf + kStagesRing - 2) % kStagesRing;
+            const uint4* sp = wbuf + b1 * kV3StageWords;
             if constexpr (Cfg::kPair) {
-                if ((s & 1) && writes && cur.t.nfull) {
-                    const uint4* spp = wbuf + ((buf + kStagesRing - 2) % kStagesRing) * kV3StageWords;
-                    write_lines_dispatch(sp, spp, cur, s - 1, true, s > 1, lane);
-                    write_lines_dispatch(sb, sp, cur, s, true, true, lane);
+                // Ring schedule: at odd s the pair (s - 1, s) is stored and
+                // both of its older slots (s - 2, s - 1) are refilled at once
+                // with s + 2 and s + 3; at even s nothing is refilled.  Stages
+                // up to s + 2 (even s) or s + 1 (odd s) have been issued.
+                if (s & 1) cp_async_wait<1>();
+                else cp_async_wait<2>();
+                __syncwarp();
+                if (s & 1) {
+                    if (writes && cur.t.nfull) {
+                        const uint4* spp = wbuf + b2 * kV3StageWords;
+                        write_lines_dispatch(sp, spp, cur, s - 1, true, s > 1, lane);
+                        write_lines_dispatch(sb, sp, cur, s, true, true, lane);
+                        if (s == kStagesPerLeaf - 1 && cur.k)
+                            write_lines_dispatch(nullptr, sb, cur, kStagesPerLeaf, false, true, lane);
+                    }
+                    __syncwarp();
+                    issue(s + 2, static_cast<int>(b2));
+                    issue(s + 3, static_cast<int>(b1));
                 }
+                if (lane < cur.t.nfull) v4_hash(sb, cur.t, lane, h1, h2);
             } else {
+                cp_async_wait<kAhead - 1>();
+                __syncwarp();
                 if (writes && cur.t.nfull) write_lines_dispatch(sb, sp, cur, s, true, s > 0, lane);
+                if (s == kStagesPerLeaf - 1 && writes && cur.t.nfull && cur.k)
+                    write_lines_dispatch(nullptr, sb, cur, kStagesPerLeaf, false, true, lane);
+                if (lane < cur.t.nfull) v4_hash(sb, cur.t, lane, h1, h2);
+                __syncwarp();
+                issue(s + kAhead, static_cast<int>((buf + kAhead) % kStagesRing));
             }
-            if (s == kStagesPerLeaf - 1 && writes && cur.t.nfull && cur.k)
-                write_lines_dispatch(nullptr, sb, cur, kStagesPerLeaf, false, true, lane);
-            if (lane < cur.t.nfull) v4_hash(sb, cur.t, lane, h1, h2);
-            __syncwarp();
-            const int ahead = s + kAhead;
-            uint4* refill = wbuf + ((buf + kAhead) % kStagesRing) * kV3StageWords;
-            if (ahead < kStagesPerLeaf) copy_issue(refill, cur, ahead, lane);
-            else copy_issue(refill, nxt, ahead - kStagesPerLeaf, lane);
             buf = (buf + 1) % kStagesRing;
         }
         if (lane < cur.t.nfull) {
