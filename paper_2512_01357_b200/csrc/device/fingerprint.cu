@@ -53,6 +53,36 @@ __device__ __forceinline__ void hash_blocks_aligned(const uint4* __restrict__ wp
     }
 }
 
+// leaf_digest over a generic (shared-memory) pointer: plain loads, 4-byte
+// words funnel-shifted into blocks.
+__device__ void leaf_digest_generic(const std::uint8_t* p, u32 len, u64 seed, u64& d1, u64& d2) {
+    mm::W32 h1 = mm::w_of(seed), h2 = h1;
+    const u32 nblk = len >> 4;
+    const u32 o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p) & 3);
+    const u32* wp = reinterpret_cast<const u32*>(p - o);
+    const u32 r8 = o * 8;
+    for (u32 j = 0; j < nblk; ++j) {
+        u32 u[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) u[q] = (q < 4 || o) ? wp[4 * j + q] : 0u;
+        const u32 a = __funnelshift_r(u[0], u[1], r8), b = __funnelshift_r(u[1], u[2], r8);
+        const u32 c = __funnelshift_r(u[2], u[3], r8), d = __funnelshift_r(u[3], u[4], r8);
+        mm::body_dev(h1, h2, mm::W32{a, b}, mm::W32{c, d});
+    }
+    const u32 rem = len & 15;
+    u64 t1 = 0, t2 = 0;
+    const std::uint8_t* tp = p + (static_cast<u64>(nblk) << 4);
+    for (u32 b = 0; b < rem; ++b) {
+        const u64 v = tp[b];
+        if (b < 8) t1 |= v << (8 * b);
+        else t2 |= v << (8 * (b - 8));
+    }
+    u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
+    mm::finish(f1, f2, t1, t2, rem, len);
+    d1 = f1;
+    d2 = f2;
+}
+
 // murmur3_x64_128(p[0..len), seed) for len <= 4096.
 __device__ void leaf_digest(const std::uint8_t* p, u32 len, u64 seed, u64& d1, u64& d2) {
     mm::W32 h1 = mm::w_of(seed), h2 = h1;
@@ -1063,18 +1093,38 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
             mm::finish(f1, f2, 0, 0, 0, kLeafBytes);
             acc_h += f1;
             acc_l += f2;
-        } else if (lane == cur.t.nfull && my_leaf * kLeafBytes < cur.t.n) {
-            const u32 len = static_cast<u32>(cur.t.n - my_leaf * kLeafBytes);
-            u64 d1, d2;
-            leaf_digest(cur.t.base + my_leaf * kLeafBytes, len, my_leaf, d1, d2);
-            acc_h += d1;
-            acc_l += d2;
         }
-        // the tensor's last tile also copies the head and tail bytes
-        if (writes && cur.t.leaf0 + 32 >= (cur.t.n + kLeafBytes - 1) / kLeafBytes) {
-            const std::uint8_t* src = cur.t.base;
-            for (u64 b = lane; b < cur.x_first && b < cur.t.n; b += 32) cur.dst[b] = src[b];
-            for (u64 b = cur.x_end + lane; b < cur.t.n; b += 32) cur.dst[b] = src[b];
+        // The tensor's last tile: the partial leaf (< 4 KiB) and, for moves,
+        // the bytes no full word covers (head < 16 B; tail = [x_end, n)).
+        // The warp stages [from, n) in the ring slot stage 31 just released
+        // (one round of coalesced loads), then hashes the partial leaf and
+        // copies the tail from shared memory — a per-byte global loop here
+        // costs tens of microseconds of DRAM latency at the end of a launch.
+        if (cur.t.leaf0 + 32 >= (cur.t.n + kLeafBytes - 1) / kLeafBytes) {
+            const u64 pl = (cur.t.n / kLeafBytes) * kLeafBytes;  // partial leaf start
+            const u64 from = writes ? min(cur.x_end, pl) : pl;
+            if (from < cur.t.n) {
+                __syncwarp();
+                uint4* tb = wbuf + ((buf + kStagesRing - 1) % kStagesRing) * kV3StageWords;
+                const std::uint8_t* g0 = cur.t.base + from;
+                const u32 ga = static_cast<u32>(reinterpret_cast<std::uintptr_t>(g0) & 15);
+                const uint4* gw = reinterpret_cast<const uint4*>(g0 - ga);
+                const u32 nw = static_cast<u32>((ga + (cur.t.n - from) + 15) / 16);
+                for (u32 w = lane; w < nw; w += 32) tb[w] = __ldg(gw + w);
+                __syncwarp();
+                const std::uint8_t* sbytes = reinterpret_cast<const std::uint8_t*>(tb) + ga;
+                if (lane == cur.t.nfull && pl < cur.t.n) {
+                    u64 d1, d2;
+                    leaf_digest_generic(sbytes + (pl - from), static_cast<u32>(cur.t.n - pl), pl / kLeafBytes, d1, d2);
+                    acc_h += d1;
+                    acc_l += d2;
+                }
+                if (writes)
+                    for (u64 b = lane; b < cur.t.n - from; b += 32) cur.dst[from + b] = sbytes[b];
+                __syncwarp();
+            }
+            if (writes)
+                for (u64 b = lane; b < cur.x_first && b < cur.t.n; b += 32) cur.dst[b] = cur.t.base[b];
         }
         if (cur.wave >= 0) {  // this tile's source bytes are all read
             __syncwarp();
