@@ -287,6 +287,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     std::vector<const std::uint8_t*> peer_src(np, nullptr);
     std::vector<Digest> peer_digest(np);  // what the peer's index says the bytes fingerprint to
     std::vector<std::vector<MoveDesc>> pieces(np);  // re-shard pulls: src, dst offset in the tensor, len
+    std::vector<u64> local_piece_bytes(np, 0);       // ... of which sourced from this pool (HBM)
     rep->placement_src.assign(np, 0);
     if (has_device()) {
         for (std::size_t i = 0; i < np; ++i) {
@@ -310,7 +311,8 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
                     }
                 }
             }
-            if (!peer_src[i] && (flags & kLoadPeer) && assemble_shard(t, &pieces[i])) rep->placement_src[i] = 3;
+            if (!peer_src[i] && (flags & kLoadPeer) && assemble_shard(t, &pieces[i], &d.plan, &local_piece_bytes[i]))
+                rep->placement_src[i] = 3;
             if (peer_src[i] || rep->placement_src[i] == 3) continue;
             if (!SourceRegistry::get().find(t.id, &src[i]) || src[i].size != t.size)
                 throw DeviceError(kErrNoSource, "no host source registered for tensor " + t.id.hex() + " (" +
@@ -366,7 +368,12 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     for (std::size_t i = 0; i < np; ++i) {
         const u64 sz = D.miss_desc[D.plan.placements[i].tensor].size;
         const std::uint8_t k = rep->placement_src[i];
-        (k == 0 ? rep->pcie_bytes : (k == 1 || k == 3) ? rep->peer_bytes : rep->device_src_bytes) += sz;
+        if (k == 3) {  // re-shard pieces: NVLink from peers, HBM from this pool
+            rep->peer_bytes += sz - local_piece_bytes[i];
+            rep->device_src_bytes += local_piece_bytes[i];
+            continue;
+        }
+        (k == 0 ? rep->pcie_bytes : k == 1 ? rep->peer_bytes : rep->device_src_bytes) += sz;
     }
 
     // ---- event layout -----------------------------------------------------------
@@ -699,44 +706,65 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
 }
 
 // Re-shard pull: cover tensor t's parent byte range with resident shards of
-// the same parent on peer pools (any TP layout); pieces hold the peer source,
-// the destination offset inside t, and the length.
-bool Pool::assemble_shard(const TensorDesc& t, std::vector<MoveDesc>* pieces) const {
+// the same parent in any TP layout — on peer pools, and (when `plan` is given)
+// in this pool itself, where a shard this load neither evicts nor relocates
+// keeps its bytes in place for the whole load (placements only fill free
+// space).  Local pieces are preferred (HBM, not NVLink).  Pieces hold the
+// source, the destination offset inside t, and the length; *local_bytes
+// counts the bytes sourced from this pool.
+bool Pool::assemble_shard(const TensorDesc& t, std::vector<MoveDesc>* pieces, const Plan* plan,
+                          u64* local_bytes) const {
     ShardOf me;
     if (!ShardLineage::get().find(t.id, &me) || me.size != t.size || t.size == 0) return false;
     struct Cand {
         u64 b, e;
         const std::uint8_t* base;
+        bool local;
     };
+    std::unordered_map<Key, bool, KeyHash> touched;  // evicted or relocated by this load
+    if (plan) {
+        for (const Candidate& c : plan->evictions) touched[c.tensor] = true;
+        for (const Move& m : plan->relocations) touched[m.tensor] = true;
+    }
     std::vector<Cand> cands;
     for (const auto& [kid, of] : ShardLineage::get().children(me.parent)) {
         if (kid == t.id || of.begin >= me.begin + me.size || of.begin + of.size <= me.begin) continue;
         const std::uint8_t* base = nullptr;
-        for (Pool* p : peers_) {
-            const Entry* e = p->store_.entry(kid);
-            if (e && e->size == of.size && e->has_digest) {
-                base = p->arena_ + e->off;
-                break;
+        bool local = false;
+        if (plan && !touched.count(kid)) {
+            const auto it = store_.tensors().find(kid);
+            if (it != store_.tensors().end() && it->second.size == of.size && it->second.has_digest) {
+                base = arena_ + it->second.off;
+                local = true;
             }
+        }
+        for (std::size_t k = 0; !base && k < peers_.size(); ++k) {
+            const Entry* e = peers_[k]->store_.entry(kid);
+            if (e && e->size == of.size && e->has_digest) base = peers_[k]->arena_ + e->off;
         }
         for (std::size_t r = 0; !base && r < remotes_.size(); ++r) {
             auto it = remotes_[r].index.find(kid);
             if (it != remotes_[r].index.end() && it->second.size == of.size) base = remotes_[r].base + it->second.off;
         }
-        if (base) cands.push_back(Cand{of.begin, of.begin + of.size, base});
+        if (base) cands.push_back(Cand{of.begin, of.begin + of.size, base, local});
     }
     std::vector<MoveDesc> out;
+    u64 local = 0;
     const u64 end = me.begin + me.size;
     for (u64 pos = me.begin; pos < end;) {
         const Cand* best = nullptr;
         for (const Cand& c : cands)
-            if (c.b <= pos && pos < c.e && (!best || c.e > best->e)) best = &c;
+            if (c.b <= pos && pos < c.e &&
+                (!best || (c.local && !best->local) || (c.local == best->local && c.e > best->e)))
+                best = &c;
         if (!best) return false;
         const u64 len = std::min(best->e, end) - pos;
         out.push_back(MoveDesc{reinterpret_cast<u64>(best->base + (pos - best->b)), pos - me.begin, len});
+        if (best->local) local += len;
         pos += len;
     }
     *pieces = std::move(out);
+    if (local_bytes) *local_bytes = local;
     return true;
 }
 
@@ -799,7 +827,7 @@ u64 Pool::peer_reuse_size(const ModelDesc& m) const {
         for (const RemotePeer& r : remotes_)
             if (!found && r.index.count(t.id)) found = true;
         std::vector<MoveDesc> pieces;  // or assembled from peer shards of another layout
-        if (found || (has_device() && assemble_shard(t, &pieces))) s += t.size;
+        if (found || (has_device() && assemble_shard(t, &pieces, nullptr, nullptr))) s += t.size;
     }
     return s;
 }

@@ -210,7 +210,7 @@ private:
     std::uint8_t* arena_ = nullptr;
     cudaStream_t s_main_ = nullptr, s_copy_ = nullptr, s_fp_ = nullptr, s_peer_ = nullptr, s_verify_ = nullptr;
     std::vector<cudaEvent_t> events_;
-    bool assemble_shard(const TensorDesc& t, std::vector<MoveDesc>* pieces) const;
+    bool assemble_shard(const TensorDesc& t, std::vector<MoveDesc>* pieces, const Plan* plan, u64* local_bytes) const;
     std::vector<Pool*> peers_;
     struct RemotePeer {
         std::uint8_t* base = nullptr;  // IPC-mapped peer arena

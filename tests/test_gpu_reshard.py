@@ -85,3 +85,40 @@ def test_reshard_needs_full_cover(tg):
     assert c.dump() == before
     a.close()
     c.close()
+
+
+def test_reshard_from_own_pool(tg, cpu, ref):
+    """One GPU switching TP layout: the TP4 shards are assembled from the
+    pool's own resident TP2 shards (device-to-device in HBM), which this load
+    neither evicts nor relocates; decisions and dumps equal the reference's."""
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    m = tg.make_model("reshard-self", 30_000_017, 2, 8192)
+    tp2 = [tg.shard_model(m, r, 2) for r in range(2)]
+    tp4 = [tg.shard_model(m, r, 4) for r in range(4)]
+    size = 70_000_000
+    c = tg.ReuseStore(tg.GpuSpec("gpu0", size), device=0)
+    r_pool, r_stats, sc = ref.ReuseStore(size), ref.ModelStatsTable(), tg.ModelStatsTable()
+    t = 0.0
+    with HostCheckpoint(tp2):
+        for sh in tp2:
+            sc.record_request(sh.model_id, t)
+            c.load_model(sh, sc, t).value()
+            c.end_instance(sh.model_id)
+            r_stats.record_request(sh.model_id, t)
+            r_pool.load_model(sh.to_json(), r_stats, t)
+            r_pool.end_instance(sh.model_id)
+            t += 1.0
+    for sh in tp4[:2]:
+        sc.record_request(sh.model_id, t)
+        o = c.load_model(sh, sc, t, tg.LoadPolicy(flags=1 | 2 | 4 | 8)).value()
+        assert all(p.source == 3 for p in o.plan.placements)
+        assert o.device_src_bytes == sh.total_size and o.peer_bytes == 0 and o.pcie_bytes == 0
+        for i, tt in enumerate(sh.tensors):
+            assert o.digests[i] == _expected(cpu, tg, tt)
+        c.end_instance(sh.model_id)
+        r_stats.record_request(sh.model_id, t)
+        r_pool.load_model(sh.to_json(), r_stats, t)
+        r_pool.end_instance(sh.model_id)
+        assert c.dump() == r_pool.dump()
+        t += 1.0
+    c.close()
