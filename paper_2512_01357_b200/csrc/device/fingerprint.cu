@@ -1,4 +1,4 @@
-// K1 — content fingerprint kernel (tgfp1), sm_100a.
+// K1 content fingerprint (tgfp1) and the load kernel, sm_100a.
 //
 // One lane hashes one 4 KiB leaf with MurmurHash3 x64-128 (seed = leaf
 // index, the reference's leaf function types.hpp:77-124); a warp owns a tile
@@ -10,7 +10,9 @@
 // Tensors sit at arbitrary byte offsets in the arena (catalog sizes are odd
 // byte counts), so every lane reads aligned 16-byte words and realigns them
 // in registers with funnel shifts; the shift is uniform per tensor, hence
-// per warp, and selects one of four unrolled bodies.
+// per warp, and selects one of four unrolled bodies.  The same kernel moves
+// bytes (relocations, device-source placements) and fingerprints them from
+// the move's own read: the load kernel below.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -24,34 +26,6 @@ namespace {
 
 using u64 = std::uint64_t;
 using u32 = std::uint32_t;
-
-__device__ __forceinline__ u64 pack64(u32 lo, u32 hi) { return (static_cast<u64>(hi) << 32) | lo; }
-
-// Hash `nblk` 16-byte blocks starting `4*Q + r8/8` bytes past the aligned
-// word pointer `wp`.
-template <int Q>
-__device__ __forceinline__ void hash_blocks(const uint4* __restrict__ wp, u32 nblk, u32 r8, mm::W32& h1, mm::W32& h2) {
-    uint4 w0 = __ldg(wp);
-#pragma unroll 4
-    for (u32 j = 0; j < nblk; ++j) {
-        const uint4 w1 = __ldg(wp + j + 1);
-        const u32 u[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-        const u32 a = __funnelshift_r(u[Q + 0], u[Q + 1], r8);
-        const u32 b = __funnelshift_r(u[Q + 1], u[Q + 2], r8);
-        const u32 c = __funnelshift_r(u[Q + 2], u[Q + 3], r8);
-        const u32 d = __funnelshift_r(u[Q + 3], u[Q + 4], r8);
-        mm::body_dev(h1, h2, mm::W32{a, b}, mm::W32{c, d});
-        w0 = w1;
-    }
-}
-
-__device__ __forceinline__ void hash_blocks_aligned(const uint4* __restrict__ wp, u32 nblk, mm::W32& h1, mm::W32& h2) {
-#pragma unroll 4
-    for (u32 j = 0; j < nblk; ++j) {
-        const uint4 w = __ldg(wp + j);
-        mm::body_dev(h1, h2, mm::W32{w.x, w.y}, mm::W32{w.z, w.w});
-    }
-}
 
 // leaf_digest over a generic (shared-memory) pointer: plain loads, 4-byte
 // words funnel-shifted into blocks.
@@ -83,108 +57,21 @@ __device__ void leaf_digest_generic(const std::uint8_t* p, u32 len, u64 seed, u6
     d2 = f2;
 }
 
-// murmur3_x64_128(p[0..len), seed) for len <= 4096.
-__device__ void leaf_digest(const std::uint8_t* p, u32 len, u64 seed, u64& d1, u64& d2) {
-    mm::W32 h1 = mm::w_of(seed), h2 = h1;
-    const u32 nblk = len >> 4;
-    const u32 o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p) & 15);
-    const uint4* wp = reinterpret_cast<const uint4*>(p - o);
-    if (nblk) {
-        const u32 r8 = (o & 3) * 8;
-        switch (o >> 2) {
-            case 0:
-                if (o == 0) hash_blocks_aligned(wp, nblk, h1, h2);
-                else hash_blocks<0>(wp, nblk, r8, h1, h2);
-                break;
-            case 1: hash_blocks<1>(wp, nblk, r8, h1, h2); break;
-            case 2: hash_blocks<2>(wp, nblk, r8, h1, h2); break;
-            default: hash_blocks<3>(wp, nblk, r8, h1, h2); break;
-        }
-    }
-    const u32 rem = len & 15;
-    u64 t1 = 0, t2 = 0;
-    const std::uint8_t* tp = p + (static_cast<u64>(nblk) << 4);
-    for (u32 b = 0; b < rem; ++b) {
-        const u64 v = tp[b];
-        if (b < 8) t1 |= v << (8 * b);
-        else t2 |= v << (8 * (b - 8));
-    }
-    u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
-    mm::finish(f1, f2, t1, t2, rem, len);
-    d1 = f1;
-    d2 = f2;
-}
-
 __device__ __forceinline__ u64 warp_sum(u64 v) {
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
     return v;
 }
 
-__global__ void __launch_bounds__(256) fp_leaves_kernel(const FpTask* __restrict__ tasks, u32 n_tasks,
-                                                        u64 total_tiles, u64* __restrict__ sums) {
-    const u32 lane = threadIdx.x & 31;
-    const u64 warp = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const u64 nwarps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
-    int cur = -1;
-    u64 acc_h = 0, acc_l = 0;
-    for (u64 t = warp; t < total_tiles; t += nwarps) {
-        // task owning tile t: last i with tasks[i].tile0 <= t
-        u32 lo = 0, hi = n_tasks - 1;
-        while (lo < hi) {
-            const u32 mid = (lo + hi + 1) >> 1;
-            if (tasks[mid].tile0 <= t) lo = mid;
-            else hi = mid - 1;
-        }
-        const int ti = static_cast<int>(lo);
-        if (ti != cur) {
-            if (cur >= 0) {
-                const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
-                if (lane == 0) {
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
-                }
-            }
-            cur = ti;
-            acc_h = acc_l = 0;
-        }
-        const FpTask tk = tasks[ti];
-        const u64 leaf = (t - tk.tile0) * kLeavesPerTile + lane;
-        const u64 off = leaf * kLeafBytes;
-        if (off < tk.n) {
-            const u64 rest = tk.n - off;
-            const u32 len = rest < kLeafBytes ? static_cast<u32>(rest) : static_cast<u32>(kLeafBytes);
-            u64 d1, d2;
-            leaf_digest(tk.base + off, len, leaf, d1, d2);
-            acc_h += d1;
-            acc_l += d2;
-        }
-    }
-    if (cur >= 0) {
-        const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
-        if (lane == 0) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
-            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
-        }
-    }
-}
-
-// ---- v1: shared-memory staged leaves ------------------------------------------
-// The v0 kernel above issues one 16-byte load per lane from 32 different 4 KiB
-// leaves, so every LDG touches 32 L1 lines and the L1 wavefront rate caps it
-// near 16 B/clk/SM.  v1 stages each warp's 32 leaves through shared memory
-// with cp.async: a stage is 8 blocks (128 B) + 1 realignment word per leaf,
-// copied with coalesced 16-byte LDGSTS (lanes walk the 9-word slots of
-// consecutive leaves), then every lane reads its own slot with conflict-free
-// LDS.128 (slot stride 9 words → 8 consecutive lanes hit 8 distinct bank
-// quads).  Three stages in flight per warp, 8 warps per CTA, 2 CTAs per SM.
+// ---- staging ---------------------------------------------------------------------
+// A stage is 8 blocks (128 B) of each of a warp's 32 leaves, copied into
+// shared memory with coalesced 16-byte cp.async (LDGSTS); every lane then
+// reads its own leaf's words with conflict-free LDS.128.  (Design history:
+// per-lane direct loads were L1-wavefront bound, per-lane TMA bulk copies
+// serialised on uniform operands.)
 constexpr int kStageBlocks = 8;
 constexpr int kSlotWords = kStageBlocks + 1;
-constexpr int kStages = 3;
 constexpr int kStagesPerLeaf = static_cast<int>(kLeafBytes / 16) / kStageBlocks;  // 32
-constexpr int kWarpsPerCta = 8;
-constexpr int kWarpSmemWords = kStages * 32 * kSlotWords;
-constexpr int kSmemBytes = kWarpsPerCta * kWarpSmemWords * 16;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -207,307 +94,13 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Stage `s` of the tile's full leaves: words [8s, 8s+9) of every leaf's
-// aligned window (the 9th only when the data is misaligned, so it always
-// holds at least one byte of the leaf).
-__device__ __forceinline__ void issue_stage(uint4* buf, const std::uint8_t* a0, u32 nfull, bool extra, int s,
-                                            u32 lane) {
-#pragma unroll
-    for (int i = 0; i < kSlotWords; ++i) {
-        const u32 f = i * 32 + lane;
-        const u32 l = f / kSlotWords, q = f % kSlotWords;
-        if (l < nfull && (q < kStageBlocks || extra))
-            cp_async16(buf + l * kSlotWords + q, a0 + static_cast<u64>(l) * kLeafBytes + s * 128 + q * 16);
-    }
-    cp_async_commit();
-}
-
-template <int Q>
-__device__ __forceinline__ void hash_stage(const uint4* slot, u32 r8, mm::W32& h1, mm::W32& h2) {
-    uint4 w[kSlotWords];
-#pragma unroll
-    for (int q = 0; q < kSlotWords; ++q) w[q] = slot[q];
-#pragma unroll
-    for (int b = 0; b < kStageBlocks; ++b) {
-        const u32 u[8] = {w[b].x, w[b].y, w[b].z, w[b].w, w[b + 1].x, w[b + 1].y, w[b + 1].z, w[b + 1].w};
-        const u32 a = __funnelshift_r(u[Q + 0], u[Q + 1], r8);
-        const u32 c = __funnelshift_r(u[Q + 1], u[Q + 2], r8);
-        const u32 d = __funnelshift_r(u[Q + 2], u[Q + 3], r8);
-        const u32 e = __funnelshift_r(u[Q + 3], u[Q + 4], r8);
-        mm::body_dev(h1, h2, mm::W32{a, c}, mm::W32{d, e});
-    }
-}
-
-template <int Q>
-__device__ __forceinline__ void hash_full_leaves(uint4* wbuf, const std::uint8_t* a0, u32 nfull, bool extra, u32 r8,
-                                                 u32 lane, mm::W32& h1, mm::W32& h2) {
-    constexpr int kStride = 32 * kSlotWords;
-#pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) issue_stage(wbuf + s * kStride, a0, nfull, extra, s, lane);
-    for (int s = 0; s < kStagesPerLeaf; ++s) {
-        const int nxt = s + kStages - 1;
-        if (nxt < kStagesPerLeaf) issue_stage(wbuf + (nxt % kStages) * kStride, a0, nfull, extra, nxt, lane);
-        else cp_async_commit();
-        cp_async_wait<kStages - 1>();
-        __syncwarp();
-        if (lane < nfull) hash_stage<Q>(wbuf + (s % kStages) * kStride + lane * kSlotWords, r8, h1, h2);
-        __syncwarp();
-    }
-}
-
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
-    fp_smem_kernel(const FpTask* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums) {
-    extern __shared__ uint4 smem[];
-    const u32 lane = threadIdx.x & 31;
-    const u32 wid = threadIdx.x >> 5;
-    uint4* wbuf = smem + wid * kWarpSmemWords;
-    const u64 nwarps = static_cast<u64>(gridDim.x) * kWarpsPerCta;
-    int cur = -1;
-    u64 acc_h = 0, acc_l = 0;
-    for (u64 t = static_cast<u64>(blockIdx.x) * kWarpsPerCta + wid; t < total_tiles; t += nwarps) {
-        u32 lo = 0, hi = n_tasks - 1;
-        while (lo < hi) {
-            const u32 mid = (lo + hi + 1) >> 1;
-            if (tasks[mid].tile0 <= t) lo = mid;
-            else hi = mid - 1;
-        }
-        const int ti = static_cast<int>(lo);
-        if (ti != cur) {
-            if (cur >= 0) {
-                const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
-                if (lane == 0) {
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
-                }
-            }
-            cur = ti;
-            acc_h = acc_l = 0;
-        }
-        const FpTask tk = tasks[ti];
-        const u64 leaf0 = (t - tk.tile0) * kLeavesPerTile;
-        const u64 full_leaves = tk.n / kLeafBytes;
-        const u32 nfull = full_leaves > leaf0 ? static_cast<u32>(min(full_leaves - leaf0, u64{32})) : 0u;
-        const std::uint8_t* p0 = tk.base + leaf0 * kLeafBytes;
-        const u32 o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p0) & 15);
-        const std::uint8_t* a0 = p0 - o;
-        const u64 my_leaf = leaf0 + lane;
-        mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
-        if (nfull) {
-            const u32 r8 = (o & 3) * 8;
-            const bool extra = o != 0;
-            switch (o >> 2) {
-                case 0: hash_full_leaves<0>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
-                case 1: hash_full_leaves<1>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
-                case 2: hash_full_leaves<2>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
-                default: hash_full_leaves<3>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
-            }
-        }
-        if (lane < nfull) {
-            u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
-            mm::finish(f1, f2, 0, 0, 0, kLeafBytes);
-            acc_h += f1;
-            acc_l += f2;
-        } else if (lane == nfull && my_leaf * kLeafBytes < tk.n) {
-            // the tensor's trailing partial leaf, hashed straight from global
-            const u32 len = static_cast<u32>(tk.n - my_leaf * kLeafBytes);
-            u64 d1, d2;
-            leaf_digest(tk.base + my_leaf * kLeafBytes, len, my_leaf, d1, d2);
-            acc_h += d1;
-            acc_l += d2;
-        }
-    }
-    if (cur >= 0) {
-        const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
-        if (lane == 0) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
-            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
-        }
-    }
-}
-
-// ---- v2: TMA bulk-copy staged leaves ------------------------------------------
-// Same smem layout as v1, but each lane stages its own leaf's 144-byte window
-// with ONE cp.async.bulk (TMA) per stage, completing on a per-warp, per-stage
-// mbarrier.  v1 spent ~25 of its ~64 instructions per 16-byte block on
-// LDGSTS address arithmetic (f/9, f%9, 64-bit adds, predicates); here the
-// producer side costs ~1 instruction per block and the kernel is left with
-// the hash itself.
-constexpr int kTmaStages = 3;
-constexpr int kTmaWarpWords = kTmaStages * 32 * kSlotWords;
-constexpr int kTmaSmemBytes = kWarpsPerCta * (kTmaWarpWords * 16 + kTmaStages * 8);
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void tma_stage(unsigned slot_smem, const std::uint8_t* src, unsigned bytes,
-                                          unsigned bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(slot_smem),
-        "l"(src), "r"(bytes), "r"(bar)
-        : "memory");
-}
-
-__device__ __forceinline__ void bar_expect(unsigned bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void bar_wait(unsigned bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-
-template <int Q>
-__device__ __forceinline__ void hash_full_leaves_tma(uint4* wbuf, unsigned bars, unsigned* phase,
-                                                     const std::uint8_t* a0, u32 nfull, bool extra, u32 r8, u32 lane,
-                                                     mm::W32& h1, mm::W32& h2) {
-    constexpr int kStride = 32 * kSlotWords;  // words per stage buffer
-    const unsigned per_leaf = extra ? 144u : 128u;
-    const unsigned stage_bytes = per_leaf * nfull;
-    const unsigned my_slot = smem_u32(wbuf + lane * kSlotWords);
-    const std::uint8_t* my_src = a0 + static_cast<u64>(lane) * kLeafBytes;
-    auto issue = [&](int s) {
-        const int b = s % kTmaStages;
-        const unsigned bar = bars + 8u * b;
-        if (lane == 0) bar_expect(bar, stage_bytes);
-        __syncwarp();
-        if (lane < nfull) tma_stage(my_slot + b * kStride * 16, my_src + s * 128, per_leaf, bar);
-    };
-#pragma unroll
-    for (int s = 0; s < kTmaStages - 1; ++s) issue(s);
-    for (int s = 0; s < kStagesPerLeaf; ++s) {
-        const int nxt = s + kTmaStages - 1;
-        if (nxt < kStagesPerLeaf) issue(nxt);
-        const int b = s % kTmaStages;
-        bar_wait(bars + 8u * b, (*phase >> b) & 1u);
-        *phase ^= 1u << b;
-        if (lane < nfull) hash_stage<Q>(wbuf + b * kStride + lane * kSlotWords, r8, h1, h2);
-        // the slot is refilled by the async proxy in a later stage: order our
-        // generic-proxy reads before it
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        __syncwarp();
-    }
-}
-
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
-    fp_tma_kernel(const FpTask* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums) {
-    extern __shared__ __align__(128) uint4 smem[];
-    const u32 lane = threadIdx.x & 31;
-    const u32 wid = threadIdx.x >> 5;
-    uint4* wbuf = smem + wid * kTmaWarpWords;
-    auto* bar_base = reinterpret_cast<unsigned long long*>(smem + kWarpsPerCta * kTmaWarpWords) + wid * kTmaStages;
-    const unsigned bars = smem_u32(bar_base);
-    if (lane == 0) {
-        for (int b = 0; b < kTmaStages; ++b)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bars + 8u * b) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncwarp();
-    unsigned phase = 0;
-    const u64 nwarps = static_cast<u64>(gridDim.x) * kWarpsPerCta;
-    int cur = -1;
-    u64 acc_h = 0, acc_l = 0;
-    for (u64 t = static_cast<u64>(blockIdx.x) * kWarpsPerCta + wid; t < total_tiles; t += nwarps) {
-        u32 lo = 0, hi = n_tasks - 1;
-        while (lo < hi) {
-            const u32 mid = (lo + hi + 1) >> 1;
-            if (tasks[mid].tile0 <= t) lo = mid;
-            else hi = mid - 1;
-        }
-        const int ti = static_cast<int>(lo);
-        if (ti != cur) {
-            if (cur >= 0) {
-                const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
-                if (lane == 0) {
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
-                }
-            }
-            cur = ti;
-            acc_h = acc_l = 0;
-        }
-        const FpTask tk = tasks[ti];
-        const u64 leaf0 = (t - tk.tile0) * kLeavesPerTile;
-        const u64 full_leaves = tk.n / kLeafBytes;
-        const u32 nfull = full_leaves > leaf0 ? static_cast<u32>(min(full_leaves - leaf0, u64{32})) : 0u;
-        const std::uint8_t* p0 = tk.base + leaf0 * kLeafBytes;
-        const u32 o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p0) & 15);
-        const std::uint8_t* a0 = p0 - o;
-        const u64 my_leaf = leaf0 + lane;
-        mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
-        if (nfull) {
-            const u32 r8 = (o & 3) * 8;
-            const bool extra = o != 0;
-            switch (o >> 2) {
-                case 0: hash_full_leaves_tma<0>(wbuf, bars, &phase, a0, nfull, extra, r8, lane, h1, h2); break;
-                case 1: hash_full_leaves_tma<1>(wbuf, bars, &phase, a0, nfull, extra, r8, lane, h1, h2); break;
-                case 2: hash_full_leaves_tma<2>(wbuf, bars, &phase, a0, nfull, extra, r8, lane, h1, h2); break;
-                default: hash_full_leaves_tma<3>(wbuf, bars, &phase, a0, nfull, extra, r8, lane, h1, h2); break;
-            }
-        }
-        if (lane < nfull) {
-            u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
-            mm::finish(f1, f2, 0, 0, 0, kLeafBytes);
-            acc_h += f1;
-            acc_l += f2;
-        } else if (lane == nfull && my_leaf * kLeafBytes < tk.n) {
-            const u32 len = static_cast<u32>(tk.n - my_leaf * kLeafBytes);
-            u64 d1, d2;
-            leaf_digest(tk.base + my_leaf * kLeafBytes, len, my_leaf, d1, d2);
-            acc_h += d1;
-            acc_l += d2;
-        }
-    }
-    if (cur >= 0) {
-        const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
-        if (lane == 0) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
-            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
-        }
-    }
-}
-
-// ---- v3: v1 with swizzled 8-word slots (default) ---------------------------------
-// v1's 9-word slots cost a divide-by-9 per copied word; per-lane TMA (v2)
-// serialises on uniform operands.  v3 keeps cp.async but lays a stage out as
-// 32 slots of 8 words (128 B) with the word index XOR-swizzled by (leaf & 7),
-// plus a 32-word column holding each leaf's 9th (realignment) word.  Then
-// copy i of a lane is leaf 4i + lane/8, word lane%8: one base register plus
-// the immediate 16 KiB·i per LDGSTS, no predicates on full tiles, and both
-// the LDGSTS writes and the per-lane LDS.128 reads are bank-conflict free.
-constexpr int kV3Stages = 3;
+// Stage layout: 32 slots of 8 words (128 B) with the word index
+// XOR-swizzled by (leaf & 7), plus a 32-word column holding each leaf's 9th
+// (realignment) word.  Copy i of a lane is leaf 4i + lane/8, word lane%8: one
+// base register plus the immediate 16 KiB·i per LDGSTS, no predicates on full
+// tiles, and both the LDGSTS writes and the per-lane LDS.128 reads are bank
+// conflict free.
 constexpr int kV3StageWords = 32 * kStageBlocks + 32;  // slots + extra column
-constexpr int kV3WarpWords = kV3Stages * kV3StageWords;
-constexpr int kV3SmemBytes = kWarpsPerCta * kV3WarpWords * 16;
-
-__device__ __forceinline__ void v3_issue(uint4* stage_buf, const std::uint8_t* src_lane, const std::uint8_t* src_extra,
-                                         u32 nfull, bool extra, u32 lane) {
-    // slot words: copy i -> leaf 4i + lane/8, word lane%8 (swizzled by leaf&7)
-    const u32 leaf_in_group = lane >> 3, q = lane & 7;
-    if (nfull == 32) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            // leaf l = 4i + g; its swizzle key is (4i + g) & 7 = ((4i) & 7) ^ g for g < 4
-            const u32 key = ((4 * i) & 7) ^ leaf_in_group;
-            cp_async16(stage_buf + (4 * i + leaf_in_group) * 8 + (q ^ key), src_lane + static_cast<u64>(i) * 16384);
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const u32 l = 4 * i + leaf_in_group;
-            if (l < nfull) cp_async16(stage_buf + l * 8 + (q ^ (l & 7)), src_lane + static_cast<u64>(i) * 16384);
-        }
-    }
-    if (extra && lane < nfull) cp_async16(stage_buf + 32 * kStageBlocks + lane, src_extra);
-    cp_async_commit();
-}
 
 template <int Q>
 __device__ __forceinline__ void v3_hash_stage(const uint4* stage_buf, u32 lane, u32 r8, mm::W32& h1, mm::W32& h2) {
@@ -539,104 +132,8 @@ __device__ __forceinline__ void v3_hash_stage_aligned(const uint4* stage_buf, u3
     }
 }
 
-template <int Q>
-__device__ __forceinline__ void v3_hash_full_leaves(uint4* wbuf, const std::uint8_t* a0, u32 nfull, bool extra,
-                                                    u32 r8, u32 lane, mm::W32& h1, mm::W32& h2) {
-    // copy i of this lane reads leaf (4i + lane/8), word lane%8 of the stage
-    const std::uint8_t* src_lane = a0 + static_cast<u64>(lane >> 3) * kLeafBytes + (lane & 7) * 16;
-    const std::uint8_t* src_extra = a0 + static_cast<u64>(lane) * kLeafBytes + 128;
-#pragma unroll
-    for (int s = 0; s < kV3Stages - 1; ++s)
-        v3_issue(wbuf + s * kV3StageWords, src_lane + s * 128, src_extra + s * 128, nfull, extra, lane);
-    for (int s = 0; s < kStagesPerLeaf; ++s) {
-        const int nxt = s + kV3Stages - 1;
-        if (nxt < kStagesPerLeaf)
-            v3_issue(wbuf + (nxt % kV3Stages) * kV3StageWords, src_lane + nxt * 128, src_extra + nxt * 128, nfull,
-                     extra, lane);
-        else
-            cp_async_commit();
-        cp_async_wait<kV3Stages - 1>();
-        __syncwarp();
-        if (lane < nfull) v3_hash_stage<Q>(wbuf + (s % kV3Stages) * kV3StageWords, lane, r8, h1, h2);
-        __syncwarp();
-    }
-}
-
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 2)
-    fp_v3_kernel(const FpTask* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums) {
-    extern __shared__ uint4 smem[];
-    const u32 lane = threadIdx.x & 31;
-    const u32 wid = threadIdx.x >> 5;
-    uint4* wbuf = smem + wid * kV3WarpWords;
-    const u64 nwarps = static_cast<u64>(gridDim.x) * kWarpsPerCta;
-    int cur = -1;
-    u64 acc_h = 0, acc_l = 0;
-    for (u64 t = static_cast<u64>(blockIdx.x) * kWarpsPerCta + wid; t < total_tiles; t += nwarps) {
-        u32 lo = 0, hi = n_tasks - 1;
-        while (lo < hi) {
-            const u32 mid = (lo + hi + 1) >> 1;
-            if (tasks[mid].tile0 <= t) lo = mid;
-            else hi = mid - 1;
-        }
-        const int ti = static_cast<int>(lo);
-        if (ti != cur) {
-            if (cur >= 0) {
-                const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
-                if (lane == 0) {
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
-                }
-            }
-            cur = ti;
-            acc_h = acc_l = 0;
-        }
-        const FpTask tk = tasks[ti];
-        const u64 leaf0 = (t - tk.tile0) * kLeavesPerTile;
-        const u64 full_leaves = tk.n / kLeafBytes;
-        const u32 nfull = full_leaves > leaf0 ? static_cast<u32>(min(full_leaves - leaf0, u64{32})) : 0u;
-        const std::uint8_t* p0 = tk.base + leaf0 * kLeafBytes;
-        const u32 o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p0) & 15);
-        const std::uint8_t* a0 = p0 - o;
-        const u64 my_leaf = leaf0 + lane;
-        mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
-        if (nfull) {
-            const u32 r8 = (o & 3) * 8;
-            const bool extra = o != 0;
-            switch (o >> 2) {
-                case 0: v3_hash_full_leaves<0>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
-                case 1: v3_hash_full_leaves<1>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
-                case 2: v3_hash_full_leaves<2>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
-                default: v3_hash_full_leaves<3>(wbuf, a0, nfull, extra, r8, lane, h1, h2); break;
-            }
-        }
-        if (lane < nfull) {
-            u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
-            mm::finish(f1, f2, 0, 0, 0, kLeafBytes);
-            acc_h += f1;
-            acc_l += f2;
-        } else if (lane == nfull && my_leaf * kLeafBytes < tk.n) {
-            const u32 len = static_cast<u32>(tk.n - my_leaf * kLeafBytes);
-            u64 d1, d2;
-            leaf_digest(tk.base + my_leaf * kLeafBytes, len, my_leaf, d1, d2);
-            acc_h += d1;
-            acc_l += d2;
-        }
-    }
-    if (cur >= 0) {
-        const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
-        if (lane == 0) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur), sh);
-            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur + 1), sl);
-        }
-    }
-}
-
-// ---- v4: v3 + cross-tile pipelining (default) ---------------------------------
-// v3 drains its cp.async pipeline at every tile boundary: the prologue of tile
-// k+1 waits a full DRAM latency (~1.5 us) after ~5 us of hashing, which ncu
-// shows as the dominant long-scoreboard stall.  v4 treats a warp's tiles as
-// one continuous stream of 32-stage groups: the stages of tile k+1 are
-// already in flight while the last stages of tile k are hashed.
+// A warp's view of one tile: the tensor, the tile's first leaf, the number of
+// full leaves in it, and the source alignment o (uniform per tensor).
 struct TileRef {
     const std::uint8_t* a0;  // aligned base of leaf 0 of the tile
     const std::uint8_t* base;  // tensor base
@@ -646,39 +143,6 @@ struct TileRef {
     u32 o;
     int task;
 };
-
-__device__ __forceinline__ TileRef tile_ref(const FpTask* __restrict__ tasks, u32 n_tasks, u64 t, u64 total_tiles) {
-    TileRef r{nullptr, nullptr, 0, 0, 0, 0, -1};
-    if (t >= total_tiles) return r;
-    u32 lo = 0, hi = n_tasks - 1;
-    while (lo < hi) {
-        const u32 mid = (lo + hi + 1) >> 1;
-        if (tasks[mid].tile0 <= t) lo = mid;
-        else hi = mid - 1;
-    }
-    const FpTask tk = tasks[lo];
-    r.task = static_cast<int>(lo);
-    r.base = tk.base;
-    r.n = tk.n;
-    r.leaf0 = (t - tk.tile0) * kLeavesPerTile;
-    const u64 full_leaves = tk.n / kLeafBytes;
-    r.nfull = full_leaves > r.leaf0 ? static_cast<u32>(min(full_leaves - r.leaf0, u64{32})) : 0u;
-    const std::uint8_t* p0 = tk.base + r.leaf0 * kLeafBytes;
-    r.o = static_cast<u32>(reinterpret_cast<std::uintptr_t>(p0) & 15);
-    r.a0 = p0 - r.o;
-    return r;
-}
-
-__device__ __forceinline__ void v4_issue(uint4* stage_buf, const TileRef& tr, int s, u32 lane) {
-    if (tr.task < 0 || tr.nfull == 0) {
-        cp_async_commit();
-        return;
-    }
-    const std::uint8_t* src_lane =
-        tr.a0 + static_cast<u64>(lane >> 3) * kLeafBytes + (lane & 7) * 16 + static_cast<u64>(s) * 128;
-    const std::uint8_t* src_extra = tr.a0 + static_cast<u64>(lane) * kLeafBytes + static_cast<u64>(s) * 128 + 128;
-    v3_issue(stage_buf, src_lane, src_extra, tr.nfull, tr.o != 0, lane);
-}
 
 __device__ __forceinline__ void v4_hash(const uint4* stage_buf, const TileRef& tr, u32 lane, mm::W32& h1,
                                         mm::W32& h2) {
@@ -695,78 +159,6 @@ __device__ __forceinline__ void v4_hash(const uint4* stage_buf, const TileRef& t
     }
 }
 
-template <int STAGES, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 2)
-    fp_v4_kernel(const FpTask* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums) {
-    extern __shared__ uint4 smem[];
-    const u32 lane = threadIdx.x & 31;
-    const u32 wid = threadIdx.x >> 5;
-    uint4* wbuf = smem + wid * (STAGES * kV3StageWords);
-    const u64 nwarps = static_cast<u64>(gridDim.x) * WARPS;
-    u64 t = static_cast<u64>(blockIdx.x) * WARPS + wid;
-    if (t >= total_tiles) return;
-    TileRef cur = tile_ref(tasks, n_tasks, t, total_tiles);
-    TileRef nxt = tile_ref(tasks, n_tasks, t + nwarps, total_tiles);
-    int cur_task = -1;
-    u64 acc_h = 0, acc_l = 0;
-    u32 buf = 0;  // running stage-buffer index
-    constexpr int kAhead = STAGES - 1;
-#pragma unroll
-    for (int s = 0; s < kAhead; ++s) v4_issue(wbuf + s * kV3StageWords, cur, s, lane);
-    while (cur.task >= 0) {
-        if (cur.task != cur_task) {
-            if (cur_task >= 0) {
-                const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
-                if (lane == 0) {
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task), sh);
-                    atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task + 1), sl);
-                }
-            }
-            cur_task = cur.task;
-            acc_h = acc_l = 0;
-        }
-        const u64 my_leaf = cur.leaf0 + lane;
-        mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
-        for (int s = 0; s < kStagesPerLeaf; ++s) {
-            const int ahead = s + kAhead;
-            u32 fill = buf + kAhead;
-            fill = fill >= STAGES ? fill - STAGES : fill;
-            if (ahead < kStagesPerLeaf) v4_issue(wbuf + fill * kV3StageWords, cur, ahead, lane);
-            else v4_issue(wbuf + fill * kV3StageWords, nxt, ahead - kStagesPerLeaf, lane);
-            cp_async_wait<STAGES - 1>();
-            __syncwarp();
-            if (lane < cur.nfull) v4_hash(wbuf + buf * kV3StageWords, cur, lane, h1, h2);
-            __syncwarp();
-            buf = buf + 1 == STAGES ? 0 : buf + 1;
-        }
-        if (lane < cur.nfull) {
-            u64 f1 = mm::u_of(h1), f2 = mm::u_of(h2);
-            mm::finish(f1, f2, 0, 0, 0, kLeafBytes);
-            acc_h += f1;
-            acc_l += f2;
-        } else if (lane == cur.nfull && my_leaf * kLeafBytes < cur.n) {
-            const u32 len = static_cast<u32>(cur.n - my_leaf * kLeafBytes);
-            u64 d1, d2;
-            leaf_digest(cur.base + my_leaf * kLeafBytes, len, my_leaf, d1, d2);
-            acc_h += d1;
-            acc_l += d2;
-        }
-        t += nwarps;
-        cur = nxt;
-        nxt = tile_ref(tasks, n_tasks, t + nwarps, total_tiles);
-    }
-    cp_async_wait<0>();
-    if (cur_task >= 0) {
-        const u64 sh = warp_sum(acc_h), sl = warp_sum(acc_l);
-        if (lane == 0) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task), sh);
-            atomicAdd(reinterpret_cast<unsigned long long*>(sums + 2 * cur_task + 1), sl);
-        }
-    }
-}
-
-// root = murmur3(le64 H ‖ le64 L ‖ le64 n, seed 0): one body block + an
-// 8-byte tail.
 __global__ void fp_finalize_kernel(const FpTask* __restrict__ tasks, u32 n_tasks, const u64* __restrict__ sums,
                                    u64* __restrict__ digests) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -936,7 +328,6 @@ __device__ __forceinline__ void copy_issue(uint4* stage_buf, const CopyTileRef& 
     const u64 extra_word = (tr.leaf0 + lane) * kLeafBytes + static_cast<u64>(s) * 128 + 128;  // tensor offset + o
     const bool extra = (tr.o != 0 || c.delta != 0) && extra_word - tr.o < tr.n;
     const std::uint8_t* src_extra = tr.a0 + static_cast<u64>(lane) * kLeafBytes + static_cast<u64>(s) * 128 + 128;
-    // v3_issue loads the extra column for lanes < nfull when `extra`
     const u32 leaf_in_group = lane >> 3, q = lane & 7;
     if (tr.nfull == 32) {
 #pragma unroll
@@ -1215,85 +606,10 @@ void copy_fp_launch(const CopyFpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64
 void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, u64* d_sync,
                int sm_count, cudaStream_t s, bool sync_zeroed) {
     if (n_tasks == 0) return;
-    // Default: the load kernel with fingerprint-only tasks.  TANGRAM_FP_KERNEL=
-    // v0..v5 selects the earlier dedicated K1 variants (A/B runs).
-    static const int variant = [] {
-        const char* e = std::getenv("TANGRAM_FP_KERNEL");
-        if (e && std::strcmp(e, "v0") == 0) return 0;
-        if (e && std::strcmp(e, "v1") == 0) return 1;
-        if (e && std::strcmp(e, "v2") == 0) return 2;
-        if (e && std::strcmp(e, "v3") == 0) return 3;
-        if (e && std::strcmp(e, "v4") == 0) return 4;
-        if (e && std::strcmp(e, "v5") == 0) return 5;
-        return 6;
-    }();
-    const bool v0 = variant == 0;
-    if (total_tiles > 0 && variant == 6) {
+    // K1 is the load kernel with fingerprint-only tasks
+    if (total_tiles > 0)
         load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, nullptr, 0, sm_count, s, sync_zeroed,
                            /*writes=*/false);
-    } else if (total_tiles > 0 && variant == 4) {
-        static const bool attr = [] {
-            return cudaFuncSetAttribute(fp_v4_kernel<kV3Stages, kWarpsPerCta>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kV3SmemBytes) == cudaSuccess;
-        }();
-        (void)attr;
-        const u64 want = (total_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
-        const u64 cap = static_cast<u64>(sm_count) * 2;
-        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
-        fp_v4_kernel<kV3Stages, kWarpsPerCta>
-            <<<blocks, kWarpsPerCta * 32, kV3SmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
-    } else if (total_tiles > 0 && variant == 5) {
-        static const bool attr = [] {
-            return cudaFuncSetAttribute(fp_v4_kernel<CfgSingle::kStages, CfgSingle::kWarps>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, CfgSingle::kSmemBytes) == cudaSuccess;
-        }();
-        (void)attr;
-        const u64 want = (total_tiles + CfgSingle::kWarps - 1) / CfgSingle::kWarps;
-        const u64 cap = static_cast<u64>(sm_count) * 2;
-        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
-        fp_v4_kernel<CfgSingle::kStages, CfgSingle::kWarps>
-            <<<blocks, CfgSingle::kWarps * 32, CfgSingle::kSmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
-        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-    } else if (total_tiles > 0 && variant == 3) {
-        static const bool attr = [] {
-            return cudaFuncSetAttribute(fp_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV3SmemBytes) ==
-                   cudaSuccess;
-        }();
-        (void)attr;
-        const u64 want = (total_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
-        const u64 cap = static_cast<u64>(sm_count) * 2;
-        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
-        fp_v3_kernel<<<blocks, kWarpsPerCta * 32, kV3SmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
-        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-    } else if (total_tiles > 0 && variant == 2) {
-        static const bool attr = [] {
-            return cudaFuncSetAttribute(fp_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemBytes) ==
-                   cudaSuccess;
-        }();
-        (void)attr;
-        const u64 want = (total_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
-        const u64 cap = static_cast<u64>(sm_count) * 2;
-        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
-        fp_tma_kernel<<<blocks, kWarpsPerCta * 32, kTmaSmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
-        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-    } else if (total_tiles > 0 && v0) {
-        const u64 want = (total_tiles + 7) / 8;  // 8 warps per block
-        const u64 cap = static_cast<u64>(sm_count) * 4;
-        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
-        fp_leaves_kernel<<<blocks, 256, 0, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
-        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-    } else if (total_tiles > 0) {
-        static const bool attr = [] {
-            return cudaFuncSetAttribute(fp_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) ==
-                   cudaSuccess;
-        }();
-        (void)attr;
-        const u64 want = (total_tiles + kWarpsPerCta - 1) / kWarpsPerCta;
-        const u64 cap = static_cast<u64>(sm_count) * 2;
-        const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
-        fp_smem_kernel<<<blocks, kWarpsPerCta * 32, kSmemBytes, s>>>(d_tasks, n_tasks, total_tiles, d_sums);
-        g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
-    }
     fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
