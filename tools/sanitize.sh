@@ -1,0 +1,20 @@
+#!/bin/bash
+# compute-sanitizer over the final kernels (run on the GPU box):
+#  memcheck : load kernel (paired stores, tail staging) at partial-leaf sizes and
+#             several alignments / line phases; K4D device KV batches
+#  racecheck: load kernel shared-memory ring (paired stores, tail staging)
+#  synccheck: same
+S=/usr/local/cuda/bin/compute-sanitizer
+OUT=gpurun_out/sanitizer.txt
+{
+echo "# compute-sanitizer on the B200 (round 1, final load kernel)"
+echo "## memcheck: copy_fingerprint_fused at partial-leaf sizes"
+timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest tests/test_gpu_kernels.py -q -k "copy_fingerprint_fused and (4097 or 135169 or 656359) and (16 or 112)" 2>&1 | tail -4
+echo "## memcheck: K4D device KV batches"
+timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest -q "tests/test_gpu_kv_device.py::test_device_batches_equal_reference[1]" tests/test_gpu_kv_device.py::test_device_batches_in_a_cuda_graph 2>&1 | tail -4
+echo "## racecheck: load kernel ring"
+timeout 900 $S --tool racecheck python -m pytest -q "tests/test_gpu_kernels.py::test_copy_fingerprint_fused[16-3-11-135169]" "tests/test_gpu_kernels.py::test_copy_fingerprint_fused[112-0-8-656359]" 2>&1 | tail -4
+echo "## synccheck: load kernel ring"
+timeout 900 $S --tool synccheck python -m pytest -q "tests/test_gpu_kernels.py::test_copy_fingerprint_fused[16-3-11-135169]" "tests/test_gpu_kernels.py::test_copy_fingerprint_fused[112-0-8-656359]" 2>&1 | tail -4
+} > $OUT
+cat $OUT
