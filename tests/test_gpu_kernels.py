@@ -95,7 +95,8 @@ def test_relocation_kernel_random_alignments(tg):
 
 @pytest.mark.parametrize("n", [0, 1, 15, 17, 4095, 4096, 4097, 8192, 4096 * 31 + 7, 4096 * 32, 4096 * 33 + 1,
                                (1 << 21) + 4093, 131072 * 5 + 999])
-@pytest.mark.parametrize("so,do", [(0, 0), (0, 5), (5, 0), (3, 11), (11, 3), (7, 7), (15, 1), (1, 15), (0, 8)])
+@pytest.mark.parametrize("so,do", [(0, 0), (0, 5), (5, 0), (3, 11), (11, 3), (7, 7), (15, 1), (1, 15), (0, 8),
+                                   (4, 0), (12, 4), (8, 12), (6, 2)])
 @pytest.mark.parametrize("pad", [16, 32, 64, 112])
 def test_copy_fingerprint_fused(tg, cpu, n, so, do, pad):
     """K3F moves the bytes exactly (including head/tail bytes, neighbours
