@@ -299,6 +299,43 @@ __device__ __forceinline__ void write_lines(const uint4* cur_buf, const uint4* p
     }
 }
 
+// Up to three line stores of one iteration (paired mode: line s - 1, line s,
+// and after a leaf's last stage the spill line) through ONE instance of the
+// unrolled store body: job t takes (cur, prev, stage, use_cur, use_prev) from
+// the arguments by index, in a loop that is not unrolled — the load kernel's
+// instruction footprint matters (warps of one SM run different alignment
+// variants; ncu shows no_instructions stalls).
+template <int QD, bool SHIFT>
+__device__ __forceinline__ void write_line_jobs(const uint4* b0, const uint4* b1, const uint4* b2, int s, int nj,
+                                                bool first_prev, const CopyTileRef& c, bool check, u32 r8, u32 lane) {
+#pragma unroll 1
+    for (int t = 0; t < nj; ++t) {
+        // t = 0: line s - 1 (cur b1, prev b0); t = 1: line s (cur b2, prev b1);
+        // t = 2: spill line s + 1 (no cur, prev b2)
+        const uint4* cur = t == 0 ? b1 : b2;
+        const uint4* prev = t == 0 ? b0 : (t == 1 ? b1 : b2);
+        write_lines<QD, SHIFT>(cur, prev, c, s - 1 + t, t < 2, t == 0 ? first_prev : true, check, r8, lane);
+    }
+}
+
+__device__ __forceinline__ void write_pair_dispatch(const uint4* b0, const uint4* b1, const uint4* b2, int s, int nj,
+                                                    bool first_prev, const CopyTileRef& c, u32 lane) {
+    const long long tile_lo = static_cast<long long>(c.t.leaf0 * kLeafBytes) - 16;
+    const long long tile_hi = static_cast<long long>((c.t.leaf0 + c.t.nfull) * kLeafBytes) + 16;
+    const bool check = tile_lo < static_cast<long long>(c.x_first) || tile_hi > static_cast<long long>(c.x_end);
+    if (c.delta == 0) {
+        write_line_jobs<0, false>(b0, b1, b2, s, nj, first_prev, c, check, 0, lane);
+        return;
+    }
+    const u32 r8 = (c.delta & 3) * 8;
+    switch (c.delta >> 2) {
+        case 0: write_line_jobs<0, true>(b0, b1, b2, s, nj, first_prev, c, check, r8, lane); break;
+        case 1: write_line_jobs<1, true>(b0, b1, b2, s, nj, first_prev, c, check, r8, lane); break;
+        case 2: write_line_jobs<2, true>(b0, b1, b2, s, nj, first_prev, c, check, r8, lane); break;
+        default: write_line_jobs<3, true>(b0, b1, b2, s, nj, first_prev, c, check, r8, lane); break;
+    }
+}
+
 __device__ __forceinline__ void write_lines_dispatch(const uint4* cur_buf, const uint4* prev_buf, const CopyTileRef& c,
                                                      int s, bool use_cur, bool use_prev, u32 lane) {
     // the whole tile is inside [x_first, x_end) unless it holds the tensor's
@@ -461,10 +498,8 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
                 if (s & 1) {
                     if (writes && cur.t.nfull) {
                         const uint4* spp = wbuf + b2 * kV3StageWords;
-                        write_lines_dispatch(sp, spp, cur, s - 1, true, s > 1, lane);
-                        write_lines_dispatch(sb, sp, cur, s, true, true, lane);
-                        if (s == kStagesPerLeaf - 1 && cur.k)
-                            write_lines_dispatch(nullptr, sb, cur, kStagesPerLeaf, false, true, lane);
+                        const int nj = (s == kStagesPerLeaf - 1 && cur.k) ? 3 : 2;
+                        write_pair_dispatch(spp, sp, sb, s, nj, s > 1, cur, lane);
                     }
                     __syncwarp();
                     issue(s + 2, static_cast<int>(b2));
