@@ -228,7 +228,8 @@ def run_reference_arm(args):
     sample = (f"load #3 of the C2 switch per step: reference ReuseStore::load_model (oracle/_ref) + CPU data plane "
               f"port (oracle/cpu_oracle.c): {len(o['plan']['relocations'])} relocations "
               f"({o['bytes_merged']} B memmove), {len(o['plan']['placements'])} placements "
-              f"({o['bytes_transferred']} B memcpy from host), tgfp1 over all 41 tensors ({total} B)")
+              f"({o['bytes_transferred']} B memcpy from host), tgfp1 over all {len(rcat[SEQ[2]]['tensors'])} tensors "
+              f"({total} B)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
@@ -240,17 +241,46 @@ def run_reference_arm(args):
     return 0
 
 
+# ---- ranks ----------------------------------------------------------------------------------------
+def shared_gpu():
+    """TANGRAM_BENCH_SHARED_GPU=1: check the N > 1 flow on a one-GPU box — every
+    rank on device 0, gloo instead of NCCL (which refuses two ranks on one
+    GPU), and the C2 switch shrunk to fit N copies (a flow check, not a bench
+    number)."""
+    return os.environ.get("TANGRAM_BENCH_SHARED_GPU") == "1"
+
+
+def dist_setup():
+    """(rank, world, device) from torchrun's environment; one process per GPU
+    over NCCL (the barrier and the max-over-ranks reduction)."""
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    dev = 0 if shared_gpu() else int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    if world > 1:
+        if shared_gpu():
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    return rank, world, dev
+
+
+def reduce_max(vals, dev):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device="cpu" if shared_gpu() else f"cuda:{dev}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
+
+
 # ---- our arm ---------------------------------------------------------------------------------------
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local = dist_setup()
 
     import paper_2512_01357_b200 as tg
     from paper_2512_01357_b200 import _native as N
@@ -258,7 +288,7 @@ def run_ours(args):
     lib = N.lib
 
     cat = catalog(tg)
-    models = [cat["opt13B"], cat["opt6.7B"]]
+    models = [cat[SEQ[0]], cat[SEQ[1]]]
     target = cat[SEQ[2]]
 
     # HBM model cache: every tensor of both models synthesised in HBM (setup
@@ -341,11 +371,7 @@ def run_ours(args):
         write_timeline(args.timeline, lambda: (register_device(miss_ids), step()))
 
     def maxrank(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return x if world == 1 else reduce_max([x], local)[0]
 
     mv = maxrank(sum(ms_v) / len(ms_v))
     me = maxrank(sum(ms_e) / len(ms_e))
@@ -500,6 +526,9 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_base
     if extras:
         line["secondary_configs"] = extras
+    if shared_gpu():
+        line["config"]["test_mode"] = (f"TANGRAM_BENCH_SHARED_GPU: {world} ranks on one GPU over gloo, switch "
+                                       f"{SEQ} in {POOL >> 30} GiB pools — a flow check, not a bench number")
     print(json.dumps(line))
     if world > 1:
         dist.barrier()
@@ -861,12 +890,7 @@ def run_c4(args):
     NVLink by K3 and fingerprint-verified against the neighbour's digest."""
     import torch
     import torch.distributed as dist
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world, local = dist_setup()
     import paper_2512_01357_b200 as tg
     from paper_2512_01357_b200.checkpoint import HostCheckpoint
     gpt = catalog(tg)["gpt20B"]
@@ -907,9 +931,8 @@ def run_c4(args):
     mc = statistics.mean(cold_ms)
     mp_ = statistics.mean(peer_ms) if peer_ms else None
     if world > 1:
-        t = torch.tensor([mc, mp_ or 0.0, float(verify)], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        mc, mp_, verify = float(t[0]), float(t[1]), int(t[2])
+        mc, mp_, v = reduce_max([mc, mp_ or 0.0, float(verify)], local)
+        verify = int(v)
     pool.close()
     if rank == 0:
         line = {"metric": "GPT-20B tensor-sharded cold load, aggregate GB/s (40e9 B over N PCIe links)",
@@ -932,7 +955,10 @@ def run_c4(args):
 
 
 def main():
+    global POOL, SEQ
     args = parse()
+    if shared_gpu():  # flow check of N > 1 on one GPU: a switch small enough for N copies
+        POOL, SEQ = 7 * GIB, ["qwen3B", "opt1.3B", "qwen3B"]  # 9 relocations, 1.2 GB placed
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.workload == "c4":
