@@ -386,7 +386,24 @@ def run_ours(args):
         parity.update(check_parity(tg, pool, target, host, cache, local))
     kernels = isolated_kernels(tg, pool, snap, target, miss_ids, local) if not args.profile else {}
 
+    def free_c2_working_set():
+        nonlocal snap
+        snap = None
+        pool.close()
+        for b in cache.values():
+            b.free()
+        for b in host.values():
+            b.free()
+        lib.tg_host_clear()
+
+    c4_secondary = world > 1 and not args.profile  # the sharded + peer paths at N GPUs
     if rank != 0:
+        if c4_secondary:
+            free_c2_working_set()
+            try:
+                c4_measure(tg, rank, world, local, 2, 1)
+            except Exception as e:  # pragma: no cover
+                print(f"rank {rank}: C4 secondary failed: {e}", file=sys.stderr)
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
@@ -420,15 +437,14 @@ def run_ours(args):
 
     cpu_base = None
     extras = {}
+    if c4_secondary:
+        free_c2_working_set()
+        try:
+            extras["c4"] = c4_measure(tg, rank, world, local, 2, 1)
+        except Exception as e:  # pragma: no cover
+            extras["c4"] = {"error": f"{type(e).__name__}: {e}"}
     if not args.profile and world == 1:
-        # free the C2 working set before the secondary configs
-        del snap
-        pool.close()
-        for b in cache.values():
-            b.free()
-        for b in host.values():
-            b.free()
-        lib.tg_host_clear()
+        free_c2_working_set()  # before the secondary configs
         for key, fn in (("c1", lambda: run_c1(tg, local, h2d_peak, hbm_peak)), ("c3", lambda: run_c3(tg, local)),
                         ("c5", lambda: run_c5(local)),
                         ("per_model", lambda: run_per_model(tg, local, h2d_peak, hbm_peak))):
@@ -881,17 +897,16 @@ def cpu_baseline(args):
                       "41 tensors)"}
 
 
-def run_c4(args):
+def c4_measure(tg, rank, world, local, steps, warmup):
     """C4: GPT-20B tensor-sharded over N ranks.  Cold: every rank
     loads its shard (40e9/N bytes) from pinned host memory over its own PCIe
     link, no collective.  Peer (N > 1): ranks exchange CUDA IPC arena handles
     and indexes (all_gather_object), then each rank loads its right
     neighbour's shard — every byte is pulled from the neighbour's pool over
-    NVLink by K3 and fingerprint-verified against the neighbour's digest."""
-    import torch
+    NVLink by the load kernel and fingerprint-verified against the
+    neighbour's digest.  Collective calls match on every rank; returns the
+    max-over-ranks result (all ranks)."""
     import torch.distributed as dist
-    rank, world, local = dist_setup()
-    import paper_2512_01357_b200 as tg
     from paper_2512_01357_b200.checkpoint import HostCheckpoint
     gpt = catalog(tg)["gpt20B"]
     mine = tg.shard_model(gpt, rank, world)
@@ -899,7 +914,7 @@ def run_c4(args):
     pool = tg.ReuseStore(tg.GpuSpec(f"gpu{local}", mine.total_size + right.total_size + GIB), device=local)
     cold_ms, peer_ms, peer_bytes, verify = [], [], 0, 0
     with HostCheckpoint([mine], device=local):
-        for step in range(args.warmup + args.steps):
+        for step in range(warmup + steps):
             pool.evict_model(right.model_id)
             pool.end_instance(mine.model_id)
             pool.evict_model(mine.model_id)
@@ -908,7 +923,7 @@ def run_c4(args):
             if world > 1:
                 dist.barrier()
             ms, o = _event_ms(pool.stream(), local, lambda: pool.load_model(mine, st, 0.0, details=False).value())
-            if step >= args.warmup:
+            if step >= warmup:
                 cold_ms.append(ms)
             verify += o.verify_mismatches
             if world > 1:
@@ -922,8 +937,8 @@ def run_c4(args):
                 st.record_request(right.model_id, 1.0)
                 dist.barrier()
                 ms, o = _event_ms(pool.stream(), local, lambda: pool.load_model(
-                    right, st, 1.0, tg.LoadPolicy(flags=1 | 2 | 4), details=False).value())
-                if step >= args.warmup:
+                    right, st, 1.0, tg.LoadPolicy(flags=1 | 2 | 4 | 8), details=False).value())
+                if step >= warmup:
                     peer_ms.append(ms)
                 peer_bytes = o.peer_bytes
                 verify += o.verify_mismatches
@@ -934,20 +949,33 @@ def run_c4(args):
         mc, mp_, v = reduce_max([mc, mp_ or 0.0, float(verify)], local)
         verify = int(v)
     pool.close()
+    return {"workload": "C4 GPT-20B sharded 1/N per rank (shard r = bytes [r*ceil(n/N), ...) of every tensor)",
+            "n_ranks": world, "shard_bytes_rank0": mine.total_size,
+            "cold_ms": mc, "cold_aggregate_GBps": gpt.total_size / (mc / 1e3) / 1e9,
+            "cold_per_rank_GBps": mine.total_size / (mc / 1e3) / 1e9,
+            "peer": None if mp_ is None else {
+                "what": "each rank loads its right neighbour's shard from the neighbour's pool (CUDA IPC + the load "
+                        "kernel over NVLink), fingerprint-verified",
+                "ms": mp_, "per_rank_GBps": peer_bytes / (mp_ / 1e3) / 1e9, "peak_GBps": 770.0,
+                "peak_source": "B200_PROFILING.md measured peer copy per direction"},
+            "verify_mismatches": verify}
+
+
+def run_c4(args):
+    """--workload c4: the C4 measurement as the bench line."""
+    import torch.distributed as dist
+    rank, world, local = dist_setup()
+    import paper_2512_01357_b200 as tg
+    r = c4_measure(tg, rank, world, local, args.steps, args.warmup)
     if rank == 0:
+        gpt = catalog(tg)["gpt20B"]
         line = {"metric": "GPT-20B tensor-sharded cold load, aggregate GB/s (40e9 B over N PCIe links)",
-                "value": gpt.total_size / (mc / 1e3) / 1e9, "unit": "GB/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": mc, "higher_is_better": True,
+                "value": r["cold_aggregate_GBps"], "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["cold_ms"], "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": {"workload": "C4 GPT-20B sharded 1/N per rank (shard r = bytes [r*ceil(n/N), ...) of "
-                                       "every tensor)", "shard_bytes_rank0": mine.total_size,
-                           "parallelism": f"tp{world} shards, independent pools"},
-                "peer": None if mp_ is None else {
-                    "what": "each rank loads its right neighbour's shard from the neighbour's pool (CUDA IPC + "
-                            "K3 over NVLink), fingerprint-verified",
-                    "ms": mp_, "per_rank_GBps": peer_bytes / (mp_ / 1e3) / 1e9, "peak_GBps": 770.0,
-                    "peak_source": "B200_PROFILING.md measured peer copy per direction"},
-                "verify_mismatches": verify}
+                "config": {"workload": r["workload"], "shard_bytes_rank0": r["shard_bytes_rank0"],
+                           "model_bytes": gpt.total_size, "parallelism": f"tp{world} shards, independent pools"},
+                "peer": r["peer"], "verify_mismatches": r["verify_mismatches"]}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
