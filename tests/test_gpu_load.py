@@ -385,3 +385,37 @@ def test_fused_load_kernel_fuzz(tg, cpu, seed, source):
             src.close()
         else:
             src.__exit__(None, None, None)
+
+
+def test_edge_models_match_reference(tg, ref, cpu):
+    """Ragged edges: a model with no tensors, one with a single 1-byte tensor,
+    and one whose tensors are 15, 16, 17, 4095, 4096 and 4097 bytes — loaded,
+    reloaded and switched against the reference on a small device pool."""
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    def spec(mid, sizes):
+        ts = [tg.TensorSpec(tg.tensor_key(mid, f"t{i}", [max(1, n // 2)]), mid, f"t{i}", n) for i, n in enumerate(sizes)]
+        ts.sort(key=lambda t: t.name)
+        return tg.ModelSpec(mid, ts, sum(sizes))
+    models = [spec("empty", []), spec("one", [1]), spec("ragged", [15, 16, 17, 4095, 4096, 4097])]
+    size = 64 * 1024
+    mine, theirs = tg.ReuseStore(tg.GpuSpec(pool_size=size), device=0), ref.ReuseStore(size)
+    sm, sr = tg.ModelStatsTable(), ref.ModelStatsTable()
+    with HostCheckpoint(models[1:]) as ck:
+        t = 0.0
+        for m in models + models[::-1]:
+            sm.record_request(m.model_id, t)
+            sr.record_request(m.model_id, t)
+            a = mine.load_model(m, sm, t)
+            b = theirs.load_model(m.to_json(), sr, t)
+            assert a.ok() == b["ok"]
+            if a.ok():
+                o = a.value()
+                assert o.bytes_transferred == b["bytes_transferred"] and o.verify_mismatches == 0
+                for i, tt in enumerate(m.tensors):
+                    assert o.digests[i] == cpu.content_fingerprint(ck.view(tt.id), threads=1)[0]
+            mine.end_instance(m.model_id)
+            theirs.end_instance(m.model_id)
+            assert mine.dump() == theirs.dump()
+            t += 1.0
+    assert mine.validate().ok()
+    mine.close()
