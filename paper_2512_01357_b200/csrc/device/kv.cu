@@ -429,6 +429,7 @@ public:
     int enqueue(const u64* d_slots, const u64* d_tokens, u32 n, void* stream) override {
         DeviceScope ds(dev_);
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s_;
+        foreign_ = foreign_ || st != s_;
         kv_device_batch_launch(d_ctl_, d_slots, d_tokens, n, st);
         TG_CUDA(cudaGetLastError());
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -556,6 +557,9 @@ private:
     void release_all() {
         DeviceScope ds(dev_);
         cudaStreamSynchronize(s_);
+        // batches enqueued on a caller's stream (or captured in a graph) may
+        // still read the control block and tables
+        if (foreign_) cudaDeviceSynchronize();
         for (u64* p : {tables_, free_, addr_, d_out_, d_runs_, d_slots_})
             if (p) cudaFree(p);
         if (d_log_) cudaFree(d_log_);
@@ -590,7 +594,7 @@ private:
     std::uint8_t* d_log_ = nullptr;
     u64 log_cap_ = 0, log_entry_ = 0, max_requests_ = 0, max_batches_ = 0;
     cudaEvent_t done_ = nullptr;
-    bool captured_ = false, pending_ = false;
+    bool captured_ = false, pending_ = false, foreign_ = false;
 };
 
 }  // namespace
