@@ -371,8 +371,9 @@ int tg_kv_device_tables(const tg_kv* kv, void** tables, uint64_t* stride, void**
  *                          enqueue one batch on `stream` (null: the engine's
  *                          stream): request table slots and token counts in
  *                          DEVICE memory, n <= max_requests; capturable in a
- *                          CUDA graph (every pointer is read at run time);
- *                          batches of one session must be stream-ordered;
+ *                          CUDA graph (every pointer is read at run time;
+ *                          the engine must outlive the graph); batches of
+ *                          one session must be stream-ordered;
  *   tg_kv_device_sync      wait, fold the device decisions into the host state,
  *                          replay on the reference path every batch the device
  *                          left to it (contended pool, unknown slot, shrinking
