@@ -357,6 +357,18 @@ int tg_kv_table(const tg_kv* kv, uint64_t request_id, uint64_t* pbns, uint64_t c
 int tg_kv_address_table(const tg_kv* kv, uint64_t* triples /*pbn,off,size*/, uint64_t cap, uint64_t* n); /* :63 */
 int tg_kv_stats_get(const tg_kv* kv, tg_kv_stats* out);
 int tg_kv_device_tables(const tg_kv* kv, void** tables, uint64_t* stride, void** addr); /* for paged attention */
+/* Block-table consumers (the cache write / gather of a paged-attention engine,
+ * PAPER.md:807 reshape_and_cache_segment): token i of the request in table
+ * slot d_slots[i] at token position d_positions[i] lives at
+ *   arena + addr[tables[slot][pos / block_tokens]] + (pos % block_tokens) * bytes_per_token.
+ * write_tokens copies d_buf[i] (bytes_per_token each) there; read_tokens
+ * gathers it into d_buf[i].  Device pointers; positions must lie in blocks the
+ * engine granted.  `cuda_stream` null = the engine's stream, which orders
+ * after its own table updates. */
+int tg_kv_write_tokens(tg_kv* kv, tg_pool* p, const uint64_t* d_slots, const uint64_t* d_positions, const void* d_buf,
+                       uint32_t n, void* cuda_stream);
+int tg_kv_read_tokens(tg_kv* kv, tg_pool* p, const uint64_t* d_slots, const uint64_t* d_positions, void* d_buf,
+                      uint32_t n, void* cuda_stream);
 
 /* ---- device-decided KV batches (K4D; new, no reference counterpart) ------------
  * The allocator decision of batch_allocate (:107-161) taken by a kernel, for

@@ -204,6 +204,8 @@ _SIGS = {
     "tg_kv_device_tables": (C.c_int, [vp, P(vp), P(u64), P(vp)]),
     "tg_lineage_register": (C.c_int, [TensorIdC, TensorIdC, u64, u64]),
     "tg_lineage_get": (C.c_int, [TensorIdC, P(TensorIdC), P(u64), P(u64)]),
+    "tg_kv_write_tokens": (C.c_int, [vp, vp, vp, vp, vp, C.c_uint32, vp]),
+    "tg_kv_read_tokens": (C.c_int, [vp, vp, vp, vp, vp, C.c_uint32, vp]),
     "tg_kv_request_slot": (C.c_int, [vp, u64, P(C.c_uint32)]),
     "tg_kv_device_arm": (C.c_int, [vp, vp, u64, C.c_uint32, C.c_uint32]),
     "tg_kv_batch_allocate_device": (C.c_int, [vp, vp, vp, C.c_uint32, vp]),

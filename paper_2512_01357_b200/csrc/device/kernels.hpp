@@ -153,6 +153,14 @@ inline std::uint64_t kv_log_entry_bytes(std::uint64_t max_requests) {
 }
 void kv_device_batch_launch(KvDevCtl* d_ctl, const std::uint64_t* d_slots, const std::uint64_t* d_tokens,
                             std::uint32_t n, cudaStream_t s);
+// Block-table consumer (what a paged-attention cache write / gather does):
+// token i of request-slot slots[i] at position pos[i] lives at
+// arena + addr[tables[slot * stride + pos / block_tokens]] + (pos % block_tokens) * token_bytes.
+// write: buf[i] -> that place; else that place -> buf[i] (token_bytes each).
+void kv_tokens_launch(const std::uint64_t* tables, std::uint64_t stride, const std::uint64_t* addr,
+                      std::uint8_t* arena, std::uint64_t block_tokens, std::uint64_t token_bytes,
+                      const std::uint64_t* slots, const std::uint64_t* pos, std::uint8_t* buf, std::uint32_t n,
+                      bool write, cudaStream_t s);
 void kv_release_launch(const std::uint64_t* table_row, std::uint64_t blocks, std::uint64_t* free_list_dst,
                        cudaStream_t s);
 

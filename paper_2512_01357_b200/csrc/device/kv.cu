@@ -246,6 +246,29 @@ __global__ void __launch_bounds__(kKvThreads) kv_device_batch_kernel(KvDevCtl* _
     }
 }
 
+// One warp per token; 16-byte words when both ends allow it, bytes otherwise.
+__global__ void kv_tokens_kernel(const u64* __restrict__ tables, u64 stride, const u64* __restrict__ addr,
+                                 std::uint8_t* __restrict__ arena, u64 block_tokens, u64 token_bytes,
+                                 const u64* __restrict__ slots, const u64* __restrict__ pos,
+                                 std::uint8_t* __restrict__ buf, u32 n, bool write) {
+    const u32 lane = threadIdx.x & 31;
+    const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
+    for (u64 i = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+        const u64 p = pos[i];
+        const u64 pbn = tables[slots[i] * stride + p / block_tokens];
+        std::uint8_t* a = arena + addr[pbn] + (p % block_tokens) * token_bytes;
+        std::uint8_t* b = buf + i * token_bytes;
+        std::uint8_t* dst = write ? a : b;
+        const std::uint8_t* src = write ? b : a;
+        if (((reinterpret_cast<std::uintptr_t>(dst) | reinterpret_cast<std::uintptr_t>(src) | token_bytes) & 15) == 0) {
+            for (u64 w = lane; w < token_bytes / 16; w += 32)
+                reinterpret_cast<uint4*>(dst)[w] = reinterpret_cast<const uint4*>(src)[w];
+        } else {
+            for (u64 k = lane; k < token_bytes; k += 32) dst[k] = src[k];
+        }
+    }
+}
+
 __global__ void kv_copy_kernel(const u64* __restrict__ src, u64 n, u64* __restrict__ dst) {
     for (u64 i = static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<u64>(gridDim.x) * blockDim.x)
@@ -479,6 +502,7 @@ public:
 
     void reset() override {}
     void* table_ptr() const override { return tables_; }
+    void* stream() const override { return s_; }
     u64 table_stride() const override { return stride_; }
     void* addr_ptr() const override { return addr_; }
 
@@ -608,6 +632,17 @@ void kv_batch_launch(const KvBatchArgs& a, cudaStream_t s) {
 
 void kv_device_batch_launch(KvDevCtl* d_ctl, const u64* d_slots, const u64* d_tokens, u32 n, cudaStream_t s) {
     kv_device_batch_kernel<<<1, kKvThreads, 0, s>>>(d_ctl, d_slots, d_tokens, n);
+    g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void kv_tokens_launch(const u64* tables, u64 stride, const u64* addr, std::uint8_t* arena, u64 block_tokens,
+                      u64 token_bytes, const u64* slots, const u64* pos, std::uint8_t* buf, u32 n, bool write,
+                      cudaStream_t s) {
+    if (n == 0 || token_bytes == 0) return;
+    const u64 want = (static_cast<u64>(n) * 32 + 255) / 256;
+    const unsigned blocks = static_cast<unsigned>(want < 4096 ? want : 4096);
+    kv_tokens_kernel<<<blocks, 256, 0, s>>>(tables, stride, addr, arena, block_tokens, token_bytes, slots, pos, buf, n,
+                                             write);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

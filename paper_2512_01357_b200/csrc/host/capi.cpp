@@ -913,6 +913,34 @@ int tg_kv_device_tables(const tg_kv* kv, void** tables, uint64_t* stride, void**
     return 0;
 }
 
+static int kv_tokens(tg_kv* kv, tg_pool* p, const uint64_t* slots, const uint64_t* pos, void* buf, uint32_t n,
+                     void* stream, bool write) {
+    return guard([&] {
+        KvDevice* d = kv->a->device();
+        if (!d || !p->pool->has_device()) return TG_ERR_NO_DEVICE;
+        if (kv->device != p->pool->device()) {
+            g_detail = "KV engine and pool on different devices";
+            return TG_ERR_BAD_ARG;
+        }
+        DeviceScope ds(p->pool->device());
+        const u64 bt = kv->a->block_tokens(), tb = kv->a->block_bytes() / bt;
+        kv_tokens_launch(static_cast<const u64*>(d->table_ptr()), d->table_stride(),
+                         static_cast<const u64*>(d->addr_ptr()), p->pool->arena(), bt, tb, slots, pos,
+                         static_cast<std::uint8_t*>(buf), n, write,
+                         static_cast<cudaStream_t>(stream ? stream : d->stream()));
+        TG_CUDA(cudaGetLastError());
+        return 0;
+    });
+}
+int tg_kv_write_tokens(tg_kv* kv, tg_pool* p, const uint64_t* slots, const uint64_t* pos, const void* buf, uint32_t n,
+                       void* stream) {
+    return kv_tokens(kv, p, slots, pos, const_cast<void*>(buf), n, stream, true);
+}
+int tg_kv_read_tokens(tg_kv* kv, tg_pool* p, const uint64_t* slots, const uint64_t* pos, void* buf, uint32_t n,
+                      void* stream) {
+    return kv_tokens(kv, p, slots, pos, buf, n, stream, false);
+}
+
 int tg_kv_request_slot(const tg_kv* kv, uint64_t rid, uint32_t* slot) {
     if (!slot) return TG_ERR_BAD_ARG;
     if (!kv->a->has_request(rid)) return code_of(Err::NotFound);

@@ -97,6 +97,7 @@ public:
     virtual std::unique_ptr<KvDevice> clone() const = 0;
     virtual void reset() = 0;
     virtual void* table_ptr() const = 0;
+    virtual void* stream() const = 0;  // the stream table updates are ordered on
     virtual u64 table_stride() const = 0;
     virtual void* addr_ptr() const = 0;
 };

@@ -707,6 +707,18 @@ class KvEngine:
                                                         C.c_void_p(stream) if stream else None),
                         "tg_kv_batch_allocate_device")
 
+    def write_tokens(self, store: ReuseStore, slots_ptr, positions_ptr, buf_ptr, n, stream=None):
+        """Paged-cache write through the block tables (device pointers; see tangram.h)."""
+        N.check_runtime(lib.tg_kv_write_tokens(self._h, store._h, C.c_void_p(slots_ptr), C.c_void_p(positions_ptr),
+                                               C.c_void_p(buf_ptr), n, C.c_void_p(stream) if stream else None),
+                        "tg_kv_write_tokens")
+
+    def read_tokens(self, store: ReuseStore, slots_ptr, positions_ptr, buf_ptr, n, stream=None):
+        """Paged-cache gather through the block tables (device pointers)."""
+        N.check_runtime(lib.tg_kv_read_tokens(self._h, store._h, C.c_void_p(slots_ptr), C.c_void_p(positions_ptr),
+                                              C.c_void_p(buf_ptr), n, C.c_void_p(stream) if stream else None),
+                        "tg_kv_read_tokens")
+
     def device_sync(self, store: ReuseStore, stats: ModelStatsTable) -> Result:
         """Fold the device's decisions into the host state; replay the batches
         the device left to the host.  Value: (applied, replayed) batch counts."""

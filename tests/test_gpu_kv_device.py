@@ -214,3 +214,83 @@ def test_destroying_an_armed_engine_releases_the_pool(tg):
     gc.collect()
     assert pool.alloc_kv_region(800, 5).ok()
     pool.close()
+
+
+@pytest.mark.parametrize("token_bytes", [48, 64])
+def test_block_tables_drive_a_paged_cache(tg, cpu, token_bytes):
+    """The allocator's block tables, consumed the way a paged-attention cache
+    write / gather does (tg_kv_write_tokens / tg_kv_read_tokens): every token
+    of every live request gets its own bytes, nothing overlaps — not other
+    requests' tokens, not the resident model's tensors — across host-decided
+    batches, device-decided decode steps, releases and free-list reuse."""
+    import numpy as np
+    import torch
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    rnd = random.Random(token_bytes)
+    model = tg.make_model("paged", 3_000_011, 2, token_bytes)
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=3_000_011 + 600_000), device=0)
+    st = tg.ModelStatsTable()
+    st.record_request(model.model_id, 0.0)
+    with HostCheckpoint([model]):
+        digests = pool.load_model(model, st, 0.0).value().digests
+    kv = tg.KvEngine(model.model_id, 8, token_bytes)
+    live = {}
+
+    def write(rids_tokens):
+        slots, pos, pat = [], [], []
+        for rid, (lo, hi) in rids_tokens.items():
+            for p in range(lo, hi):
+                slots.append(kv.request_slot(rid))
+                pos.append(p)
+                pat.append(np.full(token_bytes, (rid * 131 + p * 7) % 251, dtype=np.uint8))
+                pat[-1][:8] = np.frombuffer(np.int64(rid * 100000 + p).tobytes(), dtype=np.uint8)
+        if not slots:
+            return
+        s_d, p_d = _dev(slots), _dev(pos)
+        buf = torch.from_numpy(np.concatenate(pat)).cuda()
+        kv.write_tokens(pool, s_d.data_ptr(), p_d.data_ptr(), buf.data_ptr(), len(slots))
+        torch.cuda.synchronize()
+
+    def check():
+        slots, pos, want = [], [], []
+        for rid, n in live.items():
+            for p in range(n):
+                slots.append(kv.request_slot(rid))
+                pos.append(p)
+                w = np.full(token_bytes, (rid * 131 + p * 7) % 251, dtype=np.uint8)
+                w[:8] = np.frombuffer(np.int64(rid * 100000 + p).tobytes(), dtype=np.uint8)
+                want.append(w)
+        out = torch.empty(len(slots) * token_bytes, dtype=torch.uint8, device="cuda:0")
+        s_d, p_d = _dev(slots), _dev(pos)
+        kv.read_tokens(pool, s_d.data_ptr(), p_d.data_ptr(), out.data_ptr(), len(slots))
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), np.concatenate(want))
+        for i, t in enumerate(model.tensors):  # KV blocks never overlap the resident tensors
+            assert pool.fingerprint_tensor(t.id) == digests[i]
+
+    nxt = 1
+    for rnd_i in range(4):
+        reqs = [(nxt + i, rnd.randint(1, 60)) for i in range(12)]
+        nxt += len(reqs)
+        assert kv.batch_allocate(pool, st, reqs, want_pbns=False).ok()
+        write({r: (0, n) for r, n in reqs})
+        live.update(dict(reqs))
+        # device-decided decode steps
+        assert kv.device_arm(pool, 64, 64, 8).ok()
+        grown = {}
+        for step in range(3):
+            batch = [(r, live[r] + rnd.randint(1, 9)) for r in live]
+            s_d, t_d = _dev([kv.request_slot(r) for r, _ in batch]), _dev([t for _, t in batch])
+            kv.batch_allocate_device(s_d.data_ptr(), t_d.data_ptr(), len(batch))
+            torch.cuda.synchronize()  # the inputs must live until the batch ran
+            for r, t in batch:
+                grown[r] = (grown.get(r, (live[r], live[r]))[0], t)
+                live[r] = t
+        assert kv.device_sync(pool, st).ok()
+        write(grown)
+        check()
+        for r in [r for r in list(live) if rnd.random() < 0.4]:
+            assert kv.release_request(r).ok()
+            live.pop(r)
+        check()
+    pool.close()
