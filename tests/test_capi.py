@@ -45,6 +45,9 @@ def test_kv_device_path_needs_a_device(tg):
     with pytest.raises(N.TangramRuntimeError):
         kv.device_arm(pool, 16, 8, 4)
     assert pool.alloc_kv_region(800, 5).ok()  # not armed
+    # the paged-cache consumers need device tables too
+    assert N.lib.tg_kv_write_tokens(kv._h, pool._h, None, None, None, 0, None) == 101
+    assert N.lib.tg_kv_read_tokens(kv._h, pool._h, None, None, None, 0, None) == 101
 
 
 def test_data_plane_fails_loudly_without_device(tg):
