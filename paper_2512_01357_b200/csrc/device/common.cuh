@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <string>
@@ -16,6 +17,15 @@ inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw DeviceError(kErrCuda, std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define TG_CUDA(x) ::tg::cuda_check((x), #x)
+
+// NVTX range for the phases of a load / KV batch (visible in Nsight Systems;
+// header-only NVTX3, a no-op without a tool attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // RAII device guard.
 struct DeviceScope {

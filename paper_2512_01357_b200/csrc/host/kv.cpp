@@ -1,5 +1,7 @@
 #include "kv.hpp"
 
+#include "../device/common.cuh"
+
 #include <algorithm>
 
 namespace tg {
@@ -148,6 +150,7 @@ St KvAllocator::ensure_capacity(Store& s, const StatsView& st, u64 rid, u64 toke
 
 St KvAllocator::batch_allocate(Store& s, const StatsView& st, const std::vector<std::pair<u64, u64>>& reqs,
                                std::vector<u64>* counts, std::vector<u64>* pbns) {
+    NvtxRange nvtx("tg.kv_batch_allocate");
     counts->assign(reqs.size(), 0);
     u64 needed = 0;
     for (const auto& [rid, tokens] : reqs) {
@@ -281,6 +284,7 @@ int KvAllocator::enqueue_device(const u64* d_slots, const u64* d_tokens, u32 n, 
 }
 
 St KvAllocator::sync(Store& s, const StatsView& st, SyncReport* rep) {
+    NvtxRange nvtx("tg.kv_device_sync");
     if (!armed_) return Err::InvalidArgument;
     KvLog log;
     if (int rc = dev_->read_log(&log)) throw DeviceError(rc, "kv: device log read failed");

@@ -267,6 +267,7 @@ u64 build_tasks(std::vector<FpTask>& tasks) {
 St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, const LoadOptions& opt, u32 flags,
                     LoadReport* rep) {
     using clk = std::chrono::steady_clock;
+    NvtxRange nvtx_load("tg.load_model");
     *rep = LoadReport{};
     std::unique_ptr<DeviceScope> ds;
     if (has_device()) {
@@ -275,7 +276,10 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
         TG_CUDA(cudaEventRecord(ev(0), s_main_));  // t0: entry
     }
     const auto h0 = clk::now();
-    auto dec = store_.decide(m, stats, opt);
+    auto dec = [&] {
+        NvtxRange r("tg.plan");
+        return store_.decide(m, stats, opt);
+    }();
     rep->t.plan_us = std::chrono::duration<double, std::micro>(clk::now() - h0).count();
     if (!dec) return dec.error();
     LoadDecision& d = dec.value();
@@ -622,7 +626,11 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     TG_CUDA(cudaEventRecord(ev(3), s_main_));
     auto* h_dig = reinterpret_cast<u64*>(h + desc_bytes + sums_bytes + sync_bytes);
     if (nf + nc) TG_CUDA(cudaMemcpyAsync(h_dig, d_dig, sums_bytes, cudaMemcpyDeviceToHost, s_main_));
-    TG_CUDA(cudaStreamSynchronize(s_main_));
+    {
+        NvtxRange r("tg.wait_data_plane");
+        TG_CUDA(cudaStreamSynchronize(s_main_));
+    }
+    NvtxRange nvtx_verify("tg.record_verify_digests");
 
     rep->t.total_ms = ms_between(ev(0), ev(3));
     // fused: the whole load kernel (waves, device-source placements, verification)
