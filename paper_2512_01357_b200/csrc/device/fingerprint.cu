@@ -73,6 +73,13 @@ constexpr int kStageBlocks = 8;
 constexpr int kSlotWords = kStageBlocks + 1;
 constexpr int kStagesPerLeaf = static_cast<int>(kLeafBytes / 16) / kStageBlocks;  // 32
 
+// The 9th (realignment) word of a stage is the first word of the next 128
+// bytes — at a leaf's last stage, of the next leaf, read long before: no
+// 256-byte prefetch for it (that re-fetched 256 B per leaf from DRAM).
+__device__ __forceinline__ void cp_async16_noprefetch(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     // L2::256B: the L2 fetches the whole 256-byte pair of lines, so a leaf's
@@ -383,7 +390,7 @@ __device__ __forceinline__ void copy_issue(uint4* stage_buf, const CopyTileRef& 
             if (l < tr.nfull) cp_async16(stage_buf + l * 8 + (q ^ (l & 7)), src_lane + static_cast<u64>(i) * 16384);
         }
     }
-    if (extra && lane < tr.nfull) cp_async16(stage_buf + 32 * kStageBlocks + lane, src_extra);
+    if (extra && lane < tr.nfull) cp_async16_noprefetch(stage_buf + 32 * kStageBlocks + lane, src_extra);
     cp_async_commit();
 }
 
