@@ -72,3 +72,20 @@ def test_device_pool_without_gpu_errors(tg):
     import pytest
     with pytest.raises(N.TangramRuntimeError):
         tg.ReuseStore(tg.GpuSpec(pool_size=1 << 20), device=0)
+
+
+def test_plain_c_client(tmp_path):
+    """include/tangram.h is plain C11: a C client compiles with -Wall -Werror,
+    links libtangram.so and loads a catalog model on a control-plane pool."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        import pytest
+        pytest.skip("no gcc")
+    exe = tmp_path / "load_c11"
+    lib = os.path.join(ROOT, "paper_2512_01357_b200")
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c", "load_c11.c"), "-L", lib, "-ltangram",
+                    f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert out.strip() == "rc=0 xfer=2600000000 hits=0", out
