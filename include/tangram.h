@@ -109,6 +109,8 @@ typedef struct {
     uint64_t pcie_bytes, peer_bytes, device_src_bytes, fingerprint_bytes, repaired_bytes;
     uint32_t verify_mismatches, expected_mismatches;
     double plan_us, total_ms, relocate_ms, h2d_ms, peer_ms, fp_kernel_ms, fp_reuse_ms, fp_reuse_max_ms;
+    /* host side of the call: entry -> all device work enqueued, waiting for it, entry -> return */
+    double host_issue_us, host_wait_us, host_total_us;
 } tg_load_outcome;
 
 /* warmsim::EvictionCandidate (packing.hpp:32-38); model_id valid until the next call on the pool */

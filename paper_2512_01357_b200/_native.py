@@ -56,7 +56,8 @@ class LoadOutcomeC(C.Structure):
                 ("pcie_bytes", u64), ("peer_bytes", u64), ("device_src_bytes", u64), ("fingerprint_bytes", u64), ("repaired_bytes", u64),
                 ("verify_mismatches", u32), ("expected_mismatches", u32),
                 ("plan_us", dbl), ("total_ms", dbl), ("relocate_ms", dbl), ("h2d_ms", dbl), ("peer_ms", dbl),
-                ("fp_kernel_ms", dbl), ("fp_reuse_ms", dbl), ("fp_reuse_max_ms", dbl)]
+                ("fp_kernel_ms", dbl), ("fp_reuse_ms", dbl), ("fp_reuse_max_ms", dbl),
+                ("host_issue_us", dbl), ("host_wait_us", dbl), ("host_total_us", dbl)]
 
 
 class EvictionC(C.Structure):

@@ -370,6 +370,9 @@ int tg_load_model(tg_pool* p, const tg_model_spec* ms, const tg_stats* s, double
             out->fp_kernel_ms = r.t.fp_kernel_ms;
             out->fp_reuse_ms = r.t.fp_reuse_ms;
             out->fp_reuse_max_ms = r.t.fp_reuse_max_ms;
+            out->host_issue_us = r.t.host_issue_us;
+            out->host_wait_us = r.t.host_wait_us;
+            out->host_total_us = r.t.host_total_us;
         }
         return 0;
     });

@@ -626,10 +626,13 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     TG_CUDA(cudaEventRecord(ev(3), s_main_));
     auto* h_dig = reinterpret_cast<u64*>(h + desc_bytes + sums_bytes + sync_bytes);
     if (nf + nc) TG_CUDA(cudaMemcpyAsync(h_dig, d_dig, sums_bytes, cudaMemcpyDeviceToHost, s_main_));
+    const auto h_issued = clk::now();
+    rep->t.host_issue_us = std::chrono::duration<double, std::micro>(h_issued - h0).count();
     {
         NvtxRange r("tg.wait_data_plane");
         TG_CUDA(cudaStreamSynchronize(s_main_));
     }
+    rep->t.host_wait_us = std::chrono::duration<double, std::micro>(clk::now() - h_issued).count();
     NvtxRange nvtx_verify("tg.record_verify_digests");
 
     rep->t.total_ms = ms_between(ev(0), ev(3));
@@ -703,6 +706,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             e->has_digest = true;
         }
     }
+    rep->t.host_total_us = std::chrono::duration<double, std::micro>(clk::now() - h0).count();
     totals_.loads += 1;
     totals_.data_plane_ms += rep->t.total_ms;
     totals_.pcie_bytes += rep->pcie_bytes;

@@ -130,6 +130,9 @@ struct LoadTimings {
     double fp_kernel_ms = 0;     // Σ K1 launch durations
     double fp_reuse_ms = 0;      // Σ K1 launch durations over reused tensors (≤ 2 launches)
     double fp_reuse_max_ms = 0;  // the longer of the two
+    double host_issue_us = 0;    // host: entry .. all device work enqueued
+    double host_wait_us = 0;     // host: waiting for the device work
+    double host_total_us = 0;    // host: entry .. return
 };
 
 struct LoadReport {

@@ -417,7 +417,8 @@ class ReuseStore:
         plan = AllocationPlan(evs, rels, pls, o.total_eviction_cost, o.total_merge_cost, o.pgp_merge_cost,
                               o.initial_merge_cost, o.fallback_evictions)
         t = {k: getattr(o, k) for k in ("plan_us", "total_ms", "relocate_ms", "h2d_ms", "peer_ms", "fp_kernel_ms",
-                                        "fp_reuse_ms", "fp_reuse_max_ms")}
+                                        "fp_reuse_ms", "fp_reuse_max_ms", "host_issue_us", "host_wait_us",
+                                        "host_total_us")}
         return LoadOutcome(hits, misses, o.bytes_transferred, o.bytes_merged, o.eviction_cost_total, plan,
                            o.n_waves, o.pcie_bytes, o.peer_bytes, o.device_src_bytes, o.fingerprint_bytes, o.repaired_bytes,
                            o.verify_mismatches, o.expected_mismatches, t, digs)
