@@ -67,3 +67,61 @@ def test_ipc_peer_pull(tg, cpu):
         done.set()
         a.join(timeout=60)
     assert a.exitcode == 0
+
+
+def _reshard_model(tg):
+    return tg.make_model("ipc-reshard", 40_000_003, 2, 8192)
+
+
+def _shard_owner(q, done):
+    sys.path.insert(0, ROOT)
+    import paper_2512_01357_b200 as tg
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    m = _reshard_model(tg)
+    tp2 = [tg.shard_model(m, r, 2) for r in range(2)]
+    pool = tg.ReuseStore(tg.GpuSpec("gpu0", 48 << 20), device=0)
+    st = tg.ModelStatsTable()
+    with HostCheckpoint(tp2):
+        for sh in tp2:
+            st.record_request(sh.model_id, 0.0)
+            pool.load_model(sh, st, 0.0).value()
+            pool.end_instance(sh.model_id)
+    q.put((pool.export_ipc(), pool.index()))
+    done.wait(120)
+    pool.close()
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["K3+K1", "K3F"])
+def test_ipc_reshard_pull(tg, cpu, fused):
+    """Re-shard across processes: process A holds the TP2 shards; process B
+    attaches A's arena and index and loads the TP4 shards — every tensor
+    assembled from A's overlapping TP2 pieces (no host source registered in
+    B), fingerprints equal to the CPU restatement of the parent ranges."""
+    ctx = mp.get_context("spawn")
+    q, done = ctx.Queue(), ctx.Event()
+    a = ctx.Process(target=_shard_owner, args=(q, done))
+    a.start()
+    try:
+        handle, index = q.get(timeout=120)
+        m = _reshard_model(tg)
+        [tg.shard_model(m, r, 2) for r in range(2)]  # lineage of A's shards, known in this process too
+        tp4 = [tg.shard_model(m, r, 4) for r in range(4)]
+        pool = tg.ReuseStore(tg.GpuSpec("gpu1", 48 << 20), device=0)
+        pool.attach_remote(handle, index)
+        st = tg.ModelStatsTable()
+        for k, sh in enumerate(tp4):
+            assert pool.peer_reuse_size(sh) == sh.total_size
+            st.record_request(sh.model_id, float(k))
+            o = pool.load_model(sh, st, float(k), tg.LoadPolicy(flags=1 | 2 | 4 | (8 if fused else 0))).value()
+            assert o.peer_bytes == sh.total_size and o.pcie_bytes == 0
+            assert all(p.source == 3 for p in o.plan.placements)
+            for i, t in enumerate(sh.tensors):
+                parent, begin, size = tg.lineage(t.id)
+                want = cpu.content_fingerprint(cpu.synth(parent.hi, parent.lo, size, begin), threads=8)[0]
+                assert o.digests[i] == want
+            pool.end_instance(sh.model_id)
+        pool.close()
+    finally:
+        done.set()
+        a.join(timeout=60)
+    assert a.exitcode == 0
