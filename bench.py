@@ -447,6 +447,7 @@ def run_ours(args):
         free_c2_working_set()  # before the secondary configs
         for key, fn in (("c1", lambda: run_c1(tg, local, h2d_peak, hbm_peak)), ("c3", lambda: run_c3(tg, local)),
                         ("c5", lambda: run_c5(local)),
+                        ("c2_global_merge", lambda: run_c2_global_merge(tg, local, hbm_peak)),
                         ("per_model", lambda: run_per_model(tg, local, h2d_peak, hbm_peak))):
             try:  # a secondary config never takes the headline line down
                 extras[key] = fn()
@@ -713,6 +714,65 @@ def run_per_model(tg, dev, h2d_peak, hbm_peak):
     return {"workload": "every default_catalog() model: cold load into an empty pool from pinned host (PCIe), "
                         "then a 100%-reuse reload with every tensor fingerprint-verified in place (HBM); one "
                         "CUDA-event span per synchronous load, first-touch included", "models": rows}
+
+
+def run_c2_global_merge(tg, dev, hbm_peak, reps=3):
+    """C2's compaction stress case: the same switch under
+    LoadPolicy{merge=GlobalMerge} in a 36 GiB pool — load #3 relocates 13
+    tensors in 11 serial WAR waves, all gated inside one load-kernel launch.
+    HBM-resident sources, pool restored from a snapshot before each rep."""
+    from paper_2512_01357_b200 import _native as N
+    from paper_2512_01357_b200.checkpoint import DeviceBuffer
+    lib = N.lib
+    cat = catalog(tg)
+    seq = ["opt13B", "opt6.7B", "opt13B"]
+    bufs = []
+    for mid in seq[:2]:
+        for t in cat[mid].tensors:
+            b = DeviceBuffer(t.size, dev)
+            N.check_runtime(lib.tg_synth_fill_device(t.id.c(), 0, t.size, C.c_void_p(b.ptr), dev))
+            N.check_runtime(lib.tg_host_register(t.id.c(), C.c_void_p(b.ptr), t.size, None))
+            bufs.append((t.id, b))
+    pool = tg.ReuseStore(tg.GpuSpec("gpu0", 36 * GIB), device=dev)
+    policy = tg.LoadPolicy(merge=1, flags=1 | 2 | 8)
+
+    def stats(upto):
+        s = tg.ModelStatsTable()
+        for i, mid in enumerate(seq[:upto]):
+            s.record_request(mid, 10.0 * i)
+            s.set_load_bandwidth(mid, 55e9)
+        return s
+    try:
+        for i, mid in enumerate(seq[:2]):
+            pool.load_model(cat[mid], stats(i + 1), 10.0 * i, policy).value()
+            pool.end_instance(mid)
+        snap = pool.snapshot()
+        ms, kms, o = [], [], None
+        for r in range(reps + 1):
+            pool.restore(snap)
+            t, o = _event_ms(pool.stream(), dev, lambda: pool.load_model(cat[seq[2]], stats(3), 20.0, policy,
+                                                                          details=(r == 0)).value())
+            if r == 0:
+                plan = o.plan
+                continue
+            ms.append(t)
+            kms.append(o.timings["relocate_ms"])
+        snap = None
+        m, k = statistics.mean(ms), statistics.mean(kms)
+        moved = {x.tensor for x in plan.relocations}
+        untouched = sum(t.size for t in cat[seq[2]].tensors if t.id not in moved) - o.bytes_transferred
+        algo = 2 * o.bytes_merged + 2 * o.device_src_bytes + untouched
+        return {"workload": "C2 switch under GlobalMerge, 36 GiB pool, load #3 (opt13B), HBM sources",
+                "relocations": len(plan.relocations), "waves": o.waves, "bytes_merged": o.bytes_merged,
+                "bytes_transferred": o.bytes_transferred, "ms": m, "effective_GBps": cat[seq[2]].total_size / m / 1e6,
+                "load_kernel_ms": k, "load_kernel_GBps": algo / k / 1e6, "load_kernel_frac_of_hbm_peak":
+                    algo / k / 1e6 / hbm_peak, "algorithmic_bytes": algo,
+                "verify_mismatches": o.verify_mismatches}
+    finally:
+        pool.close()
+        for tid, b in bufs:
+            lib.tg_host_unregister(tid.c())
+            b.free()
 
 
 def run_c3(tg, dev):
