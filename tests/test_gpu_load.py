@@ -338,14 +338,14 @@ def test_model_store_file_sources(tg, cpu, tmp_path):
 
 
 @pytest.mark.parametrize("source", ["hbm", "host"])
-@pytest.mark.parametrize("seed", [52, 51, 13])
+@pytest.mark.parametrize("seed", [52, 51, 13, 7, 99, 1234])
 def test_fused_load_kernel_fuzz(tg, cpu, seed, source):
     """Odd-sized models rotating through a small pool: loads with up to 8 WAR
     waves, device-source placements gated on them and in-place verification,
     all in one load-kernel launch (TG_LOAD_FUSED).  Decisions and digests
     equal the unfused path (K3 waves + K1) load by load, and every resident
-    tensor's bytes equal the CPU restatement's.  (Seeds chosen on the control
-    plane for their wave counts.)"""
+    tensor's bytes equal the CPU restatement's.  (Seeds 52, 51 and 13 were
+    chosen on the control plane for their wave counts; the others are random.)"""
     import random
     from paper_2512_01357_b200.checkpoint import HostCheckpoint
     mb = 1 << 20
@@ -377,7 +377,7 @@ def test_fused_load_kernel_fuzz(tg, cpu, seed, source):
             for pool in pools.values():
                 pool.end_instance(m.model_id)
         assert pools[True].dump() == pools[False].dump()
-        assert waves >= 4
+        assert waves >= {52: 4, 51: 4, 13: 4}.get(seed, 1)  # the first seeds were picked for deep wave chains
     finally:
         for pool in pools.values():
             pool.close()
