@@ -80,6 +80,13 @@ __device__ __forceinline__ void cp_async16_noprefetch(void* smem, const void* gm
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
+// First `valid` (< 16) bytes only, the rest of the 16-byte slot zero-filled:
+// a source word that runs past the end of the tensor is never read beyond it
+// (registered device sources have no slack after them).
+__device__ __forceinline__ void cp_async16_partial(void* smem, const void* gmem, u32 valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid));
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     // L2::256B: the L2 fetches the whole 256-byte pair of lines, so a leaf's
@@ -390,7 +397,11 @@ __device__ __forceinline__ void copy_issue(uint4* stage_buf, const CopyTileRef& 
             if (l < tr.nfull) cp_async16(stage_buf + l * 8 + (q ^ (l & 7)), src_lane + static_cast<u64>(i) * 16384);
         }
     }
-    if (extra && lane < tr.nfull) cp_async16_noprefetch(stage_buf + 32 * kStageBlocks + lane, src_extra);
+    if (extra && lane < tr.nfull) {
+        const u64 left = tr.n - (extra_word - tr.o);  // tensor bytes from the word's start (> 0)
+        if (left >= 16) cp_async16_noprefetch(stage_buf + 32 * kStageBlocks + lane, src_extra);
+        else cp_async16_partial(stage_buf + 32 * kStageBlocks + lane, src_extra, static_cast<u32>(left));
+    }
     cp_async_commit();
 }
 
@@ -547,7 +558,22 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
                 const u32 ga = static_cast<u32>(reinterpret_cast<std::uintptr_t>(g0) & 15);
                 const uint4* gw = reinterpret_cast<const uint4*>(g0 - ga);
                 const u32 nw = static_cast<u32>((ga + (cur.t.n - from) + 15) / 16);
-                for (u32 w = lane; w < nw; w += 32) tb[w] = __ldg(gw + w);
+                const std::uint8_t* gend = cur.t.base + cur.t.n;
+                for (u32 w = lane; w < nw; w += 32) {
+                    const std::uint8_t* wa = reinterpret_cast<const std::uint8_t*>(gw + w);
+                    if (wa + 16 <= gend) {
+                        tb[w] = __ldg(gw + w);
+                    } else {  // the last word: only the bytes before the end of the tensor
+                        u64 lo = 0, hi = 0;
+                        for (u32 i = 0; wa + i < gend; ++i) {
+                            const u64 v = wa[i];
+                            if (i < 8) lo |= v << (8 * i);
+                            else hi |= v << (8 * (i - 8));
+                        }
+                        tb[w] = make_uint4(static_cast<u32>(lo), static_cast<u32>(lo >> 32), static_cast<u32>(hi),
+                                           static_cast<u32>(hi >> 32));
+                    }
+                }
                 __syncwarp();
                 const std::uint8_t* sbytes = reinterpret_cast<const std::uint8_t*>(tb) + ga;
                 if (lane == cur.t.nfull && pl < cur.t.n) {

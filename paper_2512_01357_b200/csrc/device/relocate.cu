@@ -48,13 +48,31 @@ __device__ __forceinline__ uint4 realign(uint4 w0, uint4 w1, u32 r8) {
     return o;
 }
 
+// The aligned source word after the body: only its first `valid` bytes lie
+// inside the source range (the move's tail bytes included), so it is read
+// byte by byte when the rest would run past the end of the source —
+// registered device sources (an HBM model cache) have no slack after them.
+__device__ __forceinline__ uint4 load_last_word(const uint4* p, u32 valid) {
+    if (valid >= 16) return __ldcs(p);
+    u64 lo = 0, hi = 0;
+    const std::uint8_t* b = reinterpret_cast<const std::uint8_t*>(p);
+    for (u32 i = 0; i < valid; ++i) {
+        const u64 v = b[i];
+        if (i < 8) lo |= v << (8 * i);
+        else hi |= v << (8 * (i - 8));
+    }
+    return make_uint4(static_cast<u32>(lo), static_cast<u32>(lo >> 32), static_cast<u32>(hi),
+                      static_cast<u32>(hi >> 32));
+}
+
 // Copy destination words [w_begin, w_end) of one move.  `sa` is the aligned
 // source word holding the byte that lands on destination word 0, `o` the
 // byte offset inside it.  Q = o >> 2 selects the unrolled realignment; Q < 0
-// means co-aligned (o == 0).
+// means co-aligned (o == 0).  `last_valid`: bytes of word sa[w_total] inside
+// the source range.
 template <int Q>
 __device__ __forceinline__ void copy_words(const uint4* __restrict__ sa, uint4* __restrict__ da, u64 w_begin,
-                                           u64 w_end, u32 r8, u32 lane) {
+                                           u64 w_end, u64 w_total, u32 last_valid, u32 r8, u32 lane) {
     for (u64 g = w_begin; g < w_end; g += 32 * kUnroll) {
         uint4 cur[kUnroll], nxt[kUnroll];
 #pragma unroll
@@ -67,7 +85,8 @@ __device__ __forceinline__ void copy_words(const uint4* __restrict__ sa, uint4* 
             for (int u = 0; u < kUnroll; ++u) {
                 const u64 wi = g + u * 32 + lane;
                 nxt[u] = shfl_down4(cur[u]);
-                if (wi < w_end && (lane == 31 || wi + 1 == w_end)) nxt[u] = __ldcs(sa + wi + 1);
+                if (wi < w_end && (lane == 31 || wi + 1 == w_end))
+                    nxt[u] = wi + 1 == w_total ? load_last_word(sa + wi + 1, last_valid) : __ldcs(sa + wi + 1);
             }
         }
 #pragma unroll
@@ -114,11 +133,12 @@ __global__ void __launch_bounds__(256) relocate_kernel(const __grid_constant__ R
         const uint4* sa = reinterpret_cast<const uint4*>(s0 - o);
         uint4* da = reinterpret_cast<uint4*>(d0);
         const u32 r8 = (o & 3) * 8;
-        if (o == 0) copy_words<-1>(sa, da, wb, we, 0, lane);
-        else if (o < 4) copy_words<0>(sa, da, wb, we, r8, lane);
-        else if (o < 8) copy_words<1>(sa, da, wb, we, r8, lane);
-        else if (o < 12) copy_words<2>(sa, da, wb, we, r8, lane);
-        else copy_words<3>(sa, da, wb, we, r8, lane);
+        const u32 lv = o + static_cast<u32>(tail);  // source bytes in word sa[nw]
+        if (o == 0) copy_words<-1>(sa, da, wb, we, nw, lv, 0, lane);
+        else if (o < 4) copy_words<0>(sa, da, wb, we, nw, lv, r8, lane);
+        else if (o < 8) copy_words<1>(sa, da, wb, we, nw, lv, r8, lane);
+        else if (o < 12) copy_words<2>(sa, da, wb, we, nw, lv, r8, lane);
+        else copy_words<3>(sa, da, wb, we, nw, lv, r8, lane);
     }
 }
 

@@ -12,6 +12,8 @@ echo "## memcheck: copy_fingerprint_fused at partial-leaf sizes"
 timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest tests/test_gpu_kernels.py -q -k "copy_fingerprint_fused and (4097 or 135169 or 656359) and (16 or 112)" 2>&1 | tail -4
 echo "## memcheck: K4D device KV batches"
 timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest -q "tests/test_gpu_kv_device.py::test_device_batches_equal_reference[1]" tests/test_gpu_kv_device.py::test_device_batches_in_a_cuda_graph 2>&1 | tail -4
+echo "## memcheck: fused vs unfused load fuzz (K3 device-source placements), re-shard, paged cache, peer pulls"
+timeout 1500 $S --tool memcheck --error-exitcode 1 python -m pytest -q "tests/test_gpu_load.py::test_fused_load_kernel_fuzz[52-hbm]" tests/test_gpu_reshard.py::test_reshard_from_own_pool "tests/test_gpu_kv_device.py::test_block_tables_drive_a_paged_cache[48]" tests/test_gpu_load.py::test_peer_pull_same_device 2>&1 | tail -4
 echo "## racecheck: load kernel ring"
 timeout 900 $S --tool racecheck python -m pytest -q "tests/test_gpu_kernels.py::test_copy_fingerprint_fused[16-3-11-135169]" "tests/test_gpu_kernels.py::test_copy_fingerprint_fused[112-0-8-656359]" 2>&1 | tail -4
 echo "## synccheck: load kernel ring"
