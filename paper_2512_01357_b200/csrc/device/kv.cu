@@ -406,6 +406,8 @@ public:
         reserve_buf(&d_runs_, &runs_cap_, 2 * std::max<u64>(nr, 1));
         reserve_buf(&d_slots_, &slots_cap_, 3 * std::max<u64>(slots, 1));
         reserve_bytes(&d_log_, &log_cap_, entry * a.max_batches);
+        // whole entries are read back at sync (unused request / piece space too)
+        TG_CUDA(cudaMemsetAsync(d_log_, 0, entry * a.max_batches, s_));
         if (!d_ctl_) TG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_ctl_), sizeof(KvDevCtl), s_));
         std::vector<u64> h(2 * nr + 2 * slots);
         std::copy(a.run_off.begin(), a.run_off.end(), h.begin());

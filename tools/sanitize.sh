@@ -18,5 +18,9 @@ echo "## racecheck: load kernel ring"
 timeout 900 $S --tool racecheck python -m pytest -q "tests/test_gpu_kernels.py::test_copy_fingerprint_fused[16-3-11-135169]" "tests/test_gpu_kernels.py::test_copy_fingerprint_fused[112-0-8-656359]" 2>&1 | tail -4
 echo "## synccheck: load kernel ring"
 timeout 900 $S --tool synccheck python -m pytest -q "tests/test_gpu_kernels.py::test_copy_fingerprint_fused[16-3-11-135169]" "tests/test_gpu_kernels.py::test_copy_fingerprint_fused[112-0-8-656359]" 2>&1 | tail -4
+echo "## racecheck / synccheck / initcheck: K4D, batched moves, device index (+ load fuzz, C1, peer pulls for initcheck)"
+timeout 900 $S --tool racecheck python -m pytest -q tests/test_gpu_kv_device.py "tests/test_gpu_kernels.py::test_copy_fingerprint_batched_moves" tests/test_gpu_index.py 2>&1 | tail -2
+timeout 900 $S --tool synccheck python -m pytest -q tests/test_gpu_kv_device.py "tests/test_gpu_kernels.py::test_copy_fingerprint_batched_moves" tests/test_gpu_index.py 2>&1 | tail -2
+timeout 1500 $S --tool initcheck python -m pytest -q tests/test_gpu_kv_device.py "tests/test_gpu_kernels.py::test_copy_fingerprint_batched_moves" tests/test_gpu_index.py "tests/test_gpu_load.py::test_fused_load_kernel_fuzz[52-hbm]" tests/test_gpu_load.py::test_c1_cold_then_warm_from_host tests/test_gpu_load.py::test_peer_pull_same_device 2>&1 | tail -2
 } > $OUT
 cat $OUT
