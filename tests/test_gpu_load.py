@@ -419,3 +419,61 @@ def test_edge_models_match_reference(tg, ref, cpu):
             t += 1.0
     assert mine.validate().ok()
     mine.close()
+
+
+def test_concurrent_load_kernels_on_one_gpu(tg, ref):
+    """Two pools on one GPU load concurrently from two host threads (ctypes
+    drops the GIL), each with multi-wave GlobalMerge plans: the gated load
+    kernels share the SMs without deadlock (a gated tile only waits for tiles
+    taken earlier by running warps), and both pools end equal to the
+    reference with every reused tensor verified."""
+    import random
+    import threading
+    mb = 1 << 20
+    rng = random.Random(52)
+    models = [tg.make_model(f"cc_{k}", rng.randrange(40 * mb, 90 * mb) | 1, rng.randrange(2, 6), 64) for k in range(4)]
+    size = rng.randrange(120 * mb, 170 * mb)
+    seq = [rng.randrange(4) for _ in range(12)]
+    cache = HbmCache(tg, models)
+    pools = [tg.ReuseStore(tg.GpuSpec(f"gpu{i}", size), device=0) for i in range(2)]
+    errors, waves = [], [0, 0]
+
+    def run(i):
+        try:
+            st = tg.ModelStatsTable()
+            for j, k in enumerate(seq):
+                m = models[k]
+                st.record_request(m.model_id, 10.0 * j)
+                st.set_load_bandwidth(m.model_id, 55e9)
+                r = pools[i].load_model(m, st, 10.0 * j, tg.LoadPolicy(merge=1))
+                if r.ok():
+                    assert r.value().verify_mismatches == 0
+                    waves[i] = max(waves[i], r.value().waves)
+                pools[i].end_instance(m.model_id)
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+    try:
+        threads = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=300)
+        assert not errors and not any(t.is_alive() for t in threads)
+        theirs = ref.ReuseStore(size)
+        rs = ref.ModelStatsTable()
+        for j, k in enumerate(seq):
+            m = models[k]
+            rs.record_request(m.model_id, 10.0 * j)
+            rs.set_load_bandwidth(m.model_id, 55e9)
+            theirs.load_model(m.to_json(), rs, 10.0 * j, merge=1)
+            theirs.end_instance(m.model_id)
+        for p in pools:
+            d, r = p.dump(), theirs.dump()
+            d.pop("gpu_id", None), r.pop("gpu_id", None)
+            assert d == r
+            assert p.validate().ok()
+        assert max(waves) >= 2
+    finally:
+        for p in pools:
+            p.close()
+        cache.close()
