@@ -477,3 +477,45 @@ def test_concurrent_load_kernels_on_one_gpu(tg, ref):
         for p in pools:
             p.close()
         cache.close()
+
+
+def test_kv_pressure_reclaims_tensors_then_reload(tg, ref, cpu):
+    """On-demand KV under pressure (urgent reclaim, kv_engine.hpp:183-194)
+    evicts resident tensors of an idle model on a device pool; after the KV
+    teardown the model reloads — evicted tensors re-sent, survivors verified in
+    place — every step equal to the reference, and every resident tensor's
+    bytes equal to the CPU restatement."""
+    mb = 1 << 20
+    idle = tg.make_model("idle", 90 * mb + 7, 3, 64)
+    busy = tg.make_model("busy", 30 * mb + 3, 2, 4096)
+    size = 150 * mb
+    cache = HbmCache(tg, [idle, busy])
+    mine, theirs = tg.ReuseStore(tg.GpuSpec(pool_size=size), device=0), ref.ReuseStore(size)
+    sm, sr = tg.ModelStatsTable(), ref.ModelStatsTable()
+    expected = {}
+    try:
+        for t, m in ((0.0, idle), (1.0, busy)):
+            sm.record_request(m.model_id, t)
+            sr.record_request(m.model_id, t)
+            assert mine.load_model(m, sm, t).ok() and theirs.load_model(m.to_json(), sr, t)["ok"]
+        mine.end_instance(idle.model_id)
+        theirs.end_instance(idle.model_id)
+        kvm, kvr = tg.KvEngine("busy", 16, 4096), ref.KvEngine("busy", 16, 4096)
+        reqs = [(i + 1, 2000) for i in range(8)]  # 8 x 125 blocks x 64 KiB: forces reclaim
+        a, b = kvm.batch_allocate(mine, sm, reqs), kvr.batch_allocate(theirs, sr, reqs)
+        assert a.ok() == b["ok"]
+        assert kvm.stats().reclaim_events == kvr.state()["stats"]["reclaim_events"] >= 1
+        assert mine.dump() == theirs.dump()
+        _check_pooled_bytes(tg, cpu, mine, expected)
+        kvm.instance_teardown(mine)
+        kvr.instance_teardown(theirs)
+        sm.record_request(idle.model_id, 2.0)
+        sr.record_request(idle.model_id, 2.0)
+        o = mine.load_model(idle, sm, 2.0).value()
+        r = theirs.load_model(idle.to_json(), sr, 2.0)
+        assert o.bytes_transferred == r["bytes_transferred"] > 0 and o.verify_mismatches == 0
+        assert mine.dump() == theirs.dump()
+        _check_pooled_bytes(tg, cpu, mine, expected)
+    finally:
+        mine.close()
+        cache.close()
