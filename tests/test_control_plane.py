@@ -114,21 +114,36 @@ def test_c1_cold_then_warm(tg):
 
 # ---- live differential fuzz against the compiled reference -------------------------
 
-def _small_catalog(tg, rnd, n_models):
+def _small_catalog(tg, rnd, n_models, scale=1):
     models = []
     for i in range(n_models):
-        total = rnd.randint(2_000, 60_000)
+        total = rnd.randint(2_000, 60_000) * scale + (rnd.randint(0, scale - 1) if scale > 1 else 0)
         layers = rnd.randint(1, 5)
         models.append(tg.make_model(f"m{i}", total, layers, rnd.choice([0, 16, 64]),
                                     latency_sensitivity=rnd.choice([1.0, 0.5, 0.25])))
     return models
 
 
-def _fuzz_once(tg, ref, seed, n_ops=120):
+def _fuzz_once(tg, ref, seed, n_ops=120, device=None, scale=1, sources=None, on_step=None):
+    """Random op mix on our store and the compiled reference, compared after
+    every op.  With a device: a pool in HBM whose bytes come from
+    sources(models) (a context manager), load flags drawn from a second
+    stream, and on_step(pool, outcome) checking the bytes."""
     rnd = random.Random(seed)
-    models = _small_catalog(tg, rnd, rnd.randint(2, 6))
-    pool = rnd.randint(40_000, 150_000)
-    mine = tg.ReuseStore(tg.GpuSpec(pool_size=pool, pcie_bandwidth=rnd.choice([55e9, 12e9])), device=None)
+    frnd = random.Random(~seed)
+    models = _small_catalog(tg, rnd, rnd.randint(2, 6), scale)
+    pool = rnd.randint(40_000, 150_000) * scale
+    mine = tg.ReuseStore(tg.GpuSpec(pool_size=pool, pcie_bandwidth=rnd.choice([55e9, 12e9])), device=device)
+    src = sources(models) if sources is not None else None
+    try:
+        _fuzz_ops(tg, ref, seed, n_ops, rnd, frnd, models, pool, mine, device, on_step)
+    finally:
+        if src is not None:
+            src.close()
+        mine.close()
+
+
+def _fuzz_ops(tg, ref, seed, n_ops, rnd, frnd, models, pool, mine, device, on_step):
     theirs = ref.ReuseStore(pool, pcie=mine.spec.pcie_bandwidth)
     s_m, s_r = tg.ModelStatsTable(), ref.ModelStatsTable()
     rng_m, rng_r = tg.Rng(seed), ref.Rng(seed)
@@ -137,6 +152,7 @@ def _fuzz_once(tg, ref, seed, n_ops=120):
     for step in range(n_ops):
         op = rnd.random()
         m = rnd.choice(models)
+        r = None
         if op < 0.45:
             t += rnd.choice([0.0, 0.5, 1.0, 10.0])
             s_m.record_request(m.model_id, t)
@@ -146,8 +162,10 @@ def _fuzz_once(tg, ref, seed, n_ops=120):
                 s_m.set_load_bandwidth(m.model_id, bw)
                 s_r.set_load_bandwidth(m.model_id, bw)
             merge, strict, rand_ev = rnd.random() < 0.2, rnd.random() < 0.2, rnd.random() < 0.15
-            a = result_json(mine.load_model(m, s_m, t, tg.LoadPolicy(merge=int(merge), strictness=int(strict),
-                                                                     random_eviction=rand_ev, rng=rng_m)))
+            flags = frnd.choice([11, 3, 1, 9, 2 | 8]) if device is not None else 11
+            r = mine.load_model(m, s_m, t, tg.LoadPolicy(merge=int(merge), strictness=int(strict),
+                                                         random_eviction=rand_ev, rng=rng_m, flags=flags))
+            a = result_json(r)
             b = theirs.load_model(m.to_json(), s_r, t, merge=int(merge), strictness=int(strict),
                                   random_eviction=rand_ev, rng=rng_r)
             assert a == b, (seed, step, "load")
@@ -191,6 +209,8 @@ def _fuzz_once(tg, ref, seed, n_ops=120):
                 assert (0 if a.ok() else int(a.error()) + 1) == b
         assert mine.validate().ok()
         assert mine.dump() == theirs.dump(), (seed, step)
+        if on_step is not None:
+            on_step(mine, r)
         mi, ri = mine.info(), theirs.info()
         for k in ("free_bytes", "kv_bytes", "pinned_bytes", "reusable_bytes", "bytes_merged_total",
                   "bytes_transferred_total", "evictions_total", "region_count", "largest_free"):

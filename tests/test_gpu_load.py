@@ -11,7 +11,7 @@ import os
 import numpy as np
 import pytest
 
-from test_control_plane import result_json
+from test_control_plane import _fuzz_once, result_json
 
 pytestmark = pytest.mark.gpu
 
@@ -519,3 +519,38 @@ def test_kv_pressure_reclaims_tensors_then_reload(tg, ref, cpu):
     finally:
         mine.close()
         cache.close()
+
+
+SOAK_SEEDS = int(os.environ.get("TANGRAM_SOAK_SEEDS", "6"))
+
+
+@pytest.mark.parametrize("seed", range(SOAK_SEEDS))
+def test_device_store_differential_fuzz(tg, ref, cpu, seed):
+    """The control-plane differential fuzz (loads under every merge /
+    strictness / random-eviction policy, end_instance, evict_tensor,
+    evict_model, move_tensor, KV regions) on a device pool with real bytes:
+    every op equals the reference (outcome, dump, accessors), load flags are
+    drawn from {verify+fingerprint+fused, unfused, verify-only, fused}, and
+    after every op each resident tensor's device bytes fingerprint to the CPU
+    restatement's digest of its checkpoint bytes (and to the digest the pool
+    recorded, when it has one).  TANGRAM_SOAK_SEEDS widens the seed range."""
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    expected = {}
+
+    def sources(models):
+        return HbmCache(tg, models) if seed % 2 else HostCheckpoint(models)
+
+    def on_step(pool, r):
+        if r is not None and r.ok():
+            o = r.value()
+            assert o.verify_mismatches == 0 and o.repaired_bytes == 0
+        for e in pool.dump()["tensor_map"]:
+            tid = tg.TensorId.from_hex(e["tensor"])
+            if tid not in expected:
+                expected[tid] = _expected_digest(cpu, tid, e["size"])
+            assert pool.fingerprint_tensor(tid) == expected[tid], (seed, e)
+            info = pool.tensor_info(tid)
+            if info["has_digest"]:
+                assert info["digest"] == expected[tid], (seed, e)
+
+    _fuzz_once(tg, ref, 1000 + seed, n_ops=150, device=0, scale=257, sources=sources, on_step=on_step)
