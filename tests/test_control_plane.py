@@ -124,26 +124,27 @@ def _small_catalog(tg, rnd, n_models, scale=1):
     return models
 
 
-def _fuzz_once(tg, ref, seed, n_ops=120, device=None, scale=1, sources=None, on_step=None):
+def _fuzz_once(tg, ref, seed, n_ops=120, device=None, scale=1, sources=None, on_step=None, extra_flags=0):
     """Random op mix on our store and the compiled reference, compared after
     every op.  With a device: a pool in HBM whose bytes come from
-    sources(models) (a context manager), load flags drawn from a second
-    stream, and on_step(pool, outcome) checking the bytes."""
+    sources(models, pool) (anything with close()), load flags drawn from a
+    second stream (| extra_flags), and on_step(pool, outcome) checking the
+    bytes."""
     rnd = random.Random(seed)
     frnd = random.Random(~seed)
     models = _small_catalog(tg, rnd, rnd.randint(2, 6), scale)
     pool = rnd.randint(40_000, 150_000) * scale
     mine = tg.ReuseStore(tg.GpuSpec(pool_size=pool, pcie_bandwidth=rnd.choice([55e9, 12e9])), device=device)
-    src = sources(models) if sources is not None else None
+    src = sources(models, mine) if sources is not None else None
     try:
-        _fuzz_ops(tg, ref, seed, n_ops, rnd, frnd, models, pool, mine, device, on_step)
+        _fuzz_ops(tg, ref, seed, n_ops, rnd, frnd, models, pool, mine, device, on_step, extra_flags)
     finally:
         if src is not None:
             src.close()
         mine.close()
 
 
-def _fuzz_ops(tg, ref, seed, n_ops, rnd, frnd, models, pool, mine, device, on_step):
+def _fuzz_ops(tg, ref, seed, n_ops, rnd, frnd, models, pool, mine, device, on_step, extra_flags):
     theirs = ref.ReuseStore(pool, pcie=mine.spec.pcie_bandwidth)
     s_m, s_r = tg.ModelStatsTable(), ref.ModelStatsTable()
     rng_m, rng_r = tg.Rng(seed), ref.Rng(seed)
@@ -162,7 +163,7 @@ def _fuzz_ops(tg, ref, seed, n_ops, rnd, frnd, models, pool, mine, device, on_st
                 s_m.set_load_bandwidth(m.model_id, bw)
                 s_r.set_load_bandwidth(m.model_id, bw)
             merge, strict, rand_ev = rnd.random() < 0.2, rnd.random() < 0.2, rnd.random() < 0.15
-            flags = frnd.choice([11, 3, 1, 9, 2 | 8]) if device is not None else 11
+            flags = (frnd.choice([11, 3, 1, 9, 2 | 8]) | extra_flags) if device is not None else 11
             r = mine.load_model(m, s_m, t, tg.LoadPolicy(merge=int(merge), strictness=int(strict),
                                                          random_eviction=rand_ev, rng=rng_m, flags=flags))
             a = result_json(r)

@@ -537,9 +537,14 @@ def test_device_store_differential_fuzz(tg, ref, cpu, seed):
     from paper_2512_01357_b200.checkpoint import HostCheckpoint
     expected = {}
 
-    def sources(models):
+    def sources(models, pool):
         return HbmCache(tg, models) if seed % 2 else HostCheckpoint(models)
 
+    _fuzz_once(tg, ref, 1000 + seed, n_ops=150, device=0, scale=257, sources=sources,
+               on_step=_soak_checker(tg, cpu, seed, {}))
+
+
+def _soak_checker(tg, cpu, seed, expected, peer_bytes=None):
     def on_step(pool, r):
         if r is not None and r.ok():
             o = r.value()
@@ -552,5 +557,44 @@ def test_device_store_differential_fuzz(tg, ref, cpu, seed):
             info = pool.tensor_info(tid)
             if info["has_digest"]:
                 assert info["digest"] == expected[tid], (seed, e)
+        if r is not None and r.ok() and peer_bytes is not None:
+            peer_bytes.append(r.value().peer_bytes)
+    return on_step
 
-    _fuzz_once(tg, ref, 1000 + seed, n_ops=150, device=0, scale=257, sources=sources, on_step=on_step)
+
+class _PeerHolder:
+    """A second device pool holding every model (loaded from an HBM cache that
+    is then dropped), attached as the fuzz pool's peer: the fuzz pool's misses
+    can only be served over the peer mapping."""
+
+    def __init__(self, tg, models, pool, size):
+        self.peer = tg.ReuseStore(tg.GpuSpec("peer", size), device=0)
+        cache = HbmCache(tg, models)
+        try:
+            st = tg.ModelStatsTable()
+            for i, m in enumerate(models):
+                st.record_request(m.model_id, float(i))
+                assert self.peer.load_model(m, st, float(i)).ok()
+                self.peer.end_instance(m.model_id)
+        finally:
+            cache.close()
+        pool.add_peer(self.peer)
+
+    def close(self):
+        self.peer.close()
+
+
+@pytest.mark.parametrize("seed", range(max(1, SOAK_SEEDS // 2)))
+def test_device_store_fuzz_peer_sourced(tg, ref, cpu, seed):
+    """The same fuzz with no registered byte source: every miss is pulled from
+    a peer pool that holds all models (TG_LOAD_PEER).  Decisions still equal
+    the reference's, the pulled bytes fingerprint to the CPU restatement, and
+    the misses are counted as peer bytes."""
+    pulled = []
+
+    def sources(models, pool):
+        return _PeerHolder(tg, models, pool, sum(m.total_size for m in models) + (1 << 20))
+
+    _fuzz_once(tg, ref, 2000 + seed, n_ops=120, device=0, scale=257, sources=sources,
+               on_step=_soak_checker(tg, cpu, seed, {}, pulled), extra_flags=4)
+    assert sum(pulled) > 0
