@@ -17,6 +17,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "../host/murmur_mix.hpp"
 #include "kernels.hpp"
@@ -121,13 +122,14 @@ __device__ __forceinline__ void cp_async_wait() {
 constexpr int kV3StageWords = 32 * kStageBlocks + 32;  // slots + extra column
 
 template <int Q>
-__device__ __forceinline__ void v3_hash_stage(const uint4* stage_buf, u32 lane, u32 r8, mm::W32& h1, mm::W32& h2) {
+__device__ __forceinline__ void v3_hash_stage(const uint4* stage_buf, const uint4* xw, u32 lane, u32 r8, mm::W32& h1,
+                                              mm::W32& h2) {
     const uint4* slot = stage_buf + lane * 8;
     const u32 key = lane & 7;
     uint4 w[kSlotWords];
 #pragma unroll
     for (int q = 0; q < kStageBlocks; ++q) w[q] = lds128(slot + (q ^ key));
-    w[kStageBlocks] = lds128(stage_buf + 32 * kStageBlocks + lane);
+    w[kStageBlocks] = lds128(xw);
 #pragma unroll
     for (int b = 0; b < kStageBlocks; ++b) {
         const u32 u[8] = {w[b].x, w[b].y, w[b].z, w[b].w, w[b + 1].x, w[b + 1].y, w[b + 1].z, w[b + 1].w};
@@ -162,18 +164,20 @@ struct TileRef {
     int task;
 };
 
-__device__ __forceinline__ void v4_hash(const uint4* stage_buf, const TileRef& tr, u32 lane, mm::W32& h1,
-                                        mm::W32& h2) {
+// xw: the leaf's 9th word — the extra column, or word 0 of the leaf's next
+// stage when that stage has landed in the ring.
+__device__ __forceinline__ void v4_hash(const uint4* stage_buf, const uint4* xw, const TileRef& tr, u32 lane,
+                                        mm::W32& h1, mm::W32& h2) {
     if (tr.o == 0) {
         v3_hash_stage_aligned(stage_buf, lane, h1, h2);
         return;
     }
     const u32 r8 = (tr.o & 3) * 8;
     switch (tr.o >> 2) {
-        case 0: v3_hash_stage<0>(stage_buf, lane, r8, h1, h2); break;
-        case 1: v3_hash_stage<1>(stage_buf, lane, r8, h1, h2); break;
-        case 2: v3_hash_stage<2>(stage_buf, lane, r8, h1, h2); break;
-        default: v3_hash_stage<3>(stage_buf, lane, r8, h1, h2); break;
+        case 0: v3_hash_stage<0>(stage_buf, xw, lane, r8, h1, h2); break;
+        case 1: v3_hash_stage<1>(stage_buf, xw, lane, r8, h1, h2); break;
+        case 2: v3_hash_stage<2>(stage_buf, xw, lane, r8, h1, h2); break;
+        default: v3_hash_stage<3>(stage_buf, xw, lane, r8, h1, h2); break;
     }
 }
 
@@ -372,6 +376,7 @@ __device__ __forceinline__ void write_lines_dispatch(const uint4* cur_buf, const
 
 // The extra (9th) word of every leaf-stage is needed by the writes whenever
 // delta > 0, by the hash whenever o > 0; load it when it holds a tensor byte.
+template <bool FP_NEXT = false>
 __device__ __forceinline__ void copy_issue(uint4* stage_buf, const CopyTileRef& c, int s, u32 lane) {
     const TileRef& tr = c.t;
     if (tr.task < 0 || tr.nfull == 0) {
@@ -381,7 +386,7 @@ __device__ __forceinline__ void copy_issue(uint4* stage_buf, const CopyTileRef& 
     const std::uint8_t* src_lane =
         tr.a0 + static_cast<u64>(lane >> 3) * kLeafBytes + (lane & 7) * 16 + static_cast<u64>(s) * 128;
     const u64 extra_word = (tr.leaf0 + lane) * kLeafBytes + static_cast<u64>(s) * 128 + 128;  // tensor offset + o
-    const bool extra = (tr.o != 0 || c.delta != 0) && extra_word - tr.o < tr.n;
+    const bool extra = (tr.o != 0 || c.delta != 0) && (!FP_NEXT || s == kStagesPerLeaf - 1) && extra_word - tr.o < tr.n;
     const std::uint8_t* src_extra = tr.a0 + static_cast<u64>(lane) * kLeafBytes + static_cast<u64>(s) * 128 + 128;
     const u32 leaf_in_group = lane >> 3, q = lane & 7;
     if (tr.nfull == 32) {
@@ -439,8 +444,9 @@ __device__ __forceinline__ u64 next_tile(unsigned long long* counter, u32 lane) 
 //    two or three stages are in flight.
 //  * Fingerprint-only launches (K1), or TANGRAM_LOAD_RING=single: one line per
 //    stage; a line reads s - 1 and s, and two stages are in flight.
-template <int STAGES, int WARPS, bool PAIR>
+template <int STAGES, int WARPS, bool PAIR, bool NEXT = false>
 struct CopyCfg {
+    static constexpr bool kNext = NEXT;
     static constexpr int kStages = STAGES;
     static constexpr int kWarps = WARPS;
     static constexpr bool kPair = PAIR;
@@ -450,6 +456,7 @@ struct CopyCfg {
 };
 using CfgSingle = CopyCfg<4, 6, false>;
 using CfgPair = CopyCfg<4, 6, true>;
+using CfgFpNext = CopyCfg<4, 6, false, true>;
 
 template <class Task, class Cfg>
 __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
@@ -468,9 +475,14 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
     int cur_task = -1;
     u64 acc_h = 0, acc_l = 0;
     u32 buf = 0;
+    // Fingerprint-only single ring: a stage's 9th words are word 0 of the
+    // next stage (waited for before hashing), so only the leaf's last stage
+    // loads the extra column — one uncoalesced 32-line request per leaf
+    // instead of one per stage.
+    constexpr bool kFpNext = std::is_same<Task, FpTask>::value && Cfg::kNext && !Cfg::kPair;
     constexpr int kPrologue = Cfg::kPair ? 3 : kAhead;  // stages 0 .. kPrologue - 1 before the loop
 #pragma unroll
-    for (int s = 0; s < kPrologue; ++s) copy_issue(wbuf + s * kV3StageWords, cur, s, lane);
+    for (int s = 0; s < kPrologue; ++s) copy_issue<kFpNext>(wbuf + s * kV3StageWords, cur, s, lane);
     while (cur.t.task >= 0) {
         if (cur.t.task != cur_task) {
             if (cur_task >= 0) {
@@ -498,8 +510,8 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
         // reads any more: that of s - 1 (single lines) or s - 2 (pairs).
         auto issue = [&](int stage, int slot) {
             uint4* dst = wbuf + slot * kV3StageWords;
-            if (stage < kStagesPerLeaf) copy_issue(dst, cur, stage, lane);
-            else copy_issue(dst, nxt, stage - kStagesPerLeaf, lane);
+            if (stage < kStagesPerLeaf) copy_issue<kFpNext>(dst, cur, stage, lane);
+            else copy_issue<kFpNext>(dst, nxt, stage - kStagesPerLeaf, lane);
         };
         for (int s = 0; s < kStagesPerLeaf; ++s) {
             const uint4* sb = wbuf + buf * kV3StageWords;
@@ -523,14 +535,24 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
                     issue(s + 2, static_cast<int>(b2));
                     issue(s + 3, static_cast<int>(b1));
                 }
-                if (lane < cur.t.nfull) v4_hash(sb, cur.t, lane, h1, h2);
+                if (lane < cur.t.nfull) v4_hash(sb, sb + 32 * kStageBlocks + lane, cur.t, lane, h1, h2);
+            } else if constexpr (kFpNext) {
+                // slot of s - 1 is free (no line stores): refill first, then
+                // wait for s and s + 1
+                issue(s + kAhead, static_cast<int>((buf + kAhead) % kStagesRing));
+                cp_async_wait<kAhead - 1>();
+                __syncwarp();
+                const uint4* nb = wbuf + ((buf + 1) % kStagesRing) * kV3StageWords;
+                const uint4* xw = s < kStagesPerLeaf - 1 ? nb + lane * 8 + (lane & 7) : sb + 32 * kStageBlocks + lane;
+                if (lane < cur.t.nfull) v4_hash(sb, xw, cur.t, lane, h1, h2);
+                __syncwarp();
             } else {
                 cp_async_wait<kAhead - 1>();
                 __syncwarp();
                 if (writes && cur.t.nfull) write_lines_dispatch(sb, sp, cur, s, true, s > 0, lane);
                 if (s == kStagesPerLeaf - 1 && writes && cur.t.nfull && cur.k)
                     write_lines_dispatch(nullptr, sb, cur, kStagesPerLeaf, false, true, lane);
-                if (lane < cur.t.nfull) v4_hash(sb, cur.t, lane, h1, h2);
+                if (lane < cur.t.nfull) v4_hash(sb, sb + 32 * kStageBlocks + lane, cur.t, lane, h1, h2);
                 __syncwarp();
                 issue(s + kAhead, static_cast<int>((buf + kAhead) % kStagesRing));
             }
@@ -656,7 +678,10 @@ template <class Task>
 void load_kernel_launch(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_sync,
                         const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed,
                         bool writes) {
-    if (writes && pair_ring())
+    if (!writes && !(std::getenv("TANGRAM_FP_NEXT") && std::strcmp(std::getenv("TANGRAM_FP_NEXT"), "0") == 0))
+        load_kernel_launch_cfg<Task, CfgFpNext>(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves,
+                                                sm_count, s, sync_zeroed);
+    else if (writes && pair_ring())
         load_kernel_launch_cfg<Task, CfgPair>(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves,
                                               sm_count, s, sync_zeroed);
     else
