@@ -376,8 +376,7 @@ __device__ __forceinline__ void write_lines_dispatch(const uint4* cur_buf, const
 
 // The extra (9th) word of every leaf-stage is needed by the writes whenever
 // delta > 0, by the hash whenever o > 0; load it when it holds a tensor byte.
-template <bool FP_NEXT = false>
-__device__ __forceinline__ void copy_issue(uint4* stage_buf, const CopyTileRef& c, int s, u32 lane) {
+__device__ __forceinline__ void copy_issue(uint4* stage_buf, const CopyTileRef& c, int s, u32 lane, bool next_words) {
     const TileRef& tr = c.t;
     if (tr.task < 0 || tr.nfull == 0) {
         cp_async_commit();
@@ -386,7 +385,7 @@ __device__ __forceinline__ void copy_issue(uint4* stage_buf, const CopyTileRef& 
     const std::uint8_t* src_lane =
         tr.a0 + static_cast<u64>(lane >> 3) * kLeafBytes + (lane & 7) * 16 + static_cast<u64>(s) * 128;
     const u64 extra_word = (tr.leaf0 + lane) * kLeafBytes + static_cast<u64>(s) * 128 + 128;  // tensor offset + o
-    const bool extra = (tr.o != 0 || c.delta != 0) && (!FP_NEXT || s == kStagesPerLeaf - 1) && extra_word - tr.o < tr.n;
+    const bool extra = (tr.o != 0 || c.delta != 0) && (!next_words || s == kStagesPerLeaf - 1) && extra_word - tr.o < tr.n;
     const std::uint8_t* src_extra = tr.a0 + static_cast<u64>(lane) * kLeafBytes + static_cast<u64>(s) * 128 + 128;
     const u32 leaf_in_group = lane >> 3, q = lane & 7;
     if (tr.nfull == 32) {
@@ -461,7 +460,7 @@ using CfgFpNext = CopyCfg<4, 6, false, true>;
 template <class Task, class Cfg>
 __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
     copy_fp_kernel(const Task* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums,
-                   unsigned long long* __restrict__ sync, const u64* __restrict__ need) {
+                   unsigned long long* __restrict__ sync, const u64* __restrict__ need, bool verify_next) {
     constexpr int kStagesRing = Cfg::kStages;
     constexpr int kAhead = Cfg::kAhead;
     extern __shared__ uint4 smem[];
@@ -482,7 +481,8 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
     constexpr bool kFpNext = std::is_same<Task, FpTask>::value && Cfg::kNext && !Cfg::kPair;
     constexpr int kPrologue = Cfg::kPair ? 3 : kAhead;  // stages 0 .. kPrologue - 1 before the loop
 #pragma unroll
-    for (int s = 0; s < kPrologue; ++s) copy_issue<kFpNext>(wbuf + s * kV3StageWords, cur, s, lane);
+    for (int s = 0; s < kPrologue; ++s)
+        copy_issue(wbuf + s * kV3StageWords, cur, s, lane, kFpNext || (Cfg::kPair && verify_next && cur.dst == nullptr));
     while (cur.t.task >= 0) {
         if (cur.t.task != cur_task) {
             if (cur_task >= 0) {
@@ -510,8 +510,11 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
         // reads any more: that of s - 1 (single lines) or s - 2 (pairs).
         auto issue = [&](int stage, int slot) {
             uint4* dst = wbuf + slot * kV3StageWords;
-            if (stage < kStagesPerLeaf) copy_issue<kFpNext>(dst, cur, stage, lane);
-            else copy_issue<kFpNext>(dst, nxt, stage - kStagesPerLeaf, lane);
+            // verify tiles of paired launches take the next-stage words too
+            if (stage < kStagesPerLeaf)
+                copy_issue(dst, cur, stage, lane, kFpNext || (Cfg::kPair && verify_next && cur.dst == nullptr));
+            else
+                copy_issue(dst, nxt, stage - kStagesPerLeaf, lane, kFpNext || (Cfg::kPair && verify_next && nxt.dst == nullptr));
         };
         for (int s = 0; s < kStagesPerLeaf; ++s) {
             const uint4* sb = wbuf + buf * kV3StageWords;
@@ -522,20 +525,35 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
                 // both of its older slots (s - 2, s - 1) are refilled at once
                 // with s + 2 and s + 3; at even s nothing is refilled.  Stages
                 // up to s + 2 (even s) or s + 1 (odd s) have been issued.
-                if (s & 1) cp_async_wait<1>();
-                else cp_async_wait<2>();
-                __syncwarp();
-                if (s & 1) {
-                    if (writes && cur.t.nfull) {
-                        const uint4* spp = wbuf + b2 * kV3StageWords;
-                        const int nj = (s == kStagesPerLeaf - 1 && cur.k) ? 3 : 2;
-                        write_pair_dispatch(spp, sp, sb, s, nj, s > 1, cur, lane);
-                    }
+                // Verify tiles (no stores) run the fingerprint-only schedule:
+                // refill the slot of s - 1 with s + 3, wait for s and s + 1,
+                // realign from the next stage's word 0.  Both schedules leave
+                // the next tile's stages 0..2 issued in slots (stage mod 4), so
+                // tiles of either kind follow each other.
+                if (writes || !verify_next) {
+                    if (s & 1) cp_async_wait<1>();
+                    else cp_async_wait<2>();
                     __syncwarp();
-                    issue(s + 2, static_cast<int>(b2));
+                    if (s & 1) {
+                        if (writes && cur.t.nfull) {
+                            const uint4* spp = wbuf + b2 * kV3StageWords;
+                            const int nj = (s == kStagesPerLeaf - 1 && cur.k) ? 3 : 2;
+                            write_pair_dispatch(spp, sp, sb, s, nj, s > 1, cur, lane);
+                        }
+                        __syncwarp();
+                        issue(s + 2, static_cast<int>(b2));
+                        issue(s + 3, static_cast<int>(b1));
+                    }
+                } else {
+                    __syncwarp();
                     issue(s + 3, static_cast<int>(b1));
+                    cp_async_wait<2>();
+                    __syncwarp();
                 }
-                if (lane < cur.t.nfull) v4_hash(sb, sb + 32 * kStageBlocks + lane, cur.t, lane, h1, h2);
+                const uint4* xw = (!writes && verify_next && s < kStagesPerLeaf - 1)
+                                      ? wbuf + ((buf + 1) % kStagesRing) * kV3StageWords + lane * 8 + (lane & 7)
+                                      : sb + 32 * kStageBlocks + lane;
+                if (lane < cur.t.nfull) v4_hash(sb, xw, cur.t, lane, h1, h2);
             } else if constexpr (kFpNext) {
                 // slot of s - 1 is free (no line stores): refill first, then
                 // wait for s and s + 1
@@ -654,6 +672,16 @@ static bool pair_ring() {
     return pair;
 }
 
+// Verify tiles of writing launches realign from the next stage (A/B:
+// TANGRAM_VERIFY_NEXT=0 keeps the extra column at every stage).
+static bool verify_next() {
+    static const bool on = [] {
+        const char* e = std::getenv("TANGRAM_VERIFY_NEXT");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    return on;
+}
+
 std::uint64_t copy_fp_resident_warps(int sm_count) { return static_cast<u64>(sm_count) * 2 * CfgPair::kWarps; }
 
 namespace {
@@ -670,7 +698,7 @@ void load_kernel_launch_cfg(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u
     const u64 cap = static_cast<u64>(sm_count) * 2;
     const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
     copy_fp_kernel<Task, Cfg><<<blocks, Cfg::kWarps * 32, Cfg::kSmemBytes, s>>>(
-        d_tasks, n_tasks, total_tiles, d_sums, reinterpret_cast<unsigned long long*>(d_sync), d_need);
+        d_tasks, n_tasks, total_tiles, d_sums, reinterpret_cast<unsigned long long*>(d_sync), d_need, verify_next());
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
