@@ -18,6 +18,31 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 from ncu_summary import summarise  # noqa: E402
 
 
+def load_kernel_stalls(rep):
+    """Issue activity, DRAM rate and warp-stall shares of the load kernel's
+    ncu --set full capture (PC-sampling counts normalised to 1)."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    d = dict(zip(rows[0], rows[2]))
+    units = dict(zip(rows[0], rows[1]))
+    pre = "smsp__pcsamp_warps_issue_stalled_"
+    st = {k[len(pre):]: float(v.replace(",", "")) for k, v in d.items()
+          if k.startswith(pre) and not k.endswith("_not_issued") and v}
+    tot = sum(st.values()) or 1.0
+    num = lambda k: float(d[k].replace(",", ""))
+    return {
+        "kernel": d.get("Kernel Name"),
+        "gpu__time_duration_ms": num("gpu__time_duration.sum") * {"ms": 1.0, "us": 1e-3, "ns": 1e-6}[units["gpu__time_duration.sum"]],
+        "issue_active_pct": d.get("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
+        "dram_throughput_pct": d.get("dram__throughput.avg.pct_of_peak_sustained_elapsed",
+                                     d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")),
+        "registers": d.get("launch__registers_per_thread"),
+        "warps_active_pct": d.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
+        "stall_share": dict(sorted(((k, round(v / tot, 3)) for k, v in st.items() if v / tot >= 0.005),
+                                   key=lambda kv: -kv[1])),
+    }
+
+
 def launch_shares(path):
     rows = []
     with open(path) as f:
@@ -88,6 +113,8 @@ def main():
     lk = os.path.join(OUT, "prof_load.ncu-rep")
     if os.path.exists(lk):
         traffic(lk, os.path.join(PROF, "load_kernel_traffic.json"))
+        with open(os.path.join(PROF, f"{tag}_load_kernel_stalls.json"), "w") as f:
+            json.dump(load_kernel_stalls(lk), f, indent=1)
     for extra in ("kernel_bench.json", "bench.json"):
         p = os.path.join(OUT, extra)
         if os.path.exists(p):
