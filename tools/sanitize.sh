@@ -7,9 +7,14 @@
 S=/usr/local/cuda/bin/compute-sanitizer
 OUT=gpurun_out/sanitizer.txt
 {
-echo "# compute-sanitizer on the B200 (round 1, final load kernel)"
+echo "# compute-sanitizer on the B200 (round 1, final load kernel: next-stage realignment words in K1 and verify tiles)"
 echo "## memcheck: copy_fingerprint_fused at partial-leaf sizes"
 timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest tests/test_gpu_kernels.py -q -k "copy_fingerprint_fused and (4097 or 135169 or 656359) and (16 or 112)" 2>&1 | tail -4
+echo "## memcheck / racecheck: K1 fingerprint-only ring (next-stage realignment words) at partial-leaf sizes and phases"
+timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest tests/test_gpu_kernels.py -q -k "fingerprint_matches_cpu and (4097 or 131077 or 393293)" 2>&1 | tail -2
+timeout 900 $S --tool racecheck python -m pytest tests/test_gpu_kernels.py -q -k "fingerprint_matches_cpu and (131077 or 393293) and (3- or 0-)" 2>&1 | tail -2
+echo "## memcheck: verify tiles in writing launches (device store fuzz, one seed)"
+timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest -q "tests/test_gpu_load.py::test_device_store_differential_fuzz[1]" 2>&1 | tail -2
 echo "## memcheck: K4D device KV batches"
 timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest -q "tests/test_gpu_kv_device.py::test_device_batches_equal_reference[1]" tests/test_gpu_kv_device.py::test_device_batches_in_a_cuda_graph 2>&1 | tail -4
 echo "## memcheck: fused vs unfused load fuzz (K3 device-source placements), re-shard, paged cache, peer pulls"
