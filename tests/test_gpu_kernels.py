@@ -148,6 +148,41 @@ def test_copy_fingerprint_batched_moves(tg, cpu):
         assert (dig[k].hi, dig[k].lo) == cpu.content_fingerprint(datas[k], threads=4)[0]
 
 
+def test_copy_fingerprint_mixed_verify(tg, cpu):
+    """One writing launch mixing moves and in-place verification tasks (dst =
+    0) at every phase class and ragged sizes, as a load's single launch does:
+    verify tiles realign from the next stage while move tiles keep the paired
+    ring, tiles of both kinds interleave in a warp's stream, and every digest
+    equals the CPU restatement."""
+    from paper_2512_01357_b200 import _native as N
+    from paper_2512_01357_b200.checkpoint import DeviceBuffer
+    rng = np.random.default_rng(17)
+    specs = [(4096 * 33 + 5, 3, 9), (131077, 0, None), (4097, 13, None), (4096 * 40, 8, 0), (393293, 7, None),
+             (1, 1, None), (4096 * 64 + 15, 0, 5), (200_003, 12, None), (16, 5, None), (4096 * 32, 11, 11)]
+    bufs, moves, datas = [], [], []
+    for n, so, do in specs:
+        s_ = DeviceBuffer(n + 64)
+        raw = rng.integers(0, 256, size=n + 64, dtype=np.uint8)
+        N.lib.tg_memcpy(C.c_void_p(s_.ptr), raw.ctypes.data_as(C.c_void_p), n + 64)
+        bufs.append(s_)
+        dst = 0
+        if do is not None:
+            d_ = DeviceBuffer(n + 64)
+            bufs.append(d_)
+            dst = d_.ptr + do
+        moves += [s_.ptr + so, dst, n]
+        datas.append(raw[so:so + n].copy())
+    arr = (C.c_uint64 * len(moves))(*moves)
+    dig = (N.DigestC * len(specs))()
+    assert N.lib.tg_copy_fingerprint(arr, len(specs), 0, 0, None, dig) == 0, N.lib.tg_last_error_detail()
+    for k, (n, so, do) in enumerate(specs):
+        assert (dig[k].hi, dig[k].lo) == cpu.content_fingerprint(datas[k], threads=4)[0], k
+        if do is not None:
+            out = np.empty(n, dtype=np.uint8)
+            N.lib.tg_memcpy(out.ctypes.data_as(C.c_void_p), C.c_void_p(moves[3 * k + 1]), n)
+            assert np.array_equal(out, datas[k]), k
+
+
 def test_tensor_beyond_4gib(tg, cpu):
     """A 4.5 GB tensor (byte offsets, leaf and tile counts past 2^32): K1 and
     the load kernel's move + fingerprint agree with the CPU restatement, and

@@ -13,6 +13,9 @@ timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest tests/test_gp
 echo "## memcheck / racecheck: K1 fingerprint-only ring (next-stage realignment words) at partial-leaf sizes and phases"
 timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest tests/test_gpu_kernels.py -q -k "fingerprint_matches_cpu and (4097 or 131077 or 393293)" 2>&1 | tail -2
 timeout 900 $S --tool racecheck python -m pytest tests/test_gpu_kernels.py -q -k "fingerprint_matches_cpu and (131077 or 393293) and (3- or 0-)" 2>&1 | tail -2
+echo "## memcheck / racecheck: verify and move tiles in one writing launch"
+timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest -q tests/test_gpu_kernels.py::test_copy_fingerprint_mixed_verify 2>&1 | tail -2
+timeout 900 $S --tool racecheck python -m pytest -q tests/test_gpu_kernels.py::test_copy_fingerprint_mixed_verify 2>&1 | tail -2
 echo "## memcheck: verify tiles in writing launches (device store fuzz, one seed)"
 timeout 900 $S --tool memcheck --error-exitcode 1 python -m pytest -q "tests/test_gpu_load.py::test_device_store_differential_fuzz[1]" 2>&1 | tail -2
 echo "## memcheck: K4D device KV batches"
