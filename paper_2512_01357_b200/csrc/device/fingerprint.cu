@@ -115,7 +115,8 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // Stage layout: 32 slots of 8 words (128 B) with the word index
 // XOR-swizzled by (leaf & 7), plus a 32-word column holding each leaf's 9th
-// (realignment) word.  Copy i of a lane is leaf 4i + lane/8, word lane%8: one
+// (realignment) word.  Tiles that only fingerprint fill that column at a
+// leaf's last stage alone and otherwise read word 0 of the next stage.  Copy i of a lane is leaf 4i + lane/8, word lane%8: one
 // base register plus the immediate 16 KiB·i per LDGSTS, no predicates on full
 // tiles, and both the LDGSTS writes and the per-lane LDS.128 reads are bank
 // conflict free.
