@@ -131,7 +131,7 @@ def _fuzz_once(tg, ref, seed, n_ops=120, device=None, scale=1, sources=None, on_
     second stream (| extra_flags), and on_step(pool, outcome) checking the
     bytes."""
     rnd = random.Random(seed)
-    frnd = random.Random(~seed)
+    frnd = random.Random(seed ^ 0x5EED5EED)  # load-flag stream, independent of the op stream
     models = _small_catalog(tg, rnd, rnd.randint(2, 6), scale)
     pool = rnd.randint(40_000, 150_000) * scale
     mine = tg.ReuseStore(tg.GpuSpec(pool_size=pool, pcie_bandwidth=rnd.choice([55e9, 12e9])), device=device)
