@@ -11,9 +11,17 @@
  * (types.hpp:155-166: InsufficientMemory=1, PoolExhausted=2, Infeasible=3,
  * Pinned=4, NotFound=5, OverlapMove=6, DestinationOccupied=7,
  * OrderingError=8, InstanceTooLarge=9, InvalidArgument=10); >= 100 are
- * runtime errors of this implementation (TG_ERR_*).  A failed tg_load_model
- * leaves the pool unchanged (reuse_store.hpp:117-119); a failed batch KV
- * allocation leaves engine and pool unchanged (kv_engine.hpp:104-106).
+ * runtime errors of this implementation (TG_ERR_*).  A tg_load_model that
+ * fails with a domain error (1..10) or for want of a byte source
+ * (TG_ERR_NO_SOURCE: no registered source, a missing or short checkpoint
+ * file) leaves the pool unchanged (reuse_store.hpp:117-119).  A runtime
+ * failure once bytes move (TG_ERR_CUDA, a short read of a file that shrank,
+ * TG_ERR_VERIFY: bytes that fail their fingerprint with nothing to repair
+ * them) keeps the reference's decision in the pool — the outcome is still
+ * written, with suspect_tensors > 0 — and leaves every tensor whose bytes it
+ * could not verify *suspect*: never exported to peers or used as a source,
+ * verified and re-sent from its source on its next reuse.  A failed batch
+ * KV allocation leaves engine and pool unchanged (kv_engine.hpp:104-106).
  * Thread-safety: single writer per pool, like the reference
  * (reuse_store.hpp:4-6).
  */
@@ -46,6 +54,9 @@ extern "C" {
 #define TG_LOAD_PEER 4u            /* pull misses resident on a peer pool over NVLink */
 #define TG_LOAD_FUSED 8u           /* one load-kernel launch (move + fingerprint in one pass) instead of K3 waves then K1 */
 #define TG_LOAD_DEFAULT 11u
+/* flags carrying this bit are taken literally: TG_LOAD_EXPLICIT alone asks for
+ * no optional work (flags == 0 without it means TG_LOAD_DEFAULT) */
+#define TG_LOAD_EXPLICIT 0x80000000u
 
 typedef struct tg_pool tg_pool;
 typedef struct tg_stats tg_stats;
@@ -111,6 +122,8 @@ typedef struct {
     double plan_us, total_ms, relocate_ms, h2d_ms, peer_ms, fp_kernel_ms, fp_reuse_ms, fp_reuse_max_ms;
     /* host side of the call: entry -> all device work enqueued, waiting for it, entry -> return */
     double host_issue_us, host_wait_us, host_total_us;
+    /* tensors of the model left suspect (bytes unverified); 0 after a successful load */
+    uint32_t suspect_tensors, reserved0;
 } tg_load_outcome;
 
 /* warmsim::EvictionCandidate (packing.hpp:32-38); model_id valid until the next call on the pool */
@@ -161,9 +174,10 @@ typedef struct {
 typedef struct {
     uint64_t offset, size;
     double last_access;
-    int32_t pinned, has_digest;
+    int32_t pinned, has_digest; /* has_digest: `digest` is the content truth (source / manifest / peer digest) */
     tg_digest digest;
     void* device_ptr;
+    int32_t suspect, reserved0; /* resident bytes not known to equal the content (see tg_load_model) */
 } tg_tensor_info;
 
 /* warmsim::KvAllocStats (kv_engine.hpp:33-39) + engine state */
@@ -318,6 +332,13 @@ int tg_host_unregister(tg_tensor_id id);
 int tg_host_clear(void);
 int tg_host_alloc(uint64_t size, void** out); /* pinned */
 int tg_host_free(void* p);
+
+/* ---- test failpoints ----------------------------------------------------------
+ * Arm a named fault so that its nth hit from now fails the way the real fault
+ * would; nth <= 0 disarms.  "file_read": a checkpoint-file chunk reads short;
+ * "h2d": the host->device copy of a placement fails with TG_ERR_CUDA.
+ * One-shot; process-wide. */
+int tg_failpoint(const char* name, int64_t nth);
 
 /* ---- raw device helpers ------------------------------------------------------ */
 int tg_fingerprint_device(const void* dptr, uint64_t n, int32_t device, tg_digest* out); /* K1 */

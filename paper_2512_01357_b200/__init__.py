@@ -10,10 +10,10 @@ from . import pool
 from .pool import (AllocationPlan, Error, GpuSnapshot, GpuSpec, KvEngine, LoadOutcome, LoadPolicy, MergePolicy,
                    ModelLocation, ModelSpec, ModelStatsTable, PackingStrictness, Result, ReuseStore, Rng,
                    TensorId, TensorSpec, default_catalog, estimate_load_time, make_model, murmur3_x64_128,
-                   schedule, shard_model, tensor_key, lineage)
+                   schedule, shard_model, tensor_key, lineage, failpoint)
 from ._native import LIB_PATH, device_count
 
 __all__ = ["AllocationPlan", "Error", "GpuSnapshot", "GpuSpec", "KvEngine", "LoadOutcome", "LoadPolicy",
            "MergePolicy", "ModelLocation", "ModelSpec", "ModelStatsTable", "PackingStrictness", "Result",
            "ReuseStore", "Rng", "TensorId", "TensorSpec", "default_catalog", "estimate_load_time", "make_model",
-           "murmur3_x64_128", "schedule", "shard_model", "tensor_key", "lineage", "LIB_PATH", "device_count"]
+           "murmur3_x64_128", "schedule", "shard_model", "tensor_key", "lineage", "failpoint", "LIB_PATH", "device_count"]

@@ -57,7 +57,8 @@ class LoadOutcomeC(C.Structure):
                 ("verify_mismatches", u32), ("expected_mismatches", u32),
                 ("plan_us", dbl), ("total_ms", dbl), ("relocate_ms", dbl), ("h2d_ms", dbl), ("peer_ms", dbl),
                 ("fp_kernel_ms", dbl), ("fp_reuse_ms", dbl), ("fp_reuse_max_ms", dbl),
-                ("host_issue_us", dbl), ("host_wait_us", dbl), ("host_total_us", dbl)]
+                ("host_issue_us", dbl), ("host_wait_us", dbl), ("host_total_us", dbl),
+                ("suspect_tensors", u32), ("reserved0", u32)]
 
 
 class EvictionC(C.Structure):
@@ -87,7 +88,7 @@ class PoolInfoC(C.Structure):
 
 class TensorInfoC(C.Structure):
     _fields_ = [("offset", u64), ("size", u64), ("last_access", dbl), ("pinned", i32), ("has_digest", i32),
-                ("digest", DigestC), ("device_ptr", vp)]
+                ("digest", DigestC), ("device_ptr", vp), ("suspect", i32), ("reserved0", i32)]
 
 
 class KvStatsC(C.Structure):
@@ -191,6 +192,7 @@ _SIGS = {
     "tg_device_alloc": (C.c_int, [i32, u64, P(vp)]),
     "tg_device_free": (C.c_int, [i32, vp]),
     "tg_memcpy": (C.c_int, [vp, vp, u64]),
+    "tg_failpoint": (C.c_int, [cp, i64]),
     "tg_kv_create": (C.c_int, [cp, u64, u64, P(vp)]),
     "tg_kv_destroy": (None, [vp]),
     "tg_kv_clone": (C.c_int, [vp, P(vp)]),
@@ -237,8 +239,9 @@ ERROR_NAMES = ["InsufficientMemory", "PoolExhausted", "Infeasible", "Pinned", "N
 class TangramRuntimeError(RuntimeError):
     """A TG_ERR_* runtime failure (CUDA error, missing source, no device...)."""
 
-    def __init__(self, code, where=""):
+    def __init__(self, code, where="", outcome=None):
         self.code = code
+        self.outcome = outcome  # tg_load_model after its commit: the decision taken (suspect_tensors > 0)
         detail = lib.tg_last_error_detail().decode(errors="replace")
         super().__init__(f"{where}: {lib.tg_error_string(code).decode()} ({code}) {detail}".strip())
 

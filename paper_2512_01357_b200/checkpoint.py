@@ -109,6 +109,12 @@ class HostCheckpoint:
             scratch.free()
         self.registered = register
 
+    def register(self):
+        """(Re-)register every tensor's pinned bytes as its source."""
+        for tid, (ptr, n) in self.entries.items():
+            N.check_runtime(lib.tg_host_register(tid.c(), C.c_void_p(ptr), n, None), "tg_host_register")
+        self.registered = True
+
     def view(self, tid: TensorId):
         ptr, n = self.entries[tid]
         return host_array(ptr, n)

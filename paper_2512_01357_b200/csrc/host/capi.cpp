@@ -333,11 +333,22 @@ int tg_load_model(tg_pool* p, const tg_model_spec* ms, const tg_stats* s, double
         if (!p || !ms || !s) return TG_ERR_BAD_ARG;
         if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         const ModelDesc m = model_of(ms);
-        const u32 flags = (pol && pol->flags) ? pol->flags : static_cast<u32>(TG_LOAD_DEFAULT);
+        u32 flags = static_cast<u32>(TG_LOAD_DEFAULT);
+        if (pol && (pol->flags & TG_LOAD_EXPLICIT)) flags = pol->flags & ~static_cast<u32>(TG_LOAD_EXPLICIT);
+        else if (pol && pol->flags) flags = pol->flags;
         LoadReport& r = p->last;
         std::unique_ptr<UniformCallback> cb;
-        St st = p->pool->load_model(m, s->s_view(), clock, options_of(pol, &cb), flags, &r);
-        if (!st) return code_of(st);
+        int rc = 0;
+        try {
+            St st = p->pool->load_model(m, s->s_view(), clock, options_of(pol, &cb), flags, &r);
+            if (!st) return code_of(st);
+        } catch (const DeviceError& e) {
+            // After the commit the outcome still describes the decision taken
+            // (and how many tensors it left suspect); before it, nothing changed.
+            if (!r.committed) throw;
+            g_detail = e.what();
+            rc = e.code;
+        }
         if (out) {
             const Plan& pl = r.decision.plan;
             std::memset(out, 0, sizeof *out);
@@ -373,9 +384,17 @@ int tg_load_model(tg_pool* p, const tg_model_spec* ms, const tg_stats* s, double
             out->host_issue_us = r.t.host_issue_us;
             out->host_wait_us = r.t.host_wait_us;
             out->host_total_us = r.t.host_total_us;
+            out->suspect_tensors = r.suspect_after;
         }
-        return 0;
+        if (p->pool->has_device()) p->pool->publish_index();
+        return rc;
     });
+}
+
+int tg_failpoint(const char* name, int64_t nth) {
+    if (!name) return TG_ERR_BAD_ARG;
+    Failpoints::arm(name, nth);
+    return 0;
 }
 
 uint32_t tg_last_hits(const tg_pool* p, tg_tensor_id* buf, uint32_t cap) {
@@ -534,7 +553,7 @@ int tg_tensor_info_get(const tg_pool* p, tg_tensor_id id, tg_tensor_info* o) {
     if (it == t.end()) return code_of(Err::NotFound);
     const Entry& e = it->second;
     *o = tg_tensor_info{e.off, e.size, e.last_access, e.pinned, e.has_digest, {e.digest.hi, e.digest.lo},
-                        p->pool->has_device() ? p->pool->arena() + e.off : nullptr};
+                        p->pool->has_device() ? p->pool->arena() + e.off : nullptr, e.suspect, 0};
     return 0;
 }
 

@@ -3,7 +3,10 @@
 #include <algorithm>
 #include <chrono>
 #include <fcntl.h>
+#include <sys/stat.h>
 #include <unistd.h>
+
+#include <atomic>
 
 #include <cstdlib>
 #include <cstring>
@@ -62,6 +65,39 @@ std::vector<std::pair<Key, ShardOf>> ShardLineage::children(const Key& parent) c
     return out;
 }
 
+namespace {
+std::mutex g_fp_mu;
+std::unordered_map<std::string, long long> g_fp_armed;  // name -> hits left before the failing one
+std::atomic<bool> g_fp_any{false};
+}  // namespace
+
+void Failpoints::arm(const std::string& name, long long nth) {
+    std::lock_guard<std::mutex> g(g_fp_mu);
+    if (nth <= 0) g_fp_armed.erase(name);
+    else g_fp_armed[name] = nth;
+    g_fp_any.store(!g_fp_armed.empty(), std::memory_order_relaxed);
+}
+
+bool Failpoints::hit(const char* name) {
+    if (!g_fp_any.load(std::memory_order_relaxed)) return false;
+    std::lock_guard<std::mutex> g(g_fp_mu);
+    auto it = g_fp_armed.find(name);
+    if (it == g_fp_armed.end() || --it->second > 0) return false;
+    g_fp_armed.erase(it);  // one-shot
+    g_fp_any.store(!g_fp_armed.empty(), std::memory_order_relaxed);
+    return true;
+}
+
+// A file source must hold its whole range when the load is planned; a file
+// that shrinks under a running load is a runtime failure (short read).
+void check_file_source(const HostSource& s, const Key& id) {
+    struct stat st {};
+    if (::stat(s.path.c_str(), &st) != 0)
+        throw DeviceError(kErrNoSource, "checkpoint file " + s.path + " of tensor " + id.hex() + " is missing");
+    if (static_cast<u64>(st.st_size) < s.file_off + s.size)
+        throw DeviceError(kErrNoSource, "checkpoint file " + s.path + " is too short for tensor " + id.hex());
+}
+
 void SourceRegistry::clear() {
     std::lock_guard<std::mutex> g(mu_);
     map_.clear();
@@ -115,6 +151,10 @@ void FileStager::stage(const std::string& path, u64 off, u64 size, std::uint8_t*
         for (Job& j : jobs)
             j.th = std::thread([&, jp = &j] {
                 u64 done = 0;
+                if (Failpoints::hit("file_read")) {  // injected short read
+                    jp->ok = false;
+                    return;
+                }
                 while (done < jp->n) {
                     const ssize_t r = ::pread(fd, slot_[jp->slot] + done, jp->n - done, static_cast<off_t>(off + jp->at + done));
                     if (r <= 0) {
@@ -264,8 +304,42 @@ u64 build_tasks(std::vector<FpTask>& tasks) {
 
 }  // namespace
 
+void Pool::sync_all_streams() noexcept {
+    if (!has_device()) return;
+    cudaSetDevice(device_);
+    for (cudaStream_t s : {s_main_, s_copy_, s_fp_, s_peer_, s_verify_})
+        if (s) cudaStreamSynchronize(s);
+    cudaGetLastError();
+}
+
+// Failure semantics (reuse_store.hpp:117-119 for what the reference can fail
+// on): planning errors and missing byte sources are found before anything
+// changes, so those failures leave the pool unchanged.  Runtime failures
+// after the commit (a short checkpoint read, a CUDA error, bytes that fail
+// their fingerprint with no source to repair them) keep the reference's
+// decision — the store is what ReuseStore::load_model would have made it —
+// but every tensor whose bytes the load wrote is marked suspect before the
+// first byte moves and cleared only once verified (or landed, when the
+// caller asked for no fingerprints).  A suspect tensor is never exported or
+// used as a source, and its next reuse verifies it and re-sends it from its
+// registered source: no unverified bytes are ever reused.
 St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, const LoadOptions& opt, u32 flags,
                     LoadReport* rep) {
+    try {
+        return load_model_impl(m, stats, clock, opt, flags, rep);
+    } catch (...) {
+        if (rep->committed && has_device()) {
+            sync_all_streams();  // nothing of this load may still be writing when we return
+            rep->suspect_after = 0;
+            for (const auto& t : m.tensors)
+                if (const Entry* e = store_.entry(t.id); e && e->suspect) ++rep->suspect_after;
+        }
+        throw;
+    }
+}
+
+St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double clock, const LoadOptions& opt,
+                         u32 flags, LoadReport* rep) {
     using clk = std::chrono::steady_clock;
     NvtxRange nvtx_load("tg.load_model");
     *rep = LoadReport{};
@@ -292,6 +366,12 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     std::vector<Digest> peer_digest(np);  // what the peer's index says the bytes fingerprint to
     std::vector<std::vector<MoveDesc>> pieces(np);  // re-shard pulls: src, dst offset in the tensor, len
     std::vector<u64> local_piece_bytes(np, 0);       // ... of which sourced from this pool (HBM)
+    // The content truth each placement is checked against, when one is known
+    // before the bytes land: the peer's recorded digest, or the source's
+    // expected (manifest) digest.  Without one, the landed bytes' digest is
+    // recorded as the truth.
+    std::vector<Digest> truth(np);
+    std::vector<char> has_truth(np, 0);
     rep->placement_src.assign(np, 0);
     if (has_device()) {
         for (std::size_t i = 0; i < np; ++i) {
@@ -299,7 +379,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             if (flags & kLoadPeer) {
                 for (Pool* p : peers_) {
                     const Entry* e = p->store_.entry(t.id);
-                    if (e && e->size == t.size && e->has_digest) {
+                    if (e && e->size == t.size && e->has_digest && !e->suspect) {
                         peer_src[i] = p->arena_ + e->off;
                         peer_digest[i] = e->digest;
                         rep->placement_src[i] = 1;
@@ -315,12 +395,23 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
                     }
                 }
             }
-            if (!peer_src[i] && (flags & kLoadPeer) && assemble_shard(t, &pieces[i], &d.plan, &local_piece_bytes[i]))
+            if (peer_src[i]) {
+                truth[i] = peer_digest[i];
+                has_truth[i] = 1;
+                continue;
+            }
+            if ((flags & kLoadPeer) && assemble_shard(t, &pieces[i], &d.plan, &local_piece_bytes[i])) {
                 rep->placement_src[i] = 3;
-            if (peer_src[i] || rep->placement_src[i] == 3) continue;
+                continue;
+            }
             if (!SourceRegistry::get().find(t.id, &src[i]) || src[i].size != t.size)
                 throw DeviceError(kErrNoSource, "no host source registered for tensor " + t.id.hex() + " (" +
                                                     t.model_id + "/" + t.name + ")");
+            if (src[i].is_file()) check_file_source(src[i], t.id);
+            if (src[i].has_expected) {
+                truth[i] = src[i].expected;
+                has_truth[i] = 1;
+            }
             if (src[i].on_device) {  // HBM-resident model cache: SM copy, not the PCIe engine
                 peer_src[i] = static_cast<const std::uint8_t*>(src[i].ptr);
                 rep->placement_src[i] = 2;
@@ -362,12 +453,47 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
             if (overlaps(pl.off, sz, rel[j].from, rel[j].size)) dep[i] = std::max(dep[i], static_cast<int>(rep->reloc_wave[j]));
     }
 
+    // Reused tensors to verify: all of them with kLoadVerifyReuse, and the
+    // suspect ones (left unverified by an earlier failed load) in any case.
+    // A suspect tensor without a recorded digest can only be re-sent, so its
+    // source must exist now, before anything changes.
     std::vector<Key> hit_keys;
-    for (u32 i : d.hits) hit_keys.push_back(m.tensors[i].id);
+    for (u32 i : d.hits) {
+        const Key& k = m.tensors[i].id;
+        const Entry* e = store_.entry(k);
+        if (!(flags & kLoadVerifyReuse) && !e->suspect) continue;
+        if (has_device() && e->suspect && !e->has_digest) {
+            HostSource hs;
+            if (!SourceRegistry::get().find(k, &hs) || hs.size != e->size)
+                throw DeviceError(kErrNoSource, "suspect tensor " + k.hex() + " has no source to re-send it from");
+            if (hs.is_file()) check_file_source(hs, k);
+        }
+        hit_keys.push_back(k);
+    }
     store_.commit(m, d, clock);
+    rep->committed = true;
     rep->decision = std::move(d);
     LoadDecision& D = rep->decision;
     if (!has_device()) return ok();
+
+    // Write-ahead: every tensor whose bytes this load writes is suspect from
+    // here until verified (placements start without a digest unless a truth
+    // is known; a relocated tensor keeps its digest, the content does not
+    // change by moving).
+    std::unordered_map<Key, bool, KeyHash> prior_suspect;  // relocated tensors' state before this load
+    for (std::size_t i = 0; i < np; ++i) {
+        Entry* e = store_.entry(D.miss_desc[D.plan.placements[i].tensor].id);
+        e->suspect = true;
+        if (has_truth[i]) {
+            e->digest = truth[i];
+            e->has_digest = true;
+        }
+    }
+    for (const Move& mv : D.plan.relocations) {
+        Entry* e = store_.entry(mv.tensor);
+        prior_suspect.emplace(mv.tensor, e->suspect);
+        e->suspect = true;
+    }
 
     for (std::size_t i = 0; i < np; ++i) {
         const u64 sz = D.miss_desc[D.plan.placements[i].tensor].size;
@@ -385,7 +511,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     // 8 verify joined | 9.. wave ends (waves) | then per placement "bytes landed" | then fp start/end pairs
     const bool fused = (flags & kLoadFused) != 0 && !raw_edges;
     const std::size_t ev_wave = 9, ev_land = ev_wave + waves, ev_fp = ev_land + np;
-    const bool fp_new = flags & kLoadFingerprintNew, fp_reuse = (flags & kLoadVerifyReuse) && !hit_keys.empty();
+    const bool fp_new = flags & kLoadFingerprintNew, fp_reuse = !hit_keys.empty();
     // Reused tensors no relocation touches are verified right away on the
     // verify stream, in parallel with the waves.  Relocated ones are verified
     // by the copy+fingerprint (K3F) of their wave — or, unfused, by a K1
@@ -401,8 +527,11 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     // K1 after landing: host-sourced placements always; device-sourced ones
     // only when unfused (fused: K3F hashes them while it copies)
     // (re-shard pulls, kind 3, are assembled from several pieces: K1 after the last lands)
+    // (bytes pulled from a peer — kinds 1 and 3 — are always fingerprinted:
+    // that check is what makes a stale peer index safe)
     auto k1_placement = [&](std::size_t i) {
-        return fp_new && (!fused || rep->placement_src[i] == 0 || rep->placement_src[i] == 3);
+        const std::uint8_t k = rep->placement_src[i];
+        return (fp_new || k == 1 || k == 3) && (!fused || k == 0 || k == 3);
     };
     auto tiles_of = [](u64 n) { return ((n + kLeafBytes - 1) / kLeafBytes + kLeavesPerTile - 1) / kLeavesPerTile; };
     constexpr std::size_t kNone = ~std::size_t{0};
@@ -568,6 +697,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
                 if (!stager_) stager_ = std::make_unique<FileStager>(device_, 16u << 20, 8, 4);
                 stager_->stage(src[i].path, src[i].file_off, sz, arena_ + pl.off, s);
             } else {
+                if (Failpoints::hit("h2d")) throw DeviceError(kErrCuda, "failpoint h2d: injected copy failure");
                 TG_CUDA(cudaMemcpyAsync(arena_ + pl.off, src[i].ptr, sz, cudaMemcpyHostToDevice, s));
             }
         }
@@ -650,37 +780,75 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     }
 
     // ---- record / verify digests ----------------------------------------------
+    // Every tensor is settled before a failure is reported, so one bad tensor
+    // does not leave the others of the load suspect.
     auto digest_at = [&](std::size_t slot) { return Digest{h_dig[2 * slot], h_dig[2 * slot + 1]}; };
+    int fail = 0;
+    std::string fail_what;
+    auto fail_with = [&](int code, const std::string& what) {
+        if (!fail) {
+            fail = code;
+            fail_what = what;
+        }
+    };
+    // Re-send a tensor in place from its registered source.  True when the
+    // landed bytes match the truth: the source's expected (manifest) digest
+    // when it has one, else the tensor's recorded digest, else whatever landed.
+    auto repair = [&](const Key& k, Entry* e) {
+        HostSource hs;
+        if (!SourceRegistry::get().find(k, &hs) || hs.size != e->size) return false;
+        fetch(hs, arena_ + e->off, e->size, s_main_);
+        TG_CUDA(cudaStreamSynchronize(s_main_));
+        rep->repaired_bytes += e->size;
+        const Digest g = fingerprint_resident(k);
+        if (hs.has_expected && !(hs.expected == g)) {
+            ++rep->expected_mismatches;
+            return false;
+        }
+        if (!hs.has_expected && e->has_digest && !(e->digest == g)) return false;
+        e->digest = g;
+        e->has_digest = true;
+        e->suspect = false;
+        return true;
+    };
     rep->digests.assign(m.tensors.size(), Digest{});
     std::unordered_map<Key, std::size_t, KeyHash> pos;
     for (std::size_t i = 0; i < m.tensors.size(); ++i) pos.emplace(m.tensors[i].id, i);
     for (std::size_t i = 0; i < np; ++i) {
+        const TensorDesc& t = D.miss_desc[D.plan.placements[i].tensor];
+        Entry* e = store_.entry(t.id);
         std::size_t slot = kNone;
         if (fp_of_placement[i] != kNone) slot = fp_of_placement[i];
         else if (ctask_of_placement[i] != kNone) slot = nf + ctask_of_placement[i];
-        if (slot == kNone) continue;
-        const TensorDesc& t = D.miss_desc[D.plan.placements[i].tensor];
+        if (slot == kNone) {  // landed (the streams are joined), not fingerprinted by request
+            e->suspect = false;
+            continue;
+        }
         const Digest g = digest_at(slot);
-        Entry* e = store_.entry(t.id);
-        e->digest = g;
-        e->has_digest = true;
         rep->digests[pos[t.id]] = g;
         rep->fingerprint_bytes += t.size;
-        if (!rep->placement_src[i] && src[i].has_expected && !(src[i].expected == g)) ++rep->expected_mismatches;
-        if (rep->placement_src[i] == 1 && !(peer_digest[i] == g)) {
+        if (!has_truth[i]) {
+            e->digest = g;
+            e->has_digest = true;
+            e->suspect = false;
+        } else if (g == truth[i]) {
+            e->suspect = false;
+        } else if (rep->placement_src[i] == 1) {
             // The peer's index was stale (its bytes changed under us): fetch the
             // tensor from its host source instead.
             ++rep->verify_mismatches;
-            HostSource hs;
-            if (!SourceRegistry::get().find(t.id, &hs) || hs.size != t.size)
-                throw DeviceError(kErrVerify, "peer bytes of " + t.id.hex() + " fail verification and no host source");
-            fetch(hs, arena_ + e->off, t.size, s_main_);
-            TG_CUDA(cudaStreamSynchronize(s_main_));
-            rep->repaired_bytes += t.size;
-            e->digest = fingerprint_resident(t.id);
-            rep->digests[pos[t.id]] = e->digest;
+            if (repair(t.id, e)) rep->digests[pos[t.id]] = e->digest;
+            else fail_with(kErrVerify, "peer bytes of " + t.id.hex() + " fail verification and no source repairs them");
+        } else {
+            // The registered source itself disagrees with its expected digest:
+            // nothing here is the truth any more, so the tensor can only be
+            // re-sent (from a corrected source) on its next reuse.
+            ++rep->expected_mismatches;
+            e->has_digest = false;
+            fail_with(kErrVerify, "source bytes of " + t.id.hex() + " do not match the expected digest");
         }
     }
+    std::unordered_map<Key, bool, KeyHash> verified;  // hits settled here
     for (std::size_t hix = 0; fp_reuse && hix < hit_keys.size(); ++hix) {
         const Key& k = hit_keys[hix];
         const std::size_t slot = !fused          ? hit_base + hix
@@ -688,24 +856,39 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
                                                  : nf + ctask_of_reloc[reloc_of.at(k)];
         const Digest g = digest_at(slot);
         Entry* e = store_.entry(k);
+        verified.emplace(k, true);
         rep->digests[pos[k]] = g;
         rep->fingerprint_bytes += e->size;
-        if (e->has_digest && !(e->digest == g)) {
-            // Content drifted: the key says "reuse", the bytes disagree.  Re-send
-            // the tensor in place from its host source (same plan, fresh bytes).
-            ++rep->verify_mismatches;
-            HostSource hs;
-            if (!SourceRegistry::get().find(k, &hs) || hs.size != e->size)
-                throw DeviceError(kErrVerify, "reused tensor " + k.hex() + " fails verification and has no host source");
-            fetch(hs, arena_ + e->off, e->size, s_main_);
-            TG_CUDA(cudaStreamSynchronize(s_main_));
-            rep->repaired_bytes += e->size;
-            e->digest = fingerprint_resident(k);
-        } else if (!e->has_digest) {
+        if (e->has_digest && e->digest == g) {
+            e->suspect = false;
+        } else if (!e->has_digest && !e->suspect) {
+            // Placed without a fingerprint (kLoadFingerprintNew off) by a load
+            // that completed: the first verification records the truth.
             e->digest = g;
             e->has_digest = true;
+        } else {
+            // Content drifted (the key says "reuse", the bytes disagree), or a
+            // failed load left it unverifiable: re-send it in place from its
+            // source (same plan, fresh bytes).
+            ++rep->verify_mismatches;
+            if (repair(k, e)) rep->digests[pos[k]] = e->digest;
+            else fail_with(kErrVerify, "reused tensor " + k.hex() + " fails verification and cannot be repaired");
         }
     }
+    // Relocated tensors not verified above: the load kernel hashed them from
+    // the move's own read, so they are checked against their truth for free
+    // (a mismatch leaves them suspect, to be repaired on their next reuse);
+    // otherwise the completed move leaves them as they were.
+    for (std::size_t j = 0; j < rel.size(); ++j) {
+        const Key& k = rel[j].tensor;
+        if (verified.count(k)) continue;
+        Entry* e = store_.entry(k);
+        if (fused && ctask_of_reloc[j] != kNone && e->has_digest) e->suspect = !(digest_at(nf + ctask_of_reloc[j]) == e->digest);
+        else e->suspect = prior_suspect.at(k);
+    }
+    rep->suspect_after = 0;
+    for (const auto& t : m.tensors)
+        if (store_.entry(t.id)->suspect) ++rep->suspect_after;
     rep->t.host_total_us = std::chrono::duration<double, std::micro>(clk::now() - h0).count();
     totals_.loads += 1;
     totals_.data_plane_ms += rep->t.total_ms;
@@ -714,6 +897,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
     totals_.device_src_bytes += rep->device_src_bytes;
     totals_.fingerprint_bytes += rep->fingerprint_bytes;
     totals_.relocated_bytes += D.plan.total_merge_cost;
+    if (fail) throw DeviceError(fail, fail_what);
     return ok();
 }
 
@@ -745,14 +929,15 @@ bool Pool::assemble_shard(const TensorDesc& t, std::vector<MoveDesc>* pieces, co
         bool local = false;
         if (plan && !touched.count(kid)) {
             const auto it = store_.tensors().find(kid);
-            if (it != store_.tensors().end() && it->second.size == of.size && it->second.has_digest) {
+            if (it != store_.tensors().end() && it->second.size == of.size && it->second.has_digest &&
+                !it->second.suspect) {
                 base = arena_ + it->second.off;
                 local = true;
             }
         }
         for (std::size_t k = 0; !base && k < peers_.size(); ++k) {
             const Entry* e = peers_[k]->store_.entry(kid);
-            if (e && e->size == of.size && e->has_digest) base = peers_[k]->arena_ + e->off;
+            if (e && e->size == of.size && e->has_digest && !e->suspect) base = peers_[k]->arena_ + e->off;
         }
         for (std::size_t r = 0; !base && r < remotes_.size(); ++r) {
             auto it = remotes_[r].index.find(kid);
@@ -796,10 +981,14 @@ St Pool::move_tensor(const Key& k, u64 to) {
     St st = store_.move_tensor(k, to);
     if (!st || !has_device()) return st;
     DeviceScope ds(device_);
+    Entry* moved = store_.entry(k);
+    const bool prior = moved->suspect;
+    moved->suspect = true;  // until the bytes have moved (a failure leaves it suspect)
     MoveDesc md{reinterpret_cast<u64>(arena_ + from), reinterpret_cast<u64>(arena_ + to), size};
     relocate_launch(&md, 1, sm_count_, s_main_);
     TG_CUDA(cudaGetLastError());
     TG_CUDA(cudaStreamSynchronize(s_main_));
+    moved->suspect = prior;
     return st;
 }
 
@@ -832,7 +1021,8 @@ u64 Pool::peer_reuse_size(const ModelDesc& m) const {
         if (store_.tensors().count(t.id)) continue;
         bool found = false;
         for (Pool* p : peers_)
-            if (const auto it = p->store_.tensors().find(t.id); it != p->store_.tensors().end() && it->second.has_digest) {
+            if (const auto it = p->store_.tensors().find(t.id);
+                it != p->store_.tensors().end() && it->second.has_digest && !it->second.suspect) {
                 found = true;
                 break;
             }
@@ -855,7 +1045,7 @@ std::vector<RemoteEntry> Pool::index() const {
     std::vector<RemoteEntry> out;
     out.reserve(store_.tensors().size());
     for (const auto& [k, e] : store_.tensors())
-        if (e.has_digest) out.push_back(RemoteEntry{k, e.off, e.size, e.digest});
+        if (e.has_digest && !e.suspect) out.push_back(RemoteEntry{k, e.off, e.size, e.digest});
     return out;
 }
 

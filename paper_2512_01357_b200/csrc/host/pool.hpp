@@ -64,6 +64,16 @@ private:
     u64 bytes_read_ = 0;
 };
 
+// Test failpoints (tg_failpoint, include/tangram.h): arm a named point so that
+// its n-th hit from now fails the way the real fault would (a short file
+// read, a CUDA error in the middle of a load).  Disarmed points cost one
+// relaxed atomic load.
+class Failpoints {
+public:
+    static void arm(const std::string& name, long long nth);  // nth <= 0 disarms
+    static bool hit(const char* name);                         // true: fail here
+};
+
 class SourceRegistry {
 public:
     static SourceRegistry& get();
@@ -120,6 +130,9 @@ constexpr u32 kLoadPeer = 4u;            // pull misses from peer pools that hol
 // leaving this flag out).
 constexpr u32 kLoadFused = 8u;
 constexpr u32 kLoadDefault = kLoadVerifyReuse | kLoadFingerprintNew | kLoadFused;
+// tg_load_policy.flags with this bit are taken literally (0 | explicit = no
+// optional work); without it, 0 means kLoadDefault.
+constexpr u32 kLoadExplicit = 0x80000000u;
 
 struct LoadTimings {
     double plan_us = 0;          // host planning (decide)
@@ -144,6 +157,11 @@ struct LoadReport {
     u32 verify_mismatches = 0, expected_mismatches = 0;
     std::vector<Digest> digests;     // per model tensor (model order), when fingerprinted
     LoadTimings t;
+    // The decision was committed to the store (a runtime error after this
+    // point leaves the reference's decision in place, with every tensor the
+    // load could not verify marked suspect; see Pool::load_model).
+    bool committed = false;
+    u32 suspect_after = 0;           // tensors of this load left suspect (0 on success)
 };
 
 class Pool {
@@ -204,6 +222,9 @@ public:
 
 private:
     void ensure_events(std::size_t n);
+    void sync_all_streams() noexcept;  // best effort, after a failure mid-load
+    St load_model_impl(const ModelDesc& m, const StatsView& stats, double clock, const LoadOptions& opt, u32 flags,
+                       LoadReport* rep);
     void fetch(const HostSource& hs, std::uint8_t* dst, u64 size, cudaStream_t s);
     cudaEvent_t ev(std::size_t i) { return events_[i]; }
 

@@ -80,8 +80,17 @@ struct Entry {
     std::string model;
     double last_access = 0;
     bool pinned = false;
-    bool has_digest = false;  // content fingerprint recorded by the data plane
+    // `digest` is the tensor's content truth: the fingerprint of its source
+    // bytes (measured when placed, or the manifest / peer digest they were
+    // checked against).  Not a statement about the resident bytes.
+    bool has_digest = false;
     Digest digest;
+    // The resident bytes are not known to equal the content: a load wrote
+    // them and has not verified (or failed to land / repair) them.  Suspect
+    // tensors are never exported to peers or used as byte sources, and are
+    // verified (re-sent when unverifiable) on their next reuse whatever the
+    // load flags say.  Data-plane state only: not part of the dump.
+    bool suspect = false;
 };
 
 struct LoadDecision {

@@ -202,6 +202,11 @@ def lineage(tid: TensorId):
     return TensorId(p.hi, p.lo), b.value, n.value
 
 
+def failpoint(name: str, nth: int = 1):
+    """Arm a test failpoint (tg_failpoint): its nth hit from now fails; nth <= 0 disarms."""
+    N.check_runtime(lib.tg_failpoint(name.encode(), nth), "tg_failpoint")
+
+
 def tensor_key(model_id, name, shape, dtype=1) -> TensorId:
     """fingerprint(model, name, shape, etype) (types.hpp:131-146); dtype 1 = f16."""
     arr = (C.c_int64 * max(1, len(shape)))(*shape)
@@ -269,6 +274,7 @@ class PackingStrictness(enum.IntEnum):
 
 
 LOAD_VERIFY_REUSE, LOAD_FINGERPRINT_NEW, LOAD_PEER, LOAD_FUSED = 1, 2, 4, 8
+LOAD_EXPLICIT = 0x80000000  # flags taken literally (LOAD_EXPLICIT alone: no optional work)
 
 
 @dataclass
@@ -341,6 +347,7 @@ class LoadOutcome:
     expected_mismatches: int = 0
     timings: dict = field(default_factory=dict)
     digests: List[Tuple[int, int]] = field(default_factory=list)
+    suspect_tensors: int = 0
 
 
 REGION_KIND = {0: "free", 1: "tensor", 2: "kv_block"}
@@ -395,7 +402,10 @@ class ReuseStore:
         pol = (policy or LoadPolicy()).c()
         out = N.LoadOutcomeC()
         rc = lib.tg_load_model(self._h, C.byref(model.c()), stats._h, clock, C.byref(pol), C.byref(out))
-        N.check_runtime(rc, "tg_load_model")
+        if rc >= 100:
+            # after the commit the outcome still describes the decision (see tangram.h)
+            committed = out.n_hits + out.n_misses > 0
+            raise N.TangramRuntimeError(rc, "tg_load_model", self._outcome(out, details) if committed else None)
         if rc:
             return Result(error=Error(rc - 1))
         return Result(self._outcome(out, details))
@@ -421,7 +431,7 @@ class ReuseStore:
                                         "host_total_us")}
         return LoadOutcome(hits, misses, o.bytes_transferred, o.bytes_merged, o.eviction_cost_total, plan,
                            o.n_waves, o.pcie_bytes, o.peer_bytes, o.device_src_bytes, o.fingerprint_bytes, o.repaired_bytes,
-                           o.verify_mismatches, o.expected_mismatches, t, digs)
+                           o.verify_mismatches, o.expected_mismatches, t, digs, o.suspect_tensors)
 
     def end_instance(self, model_id):
         lib.tg_end_instance(self._h, model_id.encode())
@@ -493,7 +503,7 @@ class ReuseStore:
             return None
         return {"offset": i.offset, "size": i.size, "last_access": i.last_access, "pinned": bool(i.pinned),
                 "has_digest": bool(i.has_digest), "digest": (i.digest.hi, i.digest.lo),
-                "device_ptr": i.device_ptr}
+                "device_ptr": i.device_ptr, "suspect": bool(i.suspect)}
 
     # -- device tensor index ------------------------------------------
     def index_image(self):
