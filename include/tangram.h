@@ -169,7 +169,17 @@ typedef struct {
     uint64_t loads;
     double data_plane_ms;
     uint64_t pcie_bytes, peer_bytes, device_src_bytes, fingerprint_bytes, relocated_bytes;
+    uint64_t epoch; /* changes whenever the tensor map does (unique process-wide) */
 } tg_pool_info;
+
+/* ReuseStore::tensor_map() entry (reuse_store.hpp:26-32); model_id valid while the pool is unchanged */
+typedef struct {
+    tg_tensor_id id;
+    uint64_t offset, size;
+    double last_access;
+    int32_t pinned, suspect;
+    const char* model_id;
+} tg_tensor_entry;
 
 typedef struct {
     uint64_t offset, size;
@@ -226,6 +236,15 @@ uint64_t tg_rng_uniform_below(tg_rng* r, uint64_t n);
 /* ---- pool (ReuseStore, reuse_store.hpp:50-345) ------------------------------ */
 int tg_pool_create(const tg_gpu_spec* gpu, int32_t device, tg_pool** out); /* ReuseStore(GpuSpec) :54 */
 void tg_pool_destroy(tg_pool* p);
+/* Value semantics (reuse_store.hpp:336-344; the reference copies stores for
+ * rollback, kv_engine.hpp:146-158).  tg_pool_clone: an independent
+ * control-plane pool with p's metadata (decisions identical, no arena).
+ * tg_pool_assign: dst takes src's metadata; dst keeps its arena, and a tensor
+ * keeps its verified bytes only where dst already held it at the same offset,
+ * otherwise it is suspect in dst (re-sent on its next reuse). */
+int tg_pool_clone(const tg_pool* p, tg_pool** out);
+int tg_pool_assign(tg_pool* dst, const tg_pool* src);
+int tg_pool_tensors(const tg_pool* p, tg_tensor_entry* buf, uint64_t cap, uint64_t* n); /* tensor_map() */
 int tg_pool_info_get(const tg_pool* p, tg_pool_info* out);
 int tg_pool_stream(const tg_pool* p, void** cuda_stream); /* stream every pool operation is ordered on */
 int tg_set_model_alpha(tg_pool* p, const char* model_id, double alpha); /* :76 */
@@ -379,19 +398,34 @@ int tg_kv_table(const tg_kv* kv, uint64_t request_id, uint64_t* pbns, uint64_t c
                 uint64_t* token_count);                                 /* table() :55 (reads HBM) */
 int tg_kv_address_table(const tg_kv* kv, uint64_t* triples /*pbn,off,size*/, uint64_t cap, uint64_t* n); /* :63 */
 int tg_kv_stats_get(const tg_kv* kv, tg_kv_stats* out);
-int tg_kv_device_tables(const tg_kv* kv, void** tables, uint64_t* stride, void** addr); /* for paged attention */
+/* Device tables for a paged-attention engine: tables[slot * stride + lbn] = PBN
+ * (0 = not granted), addr[pbn] = arena offset.  They are updated on the
+ * engine's own stream: a consumer on another stream first calls
+ * tg_kv_wait_tables(kv, its_stream).  Growth (more request slots, longer
+ * tables, more PBNs than reserved) moves them to new arrays, so re-query
+ * after any allocating call — or size them once with tg_kv_reserve, after
+ * which they never move.  Old arrays stay allocated until the engine is
+ * destroyed: a stale pointer reads stale tables, never freed memory. */
+int tg_kv_device_tables(const tg_kv* kv, void** tables, uint64_t* stride, void** addr);
+int tg_kv_wait_tables(tg_kv* kv, void* cuda_stream); /* cuda_stream waits for the table updates enqueued so far */
+int tg_kv_reserve(tg_kv* kv, tg_pool* p, uint32_t max_requests, uint64_t max_blocks_per_request,
+                  uint64_t max_blocks); /* pre-size the device tables (binds kv to p's device) */
 /* Block-table consumers (the cache write / gather of a paged-attention engine,
  * PAPER.md:807 reshape_and_cache_segment): token i of the request in table
  * slot d_slots[i] at token position d_positions[i] lives at
  *   arena + addr[tables[slot][pos / block_tokens]] + (pos % block_tokens) * bytes_per_token.
  * write_tokens copies d_buf[i] (bytes_per_token each) there; read_tokens
- * gathers it into d_buf[i].  Device pointers; positions must lie in blocks the
- * engine granted.  `cuda_stream` null = the engine's stream, which orders
- * after its own table updates. */
+ * gathers it into d_buf[i].  Device pointers.  The copy is ordered after every
+ * table update enqueued before the call, on any stream (`cuda_stream` null =
+ * the engine's stream).  A token outside the granted blocks (unknown slot, LBN
+ * past the table, PBN 0, a block outside the arena) moves nothing and counts a
+ * fault: tg_kv_token_faults waits for the consumers launched so far and
+ * returns the running count. */
 int tg_kv_write_tokens(tg_kv* kv, tg_pool* p, const uint64_t* d_slots, const uint64_t* d_positions, const void* d_buf,
                        uint32_t n, void* cuda_stream);
 int tg_kv_read_tokens(tg_kv* kv, tg_pool* p, const uint64_t* d_slots, const uint64_t* d_positions, void* d_buf,
                       uint32_t n, void* cuda_stream);
+int tg_kv_token_faults(tg_kv* kv, uint64_t* faults);
 
 /* ---- device-decided KV batches (K4D; new, no reference counterpart) ------------
  * The allocator decision of batch_allocate (:107-161) taken by a kernel, for
@@ -414,7 +448,8 @@ int tg_kv_read_tokens(tg_kv* kv, tg_pool* p, const uint64_t* d_slots, const uint
  *                          left to it (contended pool, unknown slot, shrinking
  *                          token count, duplicate request, ...), and disarm.
  * After sync, tables, address table, counters and pool regions equal running
- * the same batches through tg_kv_batch_allocate.  Errors of replayed batches
+ * the same batches through tg_kv_batch_allocate.  Sync must name the pool the
+ * engine was armed on (TG_ERR_BAD_ARG otherwise, the engine stays armed).  Errors of replayed batches
  * are reported by sync (the first one); TG_ERR_KV_LOG if more than
  * max_batches batches were enqueued. */
 int tg_kv_request_slot(const tg_kv* kv, uint64_t request_id, uint32_t* slot);

@@ -11,8 +11,12 @@
 // Device selection (env TANGRAM_DEVICE): "auto" (default) maps gpu_id "gpuN"
 // to CUDA device N when it exists, otherwise the pool is control-plane only;
 // "none" forces control-plane-only pools; an integer pins every pool to that
-// device.  Copies of a ReuseStore share one pool (the reference copies stores
-// only inside KvEngine's rollback path, which this binding handles natively).
+// device.  Value semantics as in the reference (reuse_store.hpp:336-344): a
+// copy is an independent store (tg_pool_clone: the metadata, control-plane
+// only — bytes never travel), and assigning a copy back (the reference's
+// rollback idiom, kv_engine.hpp:146-158) makes the target adopt its metadata
+// while keeping its own arena (tg_pool_assign: tensors the arena does not
+// hold at their adopted offsets become suspect and are re-sent on reuse).
 #pragma once
 
 #include <cstdlib>
@@ -126,10 +130,13 @@ inline std::vector<std::pair<std::string, tg_pool_info>>& finished_pools() {
 
 struct PoolDeleter {
     std::string gpu_id;
+    bool record = true;  // copies (control-plane clones) are not reported
     void operator()(tg_pool* p) const {
-        tg_pool_info i{};
-        tg_pool_info_get(p, &i);
-        finished_pools().push_back({gpu_id, i});
+        if (record) {
+            tg_pool_info i{};
+            tg_pool_info_get(p, &i);
+            finished_pools().push_back({gpu_id, i});
+        }
         tg_pool_destroy(p);
     }
 };
@@ -148,6 +155,34 @@ public:
         pool_.reset(p, tgb::PoolDeleter{gpu_.gpu_id});
     }
 
+    ReuseStore(const ReuseStore& o) : gpu_(o.gpu_) {
+        if (!o.pool_) return;
+        tg_pool* p = nullptr;
+        if (int rc = tg_pool_clone(o.handle(), &p)) tgb::fail(rc, "tg_pool_clone");
+        pool_.reset(p, tgb::PoolDeleter{gpu_.gpu_id, false});
+    }
+    ReuseStore(ReuseStore&&) noexcept = default;
+    ReuseStore& operator=(const ReuseStore& o) {
+        if (this == &o) return *this;
+        if (!pool_ || !o.pool_) return *this = ReuseStore(o);
+        if (int rc = tg_pool_assign(handle(), o.handle())) tgb::fail(rc, "tg_pool_assign");
+        gpu_ = o.gpu_;
+        return *this;
+    }
+    ReuseStore& operator=(ReuseStore&& o) {
+        if (this == &o) return *this;
+        if (!pool_ || !o.pool_) {  // nothing to keep: take the other pool
+            gpu_ = std::move(o.gpu_);
+            pool_ = std::move(o.pool_);
+            map_epoch_ = ~std::uint64_t{0};
+            return *this;
+        }
+        // keep this store's arena; adopt the other's state
+        if (int rc = tg_pool_assign(handle(), o.handle())) tgb::fail(rc, "tg_pool_assign");
+        gpu_ = o.gpu_;
+        return *this;
+    }
+
     tg_pool* handle() const { return pool_.get(); }
     const GpuSpec& gpu() const { return gpu_; }
     Bytes pool_size() const { return gpu_.pool_size; }
@@ -160,16 +195,18 @@ public:
     Bytes bytes_transferred_total() const { return info().bytes_transferred_total; }
     std::uint64_t evictions_total() const { return info().evictions_total; }
 
+    // Rebuilt from the pool's tensor list only when its epoch changed.
     const std::unordered_map<TensorId, TensorEntry, TensorIdHash>& tensor_map() const {
+        const tg_pool_info i = info();
+        if (i.epoch == map_epoch_) return tensors_cache_;
+        std::uint64_t n = 0;
+        tg_pool_tensors(handle(), nullptr, 0, &n);
+        std::vector<tg_tensor_entry> buf(n);
+        if (int rc = tg_pool_tensors(handle(), buf.data(), n, &n)) tgb::fail(rc, "tg_pool_tensors");
         tensors_cache_.clear();
-        const nlohmann::json d = dump();
-        for (const auto& e : d["tensor_map"]) {
-            const std::string h = e["tensor"].get<std::string>();
-            const TensorId id{std::stoull(h.substr(0, 16), nullptr, 16), std::stoull(h.substr(16), nullptr, 16)};
-            tensors_cache_[id] = TensorEntry{e["offset"].get<Bytes>(), e["size"].get<Bytes>(),
-                                             e["model"].get<std::string>(), e["last_access"].get<double>(),
-                                             e["pinned"].get<bool>()};
-        }
+        for (const auto& e : buf)
+            tensors_cache_[tgb::wid(e.id)] = TensorEntry{e.offset, e.size, e.model_id, e.last_access, e.pinned != 0};
+        map_epoch_ = i.epoch;
         return tensors_cache_;
     }
 
@@ -309,6 +346,7 @@ private:
     GpuSpec gpu_;
     std::shared_ptr<tg_pool> pool_;
     mutable std::unordered_map<TensorId, TensorEntry, TensorIdHash> tensors_cache_;
+    mutable std::uint64_t map_epoch_ = ~std::uint64_t{0};
     mutable RegionList regions_cache_;
 };
 

@@ -83,7 +83,12 @@ class PoolInfoC(C.Structure):
                 ("bytes_transferred_total", u64), ("evictions_total", u64), ("region_count", u64),
                 ("extent_count", u64), ("tensor_count", u64), ("largest_free", u64), ("device", i32),
                 ("arena", vp), ("loads", u64), ("data_plane_ms", dbl), ("pcie_bytes", u64), ("peer_bytes", u64),
-                ("device_src_bytes", u64), ("fingerprint_bytes", u64), ("relocated_bytes", u64)]
+                ("device_src_bytes", u64), ("fingerprint_bytes", u64), ("relocated_bytes", u64), ("epoch", u64)]
+
+
+class TensorEntryC(C.Structure):
+    _fields_ = [("id", TensorIdC), ("offset", u64), ("size", u64), ("last_access", dbl), ("pinned", i32),
+                ("suspect", i32), ("model_id", cp)]
 
 
 class TensorInfoC(C.Structure):
@@ -142,6 +147,9 @@ _SIGS = {
     "tg_pool_create": (C.c_int, [P(GpuSpecC), i32, P(vp)]),
     "tg_pool_destroy": (None, [vp]),
     "tg_pool_info_get": (C.c_int, [vp, P(PoolInfoC)]),
+    "tg_pool_clone": (C.c_int, [vp, P(vp)]),
+    "tg_pool_assign": (C.c_int, [vp, vp]),
+    "tg_pool_tensors": (C.c_int, [vp, P(TensorEntryC), u64, P(u64)]),
     "tg_pool_stream": (C.c_int, [vp, P(vp)]),
     "tg_set_model_alpha": (C.c_int, [vp, cp, dbl]),
     "tg_load_model": (C.c_int, [vp, P(ModelSpecC), vp, dbl, P(LoadPolicyC), P(LoadOutcomeC)]),
@@ -209,6 +217,9 @@ _SIGS = {
     "tg_lineage_get": (C.c_int, [TensorIdC, P(TensorIdC), P(u64), P(u64)]),
     "tg_kv_write_tokens": (C.c_int, [vp, vp, vp, vp, vp, C.c_uint32, vp]),
     "tg_kv_read_tokens": (C.c_int, [vp, vp, vp, vp, vp, C.c_uint32, vp]),
+    "tg_kv_token_faults": (C.c_int, [vp, P(u64)]),
+    "tg_kv_wait_tables": (C.c_int, [vp, vp]),
+    "tg_kv_reserve": (C.c_int, [vp, vp, u32, u64, u64]),
     "tg_kv_request_slot": (C.c_int, [vp, u64, P(C.c_uint32)]),
     "tg_kv_device_arm": (C.c_int, [vp, vp, u64, C.c_uint32, C.c_uint32]),
     "tg_kv_batch_allocate_device": (C.c_int, [vp, vp, vp, C.c_uint32, vp]),

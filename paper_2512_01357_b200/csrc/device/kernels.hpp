@@ -157,10 +157,25 @@ void kv_device_batch_launch(KvDevCtl* d_ctl, const std::uint64_t* d_slots, const
 // token i of request-slot slots[i] at position pos[i] lives at
 // arena + addr[tables[slot * stride + pos / block_tokens]] + (pos % block_tokens) * token_bytes.
 // write: buf[i] -> that place; else that place -> buf[i] (token_bytes each).
-void kv_tokens_launch(const std::uint64_t* tables, std::uint64_t stride, const std::uint64_t* addr,
-                      std::uint8_t* arena, std::uint64_t block_tokens, std::uint64_t token_bytes,
-                      const std::uint64_t* slots, const std::uint64_t* pos, std::uint8_t* buf, std::uint32_t n,
-                      bool write, cudaStream_t s);
+// A reference outside the tables (slot or LBN past the table, PBN 0 = never
+// granted, a PBN past the address table, a block outside the arena) moves
+// nothing and counts one fault in *faults.
+struct KvTokensArgs {
+    const std::uint64_t* tables;
+    std::uint64_t n_slots, stride;
+    const std::uint64_t* addr;
+    std::uint64_t n_pbns;
+    std::uint8_t* arena;
+    std::uint64_t arena_bytes;
+    std::uint64_t block_tokens, token_bytes;
+    const std::uint64_t* slots;
+    const std::uint64_t* pos;
+    std::uint8_t* buf;
+    std::uint32_t n;
+    bool write;
+    unsigned long long* faults;
+};
+void kv_tokens_launch(const KvTokensArgs& a, cudaStream_t s);
 void kv_release_launch(const std::uint64_t* table_row, std::uint64_t blocks, std::uint64_t* free_list_dst,
                        cudaStream_t s);
 

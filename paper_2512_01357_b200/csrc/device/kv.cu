@@ -247,24 +247,27 @@ __global__ void __launch_bounds__(kKvThreads) kv_device_batch_kernel(KvDevCtl* _
 }
 
 // One warp per token; 16-byte words when both ends allow it, bytes otherwise.
-__global__ void kv_tokens_kernel(const u64* __restrict__ tables, u64 stride, const u64* __restrict__ addr,
-                                 std::uint8_t* __restrict__ arena, u64 block_tokens, u64 token_bytes,
-                                 const u64* __restrict__ slots, const u64* __restrict__ pos,
-                                 std::uint8_t* __restrict__ buf, u32 n, bool write) {
+__global__ void kv_tokens_kernel(const KvTokensArgs a) {
     const u32 lane = threadIdx.x & 31;
     const u64 warps = (static_cast<u64>(gridDim.x) * blockDim.x) >> 5;
-    for (u64 i = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
-        const u64 p = pos[i];
-        const u64 pbn = tables[slots[i] * stride + p / block_tokens];
-        std::uint8_t* a = arena + addr[pbn] + (p % block_tokens) * token_bytes;
-        std::uint8_t* b = buf + i * token_bytes;
-        std::uint8_t* dst = write ? a : b;
-        const std::uint8_t* src = write ? b : a;
-        if (((reinterpret_cast<std::uintptr_t>(dst) | reinterpret_cast<std::uintptr_t>(src) | token_bytes) & 15) == 0) {
-            for (u64 w = lane; w < token_bytes / 16; w += 32)
+    const u64 block_bytes = a.block_tokens * a.token_bytes;
+    for (u64 i = (static_cast<u64>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < a.n; i += warps) {
+        const u64 p = a.pos[i], slot = a.slots[i], lbn = p / a.block_tokens;
+        const u64 pbn = slot < a.n_slots && lbn < a.stride ? a.tables[slot * a.stride + lbn] : 0;
+        const u64 off = pbn != 0 && pbn < a.n_pbns ? a.addr[pbn] : ~u64{0};
+        if (off == ~u64{0} || off + block_bytes > a.arena_bytes) {
+            if (lane == 0) atomicAdd(a.faults, 1ull);
+            continue;
+        }
+        std::uint8_t* at = a.arena + off + (p % a.block_tokens) * a.token_bytes;
+        std::uint8_t* b = a.buf + i * a.token_bytes;
+        std::uint8_t* dst = a.write ? at : b;
+        const std::uint8_t* src = a.write ? b : at;
+        if (((reinterpret_cast<std::uintptr_t>(dst) | reinterpret_cast<std::uintptr_t>(src) | a.token_bytes) & 15) == 0) {
+            for (u64 w = lane; w < a.token_bytes / 16; w += 32)
                 reinterpret_cast<uint4*>(dst)[w] = reinterpret_cast<const uint4*>(src)[w];
         } else {
-            for (u64 k = lane; k < token_bytes; k += 32) dst[k] = src[k];
+            for (u64 k = lane; k < a.token_bytes; k += 32) dst[k] = src[k];
         }
     }
 }
@@ -502,6 +505,42 @@ public:
         return 0;
     }
 
+    void order_after_updates(void* stream) override {
+        DeviceScope ds(dev_);
+        auto st = static_cast<cudaStream_t>(stream);
+        if (!st || st == s_) return;
+        if (!updated_) TG_CUDA(cudaEventCreateWithFlags(&updated_, cudaEventDisableTiming));
+        TG_CUDA(cudaEventRecord(updated_, s_));
+        TG_CUDA(cudaStreamWaitEvent(st, updated_));
+    }
+
+    int tokens(std::uint8_t* arena, u64 arena_bytes, u64 block_tokens, u64 token_bytes, const u64* slots,
+               const u64* pos, std::uint8_t* buf, u32 n, bool write, void* stream) override {
+        DeviceScope ds(dev_);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s_;
+        if (!d_faults_) {
+            TG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_faults_), sizeof(unsigned long long), s_));
+            TG_CUDA(cudaMemsetAsync(d_faults_, 0, sizeof(unsigned long long), s_));
+        }
+        order_after_updates(st);  // the tables this batch reads are the ones granted so far
+        foreign_ = foreign_ || st != s_;
+        KvTokensArgs a{tables_, slots_, stride_, addr_, pbn_cap_, arena, arena_bytes, block_tokens, token_bytes,
+                       slots, pos, buf, n, write, d_faults_};
+        kv_tokens_launch(a, st);
+        TG_CUDA(cudaGetLastError());
+        return 0;
+    }
+
+    u64 token_faults() override {
+        DeviceScope ds(dev_);
+        if (!d_faults_) return 0;
+        if (foreign_) TG_CUDA(cudaDeviceSynchronize());
+        unsigned long long f = 0;
+        TG_CUDA(cudaMemcpyAsync(&f, d_faults_, sizeof f, cudaMemcpyDeviceToHost, s_));
+        TG_CUDA(cudaStreamSynchronize(s_));
+        return f;
+    }
+
     void reset() override {}
     void* table_ptr() const override { return tables_; }
     void* stream() const override { return s_; }
@@ -516,7 +555,12 @@ private:
         return n;
     }
 
-    // Grow any of the four arrays, preserving contents (stream-ordered).
+    // Grow any of the four arrays, preserving contents (stream-ordered).  The
+    // old arrays are retired, not freed: pointers handed out earlier
+    // (tg_kv_device_tables, kernels on other streams or in graphs) stay valid
+    // memory until the engine is destroyed — stale after the growth, never
+    // dangling.  Growth doubles, so the retired arrays total less than the
+    // live ones.
     void grow(u32 slots, u64 lbns, u64 free_need, u64 pbns) {
         const u64 ns = grow_to(slots_, slots), nl = grow_to(stride_, lbns);
         if (ns != slots_ || nl != stride_) {
@@ -526,7 +570,7 @@ private:
             if (tables_ && slots_ && stride_)
                 TG_CUDA(cudaMemcpy2DAsync(t, nl * sizeof(u64), tables_, stride_ * sizeof(u64), stride_ * sizeof(u64),
                                           slots_, cudaMemcpyDeviceToDevice, s_));
-            if (tables_) TG_CUDA(cudaFreeAsync(tables_, s_));
+            if (tables_) retired_.push_back(tables_);
             tables_ = t;
             slots_ = ns;
             stride_ = nl;
@@ -542,7 +586,7 @@ private:
         TG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&q), n * sizeof(u64), s_));
         TG_CUDA(cudaMemsetAsync(q, 0, n * sizeof(u64), s_));
         if (*p && *cap) TG_CUDA(cudaMemcpyAsync(q, *p, *cap * sizeof(u64), cudaMemcpyDeviceToDevice, s_));
-        if (*p) TG_CUDA(cudaFreeAsync(*p, s_));
+        if (*p) retired_.push_back(*p);
         *p = q;
         *cap = n;
     }
@@ -588,6 +632,9 @@ private:
         if (foreign_) cudaDeviceSynchronize();
         for (u64* p : {tables_, free_, addr_, d_out_, d_runs_, d_slots_})
             if (p) cudaFree(p);
+        for (u64* p : retired_) cudaFree(p);
+        if (d_faults_) cudaFree(d_faults_);
+        if (updated_) cudaEventDestroy(updated_);
         if (d_log_) cudaFree(d_log_);
         if (d_ctl_) cudaFree(d_ctl_);
         if (done_) cudaEventDestroy(done_);
@@ -621,6 +668,9 @@ private:
     u64 log_cap_ = 0, log_entry_ = 0, max_requests_ = 0, max_batches_ = 0;
     cudaEvent_t done_ = nullptr;
     bool captured_ = false, pending_ = false, foreign_ = false;
+    std::vector<u64*> retired_;            // grown-out arrays (see grow)
+    unsigned long long* d_faults_ = nullptr;  // block-table consumer faults (kv_tokens_kernel)
+    cudaEvent_t updated_ = nullptr;           // engine stream, for consumers on other streams
 };
 
 }  // namespace
@@ -637,14 +687,11 @@ void kv_device_batch_launch(KvDevCtl* d_ctl, const u64* d_slots, const u64* d_to
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
-void kv_tokens_launch(const u64* tables, u64 stride, const u64* addr, std::uint8_t* arena, u64 block_tokens,
-                      u64 token_bytes, const u64* slots, const u64* pos, std::uint8_t* buf, u32 n, bool write,
-                      cudaStream_t s) {
-    if (n == 0 || token_bytes == 0) return;
-    const u64 want = (static_cast<u64>(n) * 32 + 255) / 256;
+void kv_tokens_launch(const KvTokensArgs& a, cudaStream_t s) {
+    if (a.n == 0 || a.token_bytes == 0) return;
+    const u64 want = (static_cast<u64>(a.n) * 32 + 255) / 256;
     const unsigned blocks = static_cast<unsigned>(want < 4096 ? want : 4096);
-    kv_tokens_kernel<<<blocks, 256, 0, s>>>(tables, stride, addr, arena, block_tokens, token_bytes, slots, pos, buf, n,
-                                             write);
+    kv_tokens_kernel<<<blocks, 256, 0, s>>>(a);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

@@ -296,6 +296,42 @@ int tg_pool_create(const tg_gpu_spec* g, int32_t device, tg_pool** out) {
 
 void tg_pool_destroy(tg_pool* p) { delete p; }
 
+int tg_pool_clone(const tg_pool* p, tg_pool** out) {
+    return guard([&] {
+        if (!p || !out) return TG_ERR_BAD_ARG;
+        auto c = std::make_unique<tg_pool>();
+        c->pool = std::make_unique<Pool>(p->pool->store().gpu(), -1);
+        c->pool->adopt_store(p->pool->store());
+        *out = c.release();
+        return 0;
+    });
+}
+
+int tg_pool_assign(tg_pool* dst, const tg_pool* src) {
+    return guard([&] {
+        if (!dst || !src) return TG_ERR_BAD_ARG;
+        if (dst == src) return 0;
+        if (dst->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
+        dst->pool->adopt_store(src->pool->store());
+        dst->pool->publish_index();
+        return 0;
+    });
+}
+
+int tg_pool_tensors(const tg_pool* p, tg_tensor_entry* buf, uint64_t cap, uint64_t* n) {
+    if (!p || !n) return TG_ERR_BAD_ARG;
+    const auto& t = p->pool->store().tensors();
+    *n = t.size();
+    if (!buf) return 0;
+    uint64_t i = 0;
+    for (const auto& [k, e] : t) {
+        if (i == cap) return TG_ERR_BUFFER;
+        buf[i++] = tg_tensor_entry{id_of(k), e.off, e.size, e.last_access, e.pinned ? 1 : 0, e.suspect ? 1 : 0,
+                                   e.model.c_str()};
+    }
+    return 0;
+}
+
 int tg_pool_info_get(const tg_pool* p, tg_pool_info* o) {
     if (!p || !o) return TG_ERR_BAD_ARG;
     const Store& s = p->pool->store();
@@ -304,7 +340,7 @@ int tg_pool_info_get(const tg_pool* p, tg_pool_info* o) {
                       s.merged_total(),    s.transferred_total(), s.evictions_total(),
                       s.map().region_count(), s.map().extent_count(), s.tensors().size(),
                       s.map().largest_free(), p->pool->device(),  p->pool->arena(),
-                      0, 0.0, 0, 0, 0, 0, 0};
+                      0, 0.0, 0, 0, 0, 0, 0, 0};
     const Pool::Totals& t = p->pool->totals();
     o->loads = t.loads;
     o->data_plane_ms = t.data_plane_ms;
@@ -313,6 +349,7 @@ int tg_pool_info_get(const tg_pool* p, tg_pool_info* o) {
     o->device_src_bytes = t.device_src_bytes;
     o->fingerprint_bytes = t.fingerprint_bytes;
     o->relocated_bytes = t.relocated_bytes;
+    o->epoch = s.epoch();
     return 0;
 }
 
@@ -944,14 +981,36 @@ static int kv_tokens(tg_kv* kv, tg_pool* p, const uint64_t* slots, const uint64_
             g_detail = "KV engine and pool on different devices";
             return TG_ERR_BAD_ARG;
         }
-        DeviceScope ds(p->pool->device());
         const u64 bt = kv->a->block_tokens(), tb = kv->a->block_bytes() / bt;
-        kv_tokens_launch(static_cast<const u64*>(d->table_ptr()), d->table_stride(),
-                         static_cast<const u64*>(d->addr_ptr()), p->pool->arena(), bt, tb, slots, pos,
-                         static_cast<std::uint8_t*>(buf), n, write,
-                         static_cast<cudaStream_t>(stream ? stream : d->stream()));
-        TG_CUDA(cudaGetLastError());
+        return d->tokens(p->pool->arena(), p->pool->store().pool_size(), bt, tb, slots, pos,
+                         static_cast<std::uint8_t*>(buf), n, write, stream);
+    });
+}
+int tg_kv_token_faults(tg_kv* kv, uint64_t* faults) {
+    return guard([&] {
+        KvDevice* d = kv ? kv->a->device() : nullptr;
+        if (!d) return TG_ERR_NO_DEVICE;
+        if (!faults) return TG_ERR_BAD_ARG;
+        *faults = d->token_faults();
         return 0;
+    });
+}
+int tg_kv_wait_tables(tg_kv* kv, void* stream) {
+    return guard([&] {
+        KvDevice* d = kv ? kv->a->device() : nullptr;
+        if (!d) return TG_ERR_NO_DEVICE;
+        d->order_after_updates(stream);
+        return 0;
+    });
+}
+int tg_kv_reserve(tg_kv* kv, tg_pool* p, uint32_t max_requests, uint64_t max_blocks_per_request,
+                  uint64_t max_blocks) {
+    return guard([&] {
+        if (!kv || !p) return TG_ERR_BAD_ARG;
+        if (int rc = bind_kv(kv, p)) return rc;
+        KvDevice* d = kv->a->device();
+        if (!d) return TG_ERR_NO_DEVICE;
+        return d->reserve(max_requests, max_blocks_per_request, max_blocks, max_blocks + 1);
     });
 }
 int tg_kv_write_tokens(tg_kv* kv, tg_pool* p, const uint64_t* slots, const uint64_t* pos, const void* buf, uint32_t n,

@@ -286,6 +286,16 @@ int KvAllocator::enqueue_device(const u64* d_slots, const u64* d_tokens, u32 n, 
 St KvAllocator::sync(Store& s, const StatsView& st, SyncReport* rep) {
     NvtxRange nvtx("tg.kv_device_sync");
     if (!armed_) return Err::InvalidArgument;
+    // the decisions were taken against the free runs of the store armed on:
+    // folding them into any other store would corrupt it
+    if (armed_on_.expired()) {  // the armed store is gone: drain and disarm, fold nothing
+        KvLog drained;
+        dev_->read_log(&drained);
+        armed_ = false;
+        return Err::InvalidArgument;
+    }
+    if (armed_on_.lock() != s.kv_arm_handle().lock())
+        throw DeviceError(104, "kv: sync against a pool the engine was not armed on");
     KvLog log;
     if (int rc = dev_->read_log(&log)) throw DeviceError(rc, "kv: device log read failed");
     armed_ = false;

@@ -100,6 +100,12 @@ public:
     virtual void* stream() const = 0;  // the stream table updates are ordered on
     virtual u64 table_stride() const = 0;
     virtual void* addr_ptr() const = 0;
+    // make `stream` wait for every table update enqueued so far
+    virtual void order_after_updates(void* stream) = 0;
+    // block-table consumer (kv_tokens_launch), ordered after the table updates
+    virtual int tokens(std::uint8_t* arena, u64 arena_bytes, u64 block_tokens, u64 token_bytes, const u64* slots,
+                       const u64* pos, std::uint8_t* buf, u32 n, bool write, void* stream) = 0;
+    virtual u64 token_faults() = 0;  // waits for the consumers launched so far
 };
 
 class KvAllocator {

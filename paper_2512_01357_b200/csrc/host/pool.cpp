@@ -1101,6 +1101,24 @@ void Pool::drop(Snapshot* s) {
     delete s;
 }
 
+void Pool::adopt_store(const Store& src) {
+    Store next = src;
+    if (has_device()) {
+        for (const auto& [k, e] : src.tensors()) {
+            Entry* n = next.entry(k);
+            const Entry* cur = store_.entry(k);
+            if (cur && cur->off == e.off && cur->size == e.size && !cur->suspect) {
+                n->suspect = false;
+                n->has_digest = cur->has_digest;
+                n->digest = cur->digest;
+            } else {
+                n->suspect = true;
+            }
+        }
+    }
+    store_ = std::move(next);
+}
+
 std::unique_ptr<KvDevice> Pool::make_kv_device() {
     if (!has_device()) return nullptr;
     return tg::make_kv_device(device_, s_main_);

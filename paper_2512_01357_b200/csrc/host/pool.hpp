@@ -209,6 +209,13 @@ public:
 
     std::unique_ptr<KvDevice> make_kv_device();
 
+    // Value semantics of the reference store (reuse_store.hpp:336-344; copied
+    // for rollback, kv_engine.hpp:146-158): adopt another store's metadata.
+    // Bytes do not travel: a tensor keeps its verified state only where this
+    // arena already holds it (same offset and size, not suspect); every other
+    // tensor of the adopted map is suspect here (its next reuse re-sends it).
+    void adopt_store(const Store& src);
+
     // Device tensor index: republish the store's tensor map to
     // HBM on the pool stream when it changed since the last publish (no-op on
     // control-plane pools).  device_index() is the published table.

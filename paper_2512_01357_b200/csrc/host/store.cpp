@@ -169,7 +169,9 @@ St Store::free_kv_region(u64 off) {
 }
 
 void Store::carve_kv_run(u64 off, u64 nblocks, u64 block_len, u64 first_block) {
-    map_.carve(off, nblocks * block_len, Kind::Kv, {}, first_block, nblocks);
+    if (!map_.carve(off, nblocks * block_len, Kind::Kv, {}, first_block, nblocks))
+        throw DeviceError(106, "kv: run [" + std::to_string(off) + ", +" + std::to_string(nblocks * block_len) +
+                                   ") is not free in this pool");
     kv_bytes_ += nblocks * block_len;
 }
 

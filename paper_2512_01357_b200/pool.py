@@ -372,6 +372,29 @@ class ReuseStore:
 
     __del__ = close
 
+    # -- value semantics (reuse_store.hpp:336-344)
+    def clone(self) -> "ReuseStore":
+        """Independent control-plane copy of this store's metadata (tg_pool_clone)."""
+        c = ReuseStore.__new__(ReuseStore)
+        c.spec, c.device, c._h = self.spec, None, C.c_void_p()
+        N.check_runtime(lib.tg_pool_clone(self._h, C.byref(c._h)), "tg_pool_clone")
+        return c
+
+    def assign(self, other: "ReuseStore"):
+        """Take other's metadata; tensors not already held here at the same
+        offset become suspect (tg_pool_assign)."""
+        N.check_runtime(lib.tg_pool_assign(self._h, other._h), "tg_pool_assign")
+
+    def tensor_map(self) -> dict:
+        """TensorId -> {offset, size, model, last_access, pinned, suspect} (tensor_map(), reuse_store.hpp:66)."""
+        n = C.c_uint64()
+        lib.tg_pool_tensors(self._h, None, 0, C.byref(n))
+        buf = (N.TensorEntryC * max(1, n.value))()
+        N.check_runtime(lib.tg_pool_tensors(self._h, buf, n.value, C.byref(n)), "tg_pool_tensors")
+        return {TensorId(e.id.hi, e.id.lo): {"offset": e.offset, "size": e.size, "model": e.model_id.decode(),
+                                             "last_access": e.last_access, "pinned": bool(e.pinned),
+                                             "suspect": bool(e.suspect)} for e in buf[:n.value]}
+
     # -- accessors (reuse_store.hpp:56-74)
     def info(self):
         i = N.PoolInfoC()
@@ -765,6 +788,21 @@ class KvEngine:
 
     def block_bytes(self):
         return self._stats().block_bytes
+
+    def token_faults(self) -> int:
+        """Block-table consumer references outside the granted blocks so far."""
+        n = C.c_uint64()
+        N.check_runtime(lib.tg_kv_token_faults(self._h, C.byref(n)), "tg_kv_token_faults")
+        return n.value
+
+    def wait_tables(self, stream):
+        """Make a CUDA stream wait for the table updates enqueued so far."""
+        N.check_runtime(lib.tg_kv_wait_tables(self._h, C.c_void_p(stream)), "tg_kv_wait_tables")
+
+    def reserve(self, store: ReuseStore, max_requests, max_blocks_per_request, max_blocks):
+        """Pre-size the device tables so their pointers never move."""
+        N.check_runtime(lib.tg_kv_reserve(self._h, store._h, max_requests, max_blocks_per_request, max_blocks),
+                        "tg_kv_reserve")
 
     def device_tables(self):
         t, a = C.c_void_p(), C.c_void_p()

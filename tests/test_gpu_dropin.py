@@ -34,3 +34,62 @@ def test_c5_replay_moves_bytes_and_matches_reference(mode):
     assert g0["device"] == 0 and g0["loads"] > 0
     assert g0["device_src_bytes"] > 0 and g0["fingerprint_bytes"] > 0
     print(json.dumps(g0))
+
+
+def test_store_copy_semantics_on_a_device_pool():
+    """The drop-in store's value semantics with real bytes: stdout (every
+    dump) equals the reference's; the copies were control-plane clones, so the
+    layout adopted back into the device pool is re-sent where the arena does
+    not hold it, and the final loads leave nothing suspect."""
+    ref_bin, tg_bin = os.path.join(BUILD, "copy_reference"), os.path.join(BUILD, "copy_tangram")
+    if not (os.path.exists(ref_bin) and os.path.exists(tg_bin)):
+        pytest.skip("copy_check binaries not built (make -C integration)")
+    a = subprocess.run([ref_bin], capture_output=True, check=True, timeout=300)
+    env = dict(os.environ, TANGRAM_DEVICE="0", TANGRAM_SYNTH_SOURCES="1")
+    b = subprocess.run([tg_bin], capture_output=True, check=True, timeout=300, env=env)
+    assert a.stdout == b.stdout
+    rep = json.loads(b.stderr.decode().strip().splitlines()[-1])
+    assert rep["suspect"] == [0, 0] and sum(rep["repaired"]) > 0 and min(rep["fingerprinted"]) > 0
+    print(rep)
+
+
+def test_clone_and_assign_keep_bytes_honest(tg, cpu):
+    """tg_pool_clone / tg_pool_assign through the Python mirror: a clone's
+    loads move no bytes and leave the device pool alone; assigning it back
+    marks exactly the tensors the arena does not hold at their adopted
+    offsets suspect; the next reloads re-send them and every resident tensor
+    then fingerprints equal to the CPU restatement."""
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    a = tg.make_model("ca", 40_000_003, 3, 0)
+    b = tg.make_model("cb", 30_000_001, 3, 0)
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=60_000_000), device=0)
+    st = tg.ModelStatsTable()
+    with HostCheckpoint([a, b]):
+        st.record_request("ca", 0.0)
+        pool.load_model(a, st, 0.0).value()
+        pool.end_instance("ca")
+        before = pool.dump()
+        c = pool.clone()
+        assert c.dump() == before and c.device is None
+        st.record_request("cb", 1.0)
+        oc = c.load_model(b, st, 1.0).value()
+        assert oc.bytes_transferred == b.total_size and oc.pcie_bytes == 0  # control plane only
+        assert pool.dump() == before
+        layout = pool.tensor_map()
+        pool.assign(c)
+        assert pool.dump() == c.dump()
+        tm = pool.tensor_map()
+        for tid, e in tm.items():
+            held = tid in layout and layout[tid]["offset"] == e["offset"] and not layout[tid]["suspect"]
+            assert e["suspect"] == (not held), tid
+        pool.end_instance("cb")
+        st.record_request("cb", 2.0)
+        o = pool.load_model(b, st, 2.0).value()
+        assert o.bytes_transferred == 0 and o.repaired_bytes == b.total_size and o.suspect_tensors == 0
+        for m in (a, b):
+            for t in m.tensors:
+                if t.id in tm and not pool.tensor_info(t.id)["suspect"]:
+                    want = cpu.content_fingerprint(cpu.synth(t.id.hi, t.id.lo, t.size), threads=8)[0]
+                    assert pool.fingerprint_tensor(t.id) == want
+        c.close()
+    pool.close()

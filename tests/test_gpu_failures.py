@@ -321,7 +321,7 @@ def test_suspect_is_verified_even_without_verify_flag(tg, cpu):
             assert o.repaired_bytes == m.total_size and o.suspect_tensors == 0
             pool.end_instance(m.model_id)
             o = pool.load_model(m, st, 2.0, none).value()
-            assert o.fingerprint_bytes == 0 and o.repaired_bytes == 0 and o.total_ms >= 0
+            assert o.fingerprint_bytes == 0 and o.repaired_bytes == 0 and o.timings["total_ms"] >= 0
             _check_bytes(tg, cpu, pool, [m])
         finally:
             tg.failpoint("h2d", 0)

@@ -294,3 +294,88 @@ def test_block_tables_drive_a_paged_cache(tg, cpu, token_bytes):
             live.pop(r)
         check()
     pool.close()
+
+
+def test_token_consumer_rejects_references_outside_the_tables(tg):
+    """an unset LBN (PBN 0), an unknown slot or a position past the
+    table moves nothing (it would otherwise land at arena offset 0, inside a
+    resident tensor) and is counted as a fault."""
+    import numpy as np
+    import torch
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    model = tg.make_model("faults", 2_000_003, 2, 64)
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=4_000_000), device=0)
+    st = tg.ModelStatsTable()
+    with HostCheckpoint([model]):
+        digests = pool.load_model(model, st, 0.0).value().digests
+    kv = tg.KvEngine(model.model_id, 8, 64)
+    assert kv.batch_allocate(pool, st, [(1, 20), (2, 5)]).ok()  # slot 0: 3 blocks, slot 1: 1 block
+    s0, s1 = kv.request_slot(1), kv.request_slot(2)
+    slots = [s0, s1, s1, 77, s0]
+    pos = [3, 2, 9, 0, 10_000]  # ok, ok, LBN 1 of slot 1 never granted, unknown slot, past the table
+    buf = torch.full((len(slots) * 64,), 0xEE, dtype=torch.uint8, device="cuda:0")
+    kv.write_tokens(pool, _dev(slots).data_ptr(), _dev(pos).data_ptr(), buf.data_ptr(), len(slots))
+    assert kv.token_faults() == 3
+    for i, t in enumerate(model.tensors):
+        assert pool.fingerprint_tensor(t.id) == digests[i]
+    out = torch.zeros(2 * 64, dtype=torch.uint8, device="cuda:0")
+    kv.read_tokens(pool, _dev(slots[:2]).data_ptr(), _dev(pos[:2]).data_ptr(), out.data_ptr(), 2)
+    assert kv.token_faults() == 3 and np.all(out.cpu().numpy() == 0xEE)
+    pool.close()
+
+
+def test_reserved_tables_never_move_and_consumers_on_other_streams(tg):
+    """tg_kv_reserve pins the device tables' addresses; a consumer on another
+    stream is ordered after the table updates of the batches before it."""
+    import numpy as np
+    import torch
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=64 << 20), device=0)
+    st = tg.ModelStatsTable()
+    kv = tg.KvEngine("r", 16, 128)
+    kv.reserve(pool, 64, 64, 4096)
+    ptrs = kv.device_tables()
+    side = torch.cuda.Stream()
+    rid = 1
+    for step in range(10):
+        reqs = [(rid + i, 16 * (step + 1)) for i in range(6)]
+        rid += 6
+        assert kv.batch_allocate(pool, st, reqs, want_pbns=False).ok()
+        # no host sync between the table update and the consumer on `side`
+        slots = [kv.request_slot(r) for r, n in reqs for p in range(n)]
+        pos = [p for r, n in reqs for p in range(n)]
+        src = torch.arange(len(slots) * 128, device="cuda:0").to(torch.uint8)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            kv.write_tokens(pool, _dev(slots).data_ptr(), _dev(pos).data_ptr(), src.data_ptr(), len(slots),
+                            stream=side.cuda_stream)
+            back = torch.empty_like(src)
+            kv.read_tokens(pool, _dev(slots).data_ptr(), _dev(pos).data_ptr(), back.data_ptr(), len(slots),
+                           stream=side.cuda_stream)
+        side.synchronize()
+        assert torch.equal(back, src)
+        assert kv.device_tables() == ptrs
+    assert kv.token_faults() == 0
+    pool.close()
+
+
+def test_device_sync_rejects_another_pool(tg):
+    """the device-decided carves are folded only into the pool the
+    engine was armed on."""
+    import torch
+    from paper_2512_01357_b200 import _native as N
+    a = tg.ReuseStore(tg.GpuSpec("a", 32 << 20), device=0)
+    b = tg.ReuseStore(tg.GpuSpec("b", 32 << 20), device=0)
+    st = tg.ModelStatsTable()
+    kv = tg.KvEngine("x", 16, 256)
+    assert kv.batch_allocate(a, st, [(1, 16)]).ok()
+    assert kv.device_arm(a, 64, 8, 4).ok()
+    kv.batch_allocate_device(_dev([kv.request_slot(1)]).data_ptr(), _dev([200]).data_ptr(), 1)
+    torch.cuda.synchronize()
+    dump_b = b.dump()
+    with pytest.raises(N.TangramRuntimeError) as ei:
+        kv.device_sync(b, st)
+    assert ei.value.code == 104 and b.dump() == dump_b
+    assert kv.device_sync(a, st).ok()
+    assert a.validate().ok() and b.validate().ok()
+    a.close()
+    b.close()
