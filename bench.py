@@ -448,7 +448,7 @@ def run_ours(args):
         for key, fn in (("c1", lambda: run_c1(tg, local, h2d_peak, hbm_peak)), ("c3", lambda: run_c3(tg, local)),
                         ("c5", lambda: run_c5(local)),
                         ("c2_global_merge", lambda: run_c2_global_merge(tg, local, hbm_peak)),
-                        ("reuse_sweep", lambda: run_reuse_sweep(tg, local)),
+                        ("reuse_sweep", lambda: run_reuse_sweep(tg, local, h2d_peak)),
                         ("per_model", lambda: run_per_model(tg, local, h2d_peak, hbm_peak))):
             try:  # a secondary config never takes the headline line down
                 extras[key] = fn()
@@ -776,7 +776,7 @@ def run_c2_global_merge(tg, dev, hbm_peak, reps=3):
             b.free()
 
 
-def run_reuse_sweep(tg, dev, reps=3):
+def run_reuse_sweep(tg, dev, h2d_peak=None, reps=3):
     """Effective load GB/s at stated reuse ratios (north star): the C2 switch's
     load #3 in 30 / 32 / 36 / 40 GiB pools (reuse 71.5 / 79.4 / 96.8 / 100 %),
     value path (misses from the HBM cache) and e2e (misses from pinned host
@@ -830,7 +830,18 @@ def run_reuse_sweep(tg, dev, reps=3):
                     if r:
                         ms.append(t)
                 m = statistics.mean(ms)
-                out[name] = {"ms": m, "effective_GBps": target.total_size / m / 1e6}
+                tl = o.timings
+                out[name] = {"ms": m, "effective_GBps": target.total_size / m / 1e6,
+                             # device timeline of the last rep, from entry: the load kernel ends; the first
+                             # H2D gated on a relocation wave may start (cuStreamWaitValue64 on the wave's
+                             # tile counter, before the kernel ends); the H2D span
+                             "timeline_ms": {"kernel_end": tl["kernel_end_ms"],
+                                             "gated_h2d_start": tl["gated_h2d_start_ms"],
+                                             "h2d_span": tl["h2d_ms"], "total": tl["total_ms"]}}
+                if name == "e2e" and o.pcie_bytes and h2d_peak:
+                    # the load's floor: its missed bytes over the measured pinned-H2D link
+                    out[name]["pcie_floor_ms"] = o.pcie_bytes / h2d_peak / 1e6
+                    out[name]["frac_of_pcie_floor"] = out[name]["pcie_floor_ms"] / m
                 assert o.verify_mismatches == 0
             rows[f"{gib}GiB"] = {"reuse_ratio": 1.0 - o.bytes_transferred / target.total_size,
                                  "bytes_transferred": o.bytes_transferred, "bytes_merged": o.bytes_merged,

@@ -124,6 +124,9 @@ typedef struct {
     double host_issue_us, host_wait_us, host_total_us;
     /* tensors of the model left suspect (bytes unverified); 0 after a successful load */
     uint32_t suspect_tensors, reserved0;
+    /* device timeline from entry: the load kernel / last relocation wave ends; the first H2D placement
+     * gated on a relocation wave may start (0 when there is none) */
+    double kernel_end_ms, gated_h2d_start_ms;
 } tg_load_outcome;
 
 /* warmsim::EvictionCandidate (packing.hpp:32-38); model_id valid until the next call on the pool */

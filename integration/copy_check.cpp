@@ -14,13 +14,18 @@
 #include <cstdio>
 #include <cstdlib>
 #include <iostream>
+#include <optional>
 #include <string>
+#include <type_traits>
 
 #include "json.hpp"
 #include <warmsim/catalog.hpp>  // <>: never the directory of this file
 #include <warmsim/reuse_store.hpp>
 
 using namespace warmsim;
+
+// containers move stores on reallocation (simulator.hpp:213, std::vector<Gpu>)
+static_assert(std::is_nothrow_move_constructible_v<ReuseStore>);
 
 static void show(const char* tag, const ReuseStore& s) { std::cout << tag << " " << s.dump().dump() << "\n"; }
 
@@ -97,16 +102,34 @@ int main(int argc, char** argv) {
     auto l = load(s, "llama3B");
     show("s_final", s);
     std::cout << "valid=" << static_cast<bool>(s.validate()) << "\n";
+
+    // the store keeps its state for a copy taken before it mutates
+    ReuseStore backup = s;
+    s.end_instance("llama3B");
+    load(s, "opt1.3B");
+    show("backup", backup);
+    show("s_after_backup", s);
+
+    // a copy that outlives its original carries on with the pool
+    std::optional<ReuseStore> first(std::in_place, GpuSpec{"gpu0", static_cast<Bytes>(4.0 * (1ull << 30)), 55e9,
+                                                            3000e9, 12e9});
+    load(*first, "opt1.3B");
+    ReuseStore second = *first;
+    first.reset();
+    second.end_instance("opt1.3B");
+    auto w = load(second, "qwen3B");
+    show("second", second);
 #ifdef TANGRAM_BINDING
-    if (q && l) {
+    if (q && l && w) {
         const auto& a = q.value().device;
         const auto& b = l.value().device;
         std::fprintf(stderr,
                      "{\"repaired\": [%llu, %llu], \"suspect\": [%u, %u], \"fingerprinted\": [%llu, %llu], "
-                     "\"mismatches\": [%u, %u]}\n",
+                     "\"mismatches\": [%u, %u], \"second_pcie\": %llu}\n",
                      (unsigned long long)a.repaired_bytes, (unsigned long long)b.repaired_bytes, a.suspect_tensors,
                      b.suspect_tensors, (unsigned long long)a.fingerprint_bytes,
-                     (unsigned long long)b.fingerprint_bytes, a.verify_mismatches, b.verify_mismatches);
+                     (unsigned long long)b.fingerprint_bytes, a.verify_mismatches, b.verify_mismatches,
+                     (unsigned long long)w.value().device.pcie_bytes);
     }
 #endif
     return 0;

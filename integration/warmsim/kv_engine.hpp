@@ -110,7 +110,7 @@ public:
         const std::uint64_t want = blocks_for(new_token_count, block_size_tokens_);
         std::vector<std::uint64_t> g(want > have ? want - have : 0, kNoPbn);
         std::uint64_t n = 0;
-        const int rc = tgb::domain(tg_kv_ensure_capacity(kv_.get(), store.handle(), sh.h, request_id, new_token_count,
+        const int rc = tgb::domain(tg_kv_ensure_capacity(kv_.get(), store.mutable_handle(), sh.h, request_id, new_token_count,
                                                          g.data(), g.size(), &n),
                                    "tg_kv_ensure_capacity");
         if (rc) return static_cast<Error>(rc - 1);
@@ -131,7 +131,7 @@ public:
         }
         std::vector<std::uint64_t> pbns(cap, kNoPbn);
         std::uint64_t total = 0;
-        const int rc = tgb::domain(tg_kv_batch_allocate(kv_.get(), store.handle(), sh.h, rids.data(), toks.data(),
+        const int rc = tgb::domain(tg_kv_batch_allocate(kv_.get(), store.mutable_handle(), sh.h, rids.data(), toks.data(),
                                                         rids.size(), counts.data(), pbns.data(), cap, &total),
                                    "tg_kv_batch_allocate");
         if (rc) return static_cast<Error>(rc - 1);
@@ -151,12 +151,12 @@ public:
     }
 
     void instance_teardown(ReuseStore& store) {
-        if (int rc = tg_kv_teardown(kv_.get(), store.handle())) tgb::fail(rc, "tg_kv_teardown");
+        if (int rc = tg_kv_teardown(kv_.get(), store.mutable_handle())) tgb::fail(rc, "tg_kv_teardown");
     }
 
     Status urgent_reclaim(ReuseStore& store, const ModelStatsTable& stats, std::uint64_t needed_blocks) {
         tgb::StatsHandle sh(stats);
-        const int rc = tgb::domain(tg_kv_urgent_reclaim(kv_.get(), store.handle(), sh.h, needed_blocks),
+        const int rc = tgb::domain(tg_kv_urgent_reclaim(kv_.get(), store.mutable_handle(), sh.h, needed_blocks),
                                    "tg_kv_urgent_reclaim");
         if (rc) return static_cast<Error>(rc - 1);
         return ok_status();

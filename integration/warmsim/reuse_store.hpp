@@ -11,12 +11,22 @@
 // Device selection (env TANGRAM_DEVICE): "auto" (default) maps gpu_id "gpuN"
 // to CUDA device N when it exists, otherwise the pool is control-plane only;
 // "none" forces control-plane-only pools; an integer pins every pool to that
-// device.  Value semantics as in the reference (reuse_store.hpp:336-344): a
-// copy is an independent store (tg_pool_clone: the metadata, control-plane
-// only — bytes never travel), and assigning a copy back (the reference's
-// rollback idiom, kv_engine.hpp:146-158) makes the target adopt its metadata
-// while keeping its own arena (tg_pool_assign: tensors the arena does not
-// hold at their adopted offsets become suspect and are re-sent on reuse).
+// device.  Value semantics as in the reference (reuse_store.hpp:336-344),
+// copy-on-write over one device pool:
+//  * a copy shares the pool until either side mutates;
+//  * the store that owns the device (the one that created it, or whoever
+//    holds it once the owner is gone) keeps it: when it mutates while shared,
+//    the sharers are first switched to a control-plane snapshot of the state
+//    they saw (tg_pool_clone); when a non-owner mutates while shared, it
+//    detaches to such a snapshot itself (bytes never travel);
+//  * assigning a store into one holding a device (the reference's rollback
+//    idiom, kv_engine.hpp:146-158: `store = std::move(store_copy)`) keeps the
+//    target's arena and adopts the metadata (tg_pool_assign: tensors the
+//    arena does not hold at their adopted offsets become suspect and are
+//    re-sent on their next reuse).
+// So `ReuseStore backup = s; s.load_model(...)` leaves backup the old state
+// and s on the GPU, and containers that copy stores on reallocation keep the
+// device with the surviving copy.
 #pragma once
 
 #include <cstdlib>
@@ -130,7 +140,7 @@ inline std::vector<std::pair<std::string, tg_pool_info>>& finished_pools() {
 
 struct PoolDeleter {
     std::string gpu_id;
-    bool record = true;  // copies (control-plane clones) are not reported
+    bool record = true;  // snapshots (control-plane clones) are not reported
     void operator()(tg_pool* p) const {
         if (record) {
             tg_pool_info i{};
@@ -139,6 +149,13 @@ struct PoolDeleter {
         }
         tg_pool_destroy(p);
     }
+};
+
+// One pool shared by a store and its unmutated copies; `owner` is the store
+// that keeps the pool when a sharer mutates (null: whoever mutates next).
+struct Box {
+    std::shared_ptr<tg_pool> pool;
+    const void* owner = nullptr;
 };
 
 }  // namespace tgb
@@ -152,38 +169,58 @@ public:
                       gpu_.store_bandwidth};
         tg_pool* p = nullptr;
         if (int rc = tg_pool_create(&g, tgb::pick_device(gpu_.gpu_id), &p)) tgb::fail(rc, "tg_pool_create");
-        pool_.reset(p, tgb::PoolDeleter{gpu_.gpu_id});
+        box_ = std::make_shared<tgb::Box>(tgb::Box{std::shared_ptr<tg_pool>(p, tgb::PoolDeleter{gpu_.gpu_id}), this});
     }
 
-    ReuseStore(const ReuseStore& o) : gpu_(o.gpu_) {
-        if (!o.pool_) return;
-        tg_pool* p = nullptr;
-        if (int rc = tg_pool_clone(o.handle(), &p)) tgb::fail(rc, "tg_pool_clone");
-        pool_.reset(p, tgb::PoolDeleter{gpu_.gpu_id, false});
+    ReuseStore(const ReuseStore& o) : gpu_(o.gpu_), box_(o.box_) {}
+    ReuseStore(ReuseStore&& o) noexcept : gpu_(std::move(o.gpu_)), box_(std::move(o.box_)) {
+        if (box_ && box_->owner == &o) box_->owner = this;
     }
-    ReuseStore(ReuseStore&&) noexcept = default;
+    ~ReuseStore() {
+        if (box_ && box_->owner == this) box_->owner = nullptr;  // a sharer may claim the device
+    }
     ReuseStore& operator=(const ReuseStore& o) {
-        if (this == &o) return *this;
-        if (!pool_ || !o.pool_) return *this = ReuseStore(o);
-        if (int rc = tg_pool_assign(handle(), o.handle())) tgb::fail(rc, "tg_pool_assign");
-        gpu_ = o.gpu_;
+        if (this == &o || (box_ && box_ == o.box_)) return *this;
+        if (!box_ || !o.box_) return *this = ReuseStore(o);
+        adopt(o);
         return *this;
     }
-    ReuseStore& operator=(ReuseStore&& o) {
-        if (this == &o) return *this;
-        if (!pool_ || !o.pool_) {  // nothing to keep: take the other pool
+    ReuseStore& operator=(ReuseStore&& o) noexcept(false) {
+        if (this == &o || (box_ && box_ == o.box_)) return *this;
+        if (!box_ || !o.box_) {  // nothing to keep: take the other store whole
+            if (box_ && box_->owner == this) box_->owner = nullptr;
             gpu_ = std::move(o.gpu_);
-            pool_ = std::move(o.pool_);
+            box_ = std::move(o.box_);
+            if (box_ && box_->owner == &o) box_->owner = this;
             map_epoch_ = ~std::uint64_t{0};
             return *this;
         }
-        // keep this store's arena; adopt the other's state
-        if (int rc = tg_pool_assign(handle(), o.handle())) tgb::fail(rc, "tg_pool_assign");
-        gpu_ = o.gpu_;
+        adopt(o);
         return *this;
     }
 
-    tg_pool* handle() const { return pool_.get(); }
+    // The pool, for reads.
+    tg_pool* handle() const { return box_ ? box_->pool.get() : nullptr; }
+    // The pool, for a mutation: resolves sharing first (copy-on-write).
+    tg_pool* mutable_handle() {
+        if (!box_) return nullptr;
+        if (box_->owner == nullptr) box_->owner = this;  // the owner is gone: this store keeps the device
+        if (box_.use_count() > 1) {
+            auto snap = std::make_shared<tgb::Box>(tgb::Box{clone_of(handle()), nullptr});
+            if (box_->owner == this) {
+                // the sharers keep the state they saw; this store keeps the device
+                std::swap(box_->pool, snap->pool);
+                box_.swap(snap);
+                box_->owner = this;
+                snap->owner = nullptr;
+            } else {
+                box_ = std::move(snap);  // detach to a snapshot of our own
+                box_->owner = this;
+            }
+        }
+        map_epoch_ = ~std::uint64_t{0};
+        return box_->pool.get();
+    }
     const GpuSpec& gpu() const { return gpu_; }
     Bytes pool_size() const { return gpu_.pool_size; }
     Bytes free_bytes() const { return info().free_bytes; }
@@ -224,7 +261,7 @@ public:
     }
 
     void set_model_alpha(const std::string& model_id, double alpha) {
-        tg_set_model_alpha(handle(), model_id.c_str(), alpha);
+        tg_set_model_alpha(mutable_handle(), model_id.c_str(), alpha);
     }
 
     std::pair<std::vector<TensorId>, std::vector<TensorSpec>> lookup(const ModelSpec& model) const {
@@ -270,7 +307,7 @@ public:
             pol.rng_ctx = policy.rng;
         }
         LoadOutcome out;
-        const int rc = tgb::domain(tg_load_model(handle(), &v.spec, sh.h, clock, &pol, &out.device), "tg_load_model");
+        const int rc = tgb::domain(tg_load_model(mutable_handle(), &v.spec, sh.h, clock, &pol, &out.device), "tg_load_model");
         if (rc) return static_cast<Error>(rc - 1);
         const tg_load_outcome& o = out.device;
         std::vector<tg_tensor_id> ids(o.n_hits);
@@ -301,24 +338,24 @@ public:
         return out;
     }
 
-    void end_instance(const std::string& model_id) { tg_end_instance(handle(), model_id.c_str()); }
+    void end_instance(const std::string& model_id) { tg_end_instance(mutable_handle(), model_id.c_str()); }
 
-    Status evict_tensor(const TensorId& id) { return status(tg_evict_tensor(handle(), tgb::cid(id)), "evict"); }
+    Status evict_tensor(const TensorId& id) { return status(tg_evict_tensor(mutable_handle(), tgb::cid(id)), "evict"); }
 
-    void evict_model(const std::string& model_id) { tg_evict_model(handle(), model_id.c_str()); }
+    void evict_model(const std::string& model_id) { tg_evict_model(mutable_handle(), model_id.c_str()); }
 
     Status move_tensor(const TensorId& id, Bytes new_offset) {
-        return status(tg_move_tensor(handle(), tgb::cid(id), new_offset), "tg_move_tensor");
+        return status(tg_move_tensor(mutable_handle(), tgb::cid(id), new_offset), "tg_move_tensor");
     }
 
     Result<Bytes> alloc_kv_region(Bytes size, std::uint64_t block_id) {
         std::uint64_t off = 0;
-        const int rc = tgb::domain(tg_alloc_kv_region(handle(), size, block_id, &off), "tg_alloc_kv_region");
+        const int rc = tgb::domain(tg_alloc_kv_region(mutable_handle(), size, block_id, &off), "tg_alloc_kv_region");
         if (rc) return static_cast<Error>(rc - 1);
         return off;
     }
 
-    Status free_kv_region(Bytes offset) { return status(tg_free_kv_region(handle(), offset), "tg_free_kv_region"); }
+    Status free_kv_region(Bytes offset) { return status(tg_free_kv_region(mutable_handle(), offset), "tg_free_kv_region"); }
 
     Status validate() const { return status(tg_validate(handle()), "tg_validate"); }
 
@@ -343,8 +380,19 @@ private:
         return i;
     }
 
+    static std::shared_ptr<tg_pool> clone_of(tg_pool* p) {
+        tg_pool* c = nullptr;
+        if (int rc = tg_pool_clone(p, &c)) tgb::fail(rc, "tg_pool_clone");
+        return std::shared_ptr<tg_pool>(c, tgb::PoolDeleter{"", false});
+    }
+    void adopt(const ReuseStore& o) {
+        tg_pool* dst = mutable_handle();
+        if (int rc = tg_pool_assign(dst, o.handle())) tgb::fail(rc, "tg_pool_assign");
+        gpu_ = o.gpu_;
+    }
+
     GpuSpec gpu_;
-    std::shared_ptr<tg_pool> pool_;
+    std::shared_ptr<tgb::Box> box_;
     mutable std::unordered_map<TensorId, TensorEntry, TensorIdHash> tensors_cache_;
     mutable std::uint64_t map_epoch_ = ~std::uint64_t{0};
     mutable RegionList regions_cache_;

@@ -58,7 +58,7 @@ class LoadOutcomeC(C.Structure):
                 ("plan_us", dbl), ("total_ms", dbl), ("relocate_ms", dbl), ("h2d_ms", dbl), ("peer_ms", dbl),
                 ("fp_kernel_ms", dbl), ("fp_reuse_ms", dbl), ("fp_reuse_max_ms", dbl),
                 ("host_issue_us", dbl), ("host_wait_us", dbl), ("host_total_us", dbl),
-                ("suspect_tensors", u32), ("reserved0", u32)]
+                ("suspect_tensors", u32), ("reserved0", u32), ("kernel_end_ms", dbl), ("gated_h2d_start_ms", dbl)]
 
 
 class EvictionC(C.Structure):

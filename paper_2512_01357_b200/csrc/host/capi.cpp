@@ -422,6 +422,8 @@ int tg_load_model(tg_pool* p, const tg_model_spec* ms, const tg_stats* s, double
             out->host_wait_us = r.t.host_wait_us;
             out->host_total_us = r.t.host_total_us;
             out->suspect_tensors = r.suspect_after;
+            out->kernel_end_ms = r.t.kernel_end_ms;
+            out->gated_h2d_start_ms = r.t.gated_h2d_start_ms;
         }
         if (p->pool->has_device()) p->pool->publish_index();
         return rc;

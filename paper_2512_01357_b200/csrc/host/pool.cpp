@@ -13,11 +13,35 @@
 #include <thread>
 #include <unordered_set>
 
+#include <cuda.h>  // stream memory-op types only; the entry point is resolved at run time
+
 #include "../device/common.cuh"
 #include "../device/kernels.hpp"
 #include "index.hpp"
 
 namespace tg {
+
+namespace {
+// cuStreamWaitValue64 through the runtime's driver entry point (no -lcuda):
+// lets a copy stream wait on a counter the load kernel bumps, so a placement
+// gated on relocation wave w starts when that wave's tiles are done instead
+// of when the whole launch ends.  Null when the driver lacks it.
+using WaitValue64Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+WaitValue64Fn wait_value64() {
+    static const WaitValue64Fn fn = []() -> WaitValue64Fn {
+        if (const char* e = std::getenv("TANGRAM_WAIT_VALUE"); e && std::strcmp(e, "0") == 0) return nullptr;  // A/B
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue64", &p, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        return reinterpret_cast<WaitValue64Fn>(p);
+    }();
+    return fn;
+}
+}  // namespace
 
 // ---- host source registry ----------------------------------------------------
 SourceRegistry& SourceRegistry::get() {
@@ -609,7 +633,8 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     const std::size_t nf = tasks.size(), nc = ctasks.size();
     std::size_t n_fp_launch = 2;
     for (std::size_t i = 0; i < np; ++i) n_fp_launch += fp_of_placement[i] != kNone;
-    ensure_events(ev_fp + 2 * n_fp_launch);
+    const std::size_t ev_gate = ev_fp + 2 * n_fp_launch;  // copy stream: first gated H2D may start
+    ensure_events(ev_gate + 1);
     // stage: [FpTask...][CopyFpTask...][need...] (H2D) | sums | digests | sync
     const std::size_t fdesc = nf * sizeof(FpTask), cdesc = nc * sizeof(CopyFpTask), ndesc = waves * sizeof(u64);
     const std::size_t desc_bytes = (fdesc + cdesc + ndesc + 15) & ~std::size_t{15};
@@ -667,7 +692,26 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     TG_CUDA(cudaStreamWaitEvent(s_peer_, ev(1)));  // K3F reads its descriptors
     TG_CUDA(cudaEventRecord(ev(4), s_copy_));
     TG_CUDA(cudaEventRecord(ev(6), s_peer_));
+    // Gates: unfused, the event after wave w's K3 launch.  Fused, the load
+    // kernel's own counter of wave w's finished tiles (each bumped with a
+    // release after the tile's last read of its source): the stream waits
+    // for done[w] >= need[w] (cuStreamWaitValue64), once the counters of this
+    // load are zeroed (ev 1), so the H2D overlaps the rest of the launch.
     int waited_copy = -1, waited_peer = -1;
+    bool zeroed_copy = false, zeroed_peer = false, gate_recorded = false;
+    const WaitValue64Fn wv = fused ? wait_value64() : nullptr;
+    auto gate = [&](cudaStream_t s, bool& zeroed, int w) {
+        if (wv) {
+            if (!zeroed) {
+                TG_CUDA(cudaStreamWaitEvent(s, ev(1)));
+                zeroed = true;
+            }
+            const CUresult r = wv(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(d_sync + 1 + w),
+                                  need[static_cast<std::size_t>(w)], CU_STREAM_WAIT_VALUE_GEQ);
+            if (r == CUDA_SUCCESS) return;
+        }
+        TG_CUDA(cudaStreamWaitEvent(s, ev(ev_wave + w)));
+    };
     for (std::size_t i : order) {
         const auto& pl = D.plan.placements[i];
         const u64 sz = D.miss_desc[pl.tensor].size;
@@ -675,8 +719,12 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         cudaStream_t s = dev_src ? s_peer_ : s_copy_;
         int& waited = dev_src ? waited_peer : waited_copy;
         if (dep[i] > waited) {
-            TG_CUDA(cudaStreamWaitEvent(s, ev(ev_wave + dep[i])));
+            gate(s, dev_src ? zeroed_peer : zeroed_copy, dep[i]);
             waited = dep[i];
+            if (!dev_src && !gate_recorded) {
+                TG_CUDA(cudaEventRecord(ev(ev_gate), s));
+                gate_recorded = true;
+            }
         }
         if (rep->placement_src[i] == 3) {
             std::vector<MoveDesc> mv = pieces[i];
@@ -768,6 +816,8 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     rep->t.total_ms = ms_between(ev(0), ev(3));
     // fused: the whole load kernel (waves, device-source placements, verification)
     rep->t.relocate_ms = (waves || (fused && nc)) ? ms_between(ev(1), ev(2)) : 0.0;
+    rep->t.kernel_end_ms = ms_between(ev(0), ev(2));
+    rep->t.gated_h2d_start_ms = gate_recorded ? ms_between(ev(0), ev(ev_gate)) : 0.0;
     rep->t.h2d_ms = rep->pcie_bytes ? ms_between(ev(4), ev(5)) : 0.0;
     rep->t.peer_ms = (rep->peer_bytes || rep->device_src_bytes) ? ms_between(ev(6), ev(7)) : 0.0;
     for (std::size_t f = 0; f < fp_i; ++f) {
@@ -791,9 +841,10 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             fail_what = what;
         }
     };
-    // Re-send a tensor in place from its registered source.  True when the
-    // landed bytes match the truth: the source's expected (manifest) digest
-    // when it has one, else the tensor's recorded digest, else whatever landed.
+    // Re-send a tensor in place from its registered source.  The source is
+    // the checkpoint, so what lands is the truth — unless the source carries
+    // an expected (manifest) digest the bytes must match.  (A recorded digest
+    // does not veto it: it may be a stale peer's claim.)
     auto repair = [&](const Key& k, Entry* e) {
         HostSource hs;
         if (!SourceRegistry::get().find(k, &hs) || hs.size != e->size) return false;
@@ -805,7 +856,6 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             ++rep->expected_mismatches;
             return false;
         }
-        if (!hs.has_expected && e->has_digest && !(e->digest == g)) return false;
         e->digest = g;
         e->has_digest = true;
         e->suspect = false;

@@ -146,6 +146,8 @@ struct LoadTimings {
     double host_issue_us = 0;    // host: entry .. all device work enqueued
     double host_wait_us = 0;     // host: waiting for the device work
     double host_total_us = 0;    // host: entry .. return
+    double kernel_end_ms = 0;        // device: entry .. the load kernel (or the last K3 wave) ends
+    double gated_h2d_start_ms = 0;   // device: entry .. the first wave-gated H2D may start (0: none)
 };
 
 struct LoadReport {

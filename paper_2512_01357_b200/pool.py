@@ -451,7 +451,7 @@ class ReuseStore:
                               o.initial_merge_cost, o.fallback_evictions)
         t = {k: getattr(o, k) for k in ("plan_us", "total_ms", "relocate_ms", "h2d_ms", "peer_ms", "fp_kernel_ms",
                                         "fp_reuse_ms", "fp_reuse_max_ms", "host_issue_us", "host_wait_us",
-                                        "host_total_us")}
+                                        "host_total_us", "kernel_end_ms", "gated_h2d_start_ms")}
         return LoadOutcome(hits, misses, o.bytes_transferred, o.bytes_merged, o.eviction_cost_total, plan,
                            o.n_waves, o.pcie_bytes, o.peer_bytes, o.device_src_bytes, o.fingerprint_bytes, o.repaired_bytes,
                            o.verify_mismatches, o.expected_mismatches, t, digs, o.suspect_tensors)

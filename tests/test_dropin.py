@@ -74,3 +74,4 @@ def test_store_copies_are_independent_values():
     assert dumps["c"] != dumps["s0"] and dumps["r"] != dumps["s0"]
     assert dumps["s_eq_c"] == dumps["c"] and dumps["s_eq_r"] == dumps["r"]
     assert b"evict ok=1" in a and b"kv ok=1" in a
+    assert dumps["backup"] == dumps["s_final"] != dumps["s_after_backup"]  # a copy taken before a mutation

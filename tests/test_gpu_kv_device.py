@@ -314,12 +314,14 @@ def test_token_consumer_rejects_references_outside_the_tables(tg):
     slots = [s0, s1, s1, 77, s0]
     pos = [3, 2, 9, 0, 10_000]  # ok, ok, LBN 1 of slot 1 never granted, unknown slot, past the table
     buf = torch.full((len(slots) * 64,), 0xEE, dtype=torch.uint8, device="cuda:0")
-    kv.write_tokens(pool, _dev(slots).data_ptr(), _dev(pos).data_ptr(), buf.data_ptr(), len(slots))
+    s_d, p_d = _dev(slots), _dev(pos)  # kept alive until the kernels ran
+    kv.write_tokens(pool, s_d.data_ptr(), p_d.data_ptr(), buf.data_ptr(), len(slots))
     assert kv.token_faults() == 3
     for i, t in enumerate(model.tensors):
         assert pool.fingerprint_tensor(t.id) == digests[i]
     out = torch.zeros(2 * 64, dtype=torch.uint8, device="cuda:0")
-    kv.read_tokens(pool, _dev(slots[:2]).data_ptr(), _dev(pos[:2]).data_ptr(), out.data_ptr(), 2)
+    s2, p2 = _dev(slots[:2]), _dev(pos[:2])
+    kv.read_tokens(pool, s2.data_ptr(), p2.data_ptr(), out.data_ptr(), 2)
     assert kv.token_faults() == 3 and np.all(out.cpu().numpy() == 0xEE)
     pool.close()
 
@@ -346,10 +348,11 @@ def test_reserved_tables_never_move_and_consumers_on_other_streams(tg):
         src = torch.arange(len(slots) * 128, device="cuda:0").to(torch.uint8)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            kv.write_tokens(pool, _dev(slots).data_ptr(), _dev(pos).data_ptr(), src.data_ptr(), len(slots),
+            s_d, p_d = _dev(slots), _dev(pos)
+            kv.write_tokens(pool, s_d.data_ptr(), p_d.data_ptr(), src.data_ptr(), len(slots),
                             stream=side.cuda_stream)
             back = torch.empty_like(src)
-            kv.read_tokens(pool, _dev(slots).data_ptr(), _dev(pos).data_ptr(), back.data_ptr(), len(slots),
+            kv.read_tokens(pool, s_d.data_ptr(), p_d.data_ptr(), back.data_ptr(), len(slots),
                            stream=side.cuda_stream)
         side.synchronize()
         assert torch.equal(back, src)
@@ -369,7 +372,8 @@ def test_device_sync_rejects_another_pool(tg):
     kv = tg.KvEngine("x", 16, 256)
     assert kv.batch_allocate(a, st, [(1, 16)]).ok()
     assert kv.device_arm(a, 64, 8, 4).ok()
-    kv.batch_allocate_device(_dev([kv.request_slot(1)]).data_ptr(), _dev([200]).data_ptr(), 1)
+    s_d, t_d = _dev([kv.request_slot(1)]), _dev([200])
+    kv.batch_allocate_device(s_d.data_ptr(), t_d.data_ptr(), 1)
     torch.cuda.synchronize()
     dump_b = b.dump()
     with pytest.raises(N.TangramRuntimeError) as ei:
