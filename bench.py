@@ -621,6 +621,24 @@ def isolated_kernels(tg, pool, snap, target, miss_ids, dev, reps=5):
     return out
 
 
+def _capi_load(pool, model, stats, clock):
+    """A tg_load_model call with its C arguments built up front: timing it
+    measures the library (the C-ABI a caller binds), not the Python mirror's
+    argument marshalling.  Returns fn() -> tg_load_outcome (raises on error)."""
+    from paper_2512_01357_b200 import _native as N
+    from paper_2512_01357_b200.pool import LoadPolicy
+    spec, pol, out = model.c(), LoadPolicy().c(), N.LoadOutcomeC()
+    args = (pool._h, C.byref(spec), stats._h, C.c_double(clock), C.byref(pol), C.byref(out))
+    load = N.lib.tg_load_model
+
+    def fn():
+        rc = load(*args)
+        if rc:
+            raise RuntimeError(f"tg_load_model -> {rc}")
+        return out
+    return fn
+
+
 def _event_ms(stream_ptr, dev, fn):
     import torch
     s = torch.cuda.ExternalStream(stream_ptr, device=dev)
@@ -647,7 +665,7 @@ def run_c1(tg, dev, h2d_peak, hbm_peak, reps=3):
             pool.end_instance(m.model_id)
             t += 1.0
             stats.record_request(m.model_id, t)
-            ms_w, ow = _event_ms(pool.stream(), dev, lambda: pool.load_model(m, stats, t, details=False).value())
+            ms_w, ow = _event_ms(pool.stream(), dev, _capi_load(pool, m, stats, t))
             pool.end_instance(m.model_id)
             pool.evict_model(m.model_id)
             t += 1.0
@@ -662,7 +680,10 @@ def run_c1(tg, dev, h2d_peak, hbm_peak, reps=3):
             "cold_h2d_bytes": oc.pcie_bytes, "cold_h2d_ms": oc.timings["h2d_ms"],
             "warm_ms": mw, "warm_effective_GBps": m.total_size / mw / 1e6,
             "warm_fingerprint_bytes": ow.fingerprint_bytes, "warm_verify_mismatches": ow.verify_mismatches,
-            "plan_us_cold": oc.timings["plan_us"], "plan_us_warm": ow.timings["plan_us"],
+            "warm_device_ms": ow.total_ms, "warm_kernel_ms": ow.relocate_ms,
+            "warm_timing": "CUDA events on the pool stream around one tg_load_model C-ABI call (arguments built "
+                           "beforehand): host planning, launch, verification and digest readback included",
+            "plan_us_cold": oc.timings["plan_us"], "plan_us_warm": ow.plan_us,
             "cold_frac_of_h2d_peak": m.total_size / mc / 1e6 / h2d_peak,
             "warm_frac_of_hbm_peak": ow.fingerprint_bytes / mw / 1e6 / hbm_peak,
             "roofline_note": "cold: whole-load latency vs the measured pinned-H2D peak; warm: fingerprint bytes "
@@ -696,8 +717,17 @@ def run_per_model(tg, dev, h2d_peak, hbm_peak):
             st.record_request(m.model_id, 0.0)
             ms_c, oc = _event_ms(pool.stream(), dev, lambda: pool.load_model(m, st, 0.0, details=False).value())
             pool.end_instance(m.model_id)
-            st.record_request(m.model_id, 1.0)
-            ms_w, ow = _event_ms(pool.stream(), dev, lambda: pool.load_model(m, st, 1.0, details=False).value())
+            warm = []
+            for k in range(4):  # the first reload is first-touch; the median of the next three is reported
+                st.record_request(m.model_id, 1.0 + k)
+                ms_w, o = _event_ms(pool.stream(), dev, _capi_load(pool, m, st, 1.0 + k))
+                warm.append((ms_w, o.relocate_ms))
+                ow = {"fingerprint_bytes": o.fingerprint_bytes, "bytes_transferred": o.bytes_transferred,
+                      "verify_mismatches": o.verify_mismatches}
+                pool.end_instance(m.model_id)
+            first_ms = warm[0][0]
+            ms_w = statistics.median(w[0] for w in warm[1:])
+            ow["kernel_ms"] = statistics.median(w[1] for w in warm[1:])
             pool.close()
             for t in m.tensors:
                 lib.tg_host_unregister(t.id.c())
@@ -706,15 +736,17 @@ def run_per_model(tg, dev, h2d_peak, hbm_peak):
                 "cold_ms": ms_c, "cold_GBps": m.total_size / ms_c / 1e6,
                 "cold_frac_of_h2d_peak": m.total_size / ms_c / 1e6 / h2d_peak,
                 "warm_ms": ms_w, "warm_GBps": m.total_size / ms_w / 1e6,
-                "warm_frac_of_hbm_peak": ow.fingerprint_bytes / ms_w / 1e6 / hbm_peak,
-                "warm_reuse": 1.0 - ow.bytes_transferred / m.total_size,
-                "verify_mismatches": oc.verify_mismatches + ow.verify_mismatches}
+                "warm_frac_of_hbm_peak": ow["fingerprint_bytes"] / ms_w / 1e6 / hbm_peak,
+                "warm_kernel_ms": ow["kernel_ms"], "warm_first_touch_ms": first_ms,
+                "warm_reuse": 1.0 - ow["bytes_transferred"] / m.total_size,
+                "verify_mismatches": oc.verify_mismatches + ow["verify_mismatches"]}
     finally:
         scratch.free()
         slab.free()
     return {"workload": "every default_catalog() model: cold load into an empty pool from pinned host (PCIe), "
                         "then a 100%-reuse reload with every tensor fingerprint-verified in place (HBM); one "
-                        "CUDA-event span per synchronous load, first-touch included", "models": rows}
+                        "CUDA-event span per synchronous C-ABI load (arguments built beforehand); warm = median of 3 reloads "
+                        "after a first-touch one (reported too)", "models": rows}
 
 
 def run_c2_global_merge(tg, dev, hbm_peak, reps=3):

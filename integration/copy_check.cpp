@@ -111,7 +111,7 @@ int main(int argc, char** argv) {
     show("s_after_backup", s);
 
     // a copy that outlives its original carries on with the pool
-    std::optional<ReuseStore> first(std::in_place, GpuSpec{"gpu0", static_cast<Bytes>(4.0 * (1ull << 30)), 55e9,
+    std::optional<ReuseStore> first(std::in_place, GpuSpec{"gpu0", static_cast<Bytes>(8.0 * (1ull << 30)), 55e9,
                                                             3000e9, 12e9});
     load(*first, "opt1.3B");
     ReuseStore second = *first;

@@ -459,9 +459,9 @@ using CfgPair = CopyCfg<4, 6, true>;
 using CfgFpNext = CopyCfg<4, 6, false, true>;
 
 template <class Task, class Cfg>
-__global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
-    copy_fp_kernel(const Task* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums,
-                   unsigned long long* __restrict__ sync, const u64* __restrict__ need, bool verify_next) {
+__device__ __forceinline__ void load_tiles(const Task* __restrict__ tasks, u32 n_tasks, u64 total_tiles,
+                                           u64* __restrict__ sums, unsigned long long* __restrict__ sync,
+                                           const u64* __restrict__ need, bool verify_next) {
     constexpr int kStagesRing = Cfg::kStages;
     constexpr int kAhead = Cfg::kAhead;
     extern __shared__ uint4 smem[];
@@ -648,6 +648,43 @@ __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
     }
 }
 
+// tgfp1 root of one task from its leaf sums (types.hpp:77-124 over
+// le64 H || le64 L || le64 n).
+__device__ __forceinline__ void digest_of(u64 sum_h, u64 sum_l, u64 n, u64* out) {
+    u64 h1 = 0, h2 = 0;
+    mm::body(h1, h2, sum_h, sum_l);
+    mm::finish(h1, h2, n, 0, 8, 24);
+    out[0] = h1;
+    out[1] = h2;
+}
+
+// The last CTA of the launch to finish writes every task's digest, so a load
+// needs no second kernel (threadFenceReduction pattern: each CTA's sums are
+// device-visible before its ticket, the last ticket sees them all).
+template <class Task>
+__device__ __forceinline__ void finalize_if_last(const Task* __restrict__ tasks, u32 n_tasks,
+                                                 const u64* __restrict__ sums, u64* __restrict__ digests,
+                                                 unsigned long long* __restrict__ done) {
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(done, 1ull) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (u32 i = threadIdx.x; i < n_tasks; i += blockDim.x)
+        digest_of(__ldcg(sums + 2 * i), __ldcg(sums + 2 * i + 1), tasks[i].n, digests + 2 * i);
+}
+
+template <class Task, class Cfg>
+__global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
+    copy_fp_kernel(const Task* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums,
+                   unsigned long long* __restrict__ sync, const u64* __restrict__ need, bool verify_next,
+                   u64* __restrict__ digests, unsigned long long* __restrict__ done) {
+    load_tiles<Task, Cfg>(tasks, n_tasks, total_tiles, sums, sync, need, verify_next);
+    finalize_if_last(tasks, n_tasks, sums, digests, done);
+}
+
 __global__ void copy_fp_finalize_kernel(const CopyFpTask* __restrict__ tasks, u32 n_tasks,
                                         const u64* __restrict__ sums, u64* __restrict__ digests) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -687,34 +724,36 @@ std::uint64_t copy_fp_resident_warps(int sm_count) { return static_cast<u64>(sm_
 
 namespace {
 template <class Task, class Cfg>
-void load_kernel_launch_cfg(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_sync,
-                            const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed) {
+void load_kernel_launch_cfg(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests,
+                            u64* d_sync, const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s,
+                            bool sync_zeroed) {
     static const bool attr = [] {
         return cudaFuncSetAttribute(copy_fp_kernel<Task, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     Cfg::kSmemBytes) == cudaSuccess;
     }();
     (void)attr;
-    if (!sync_zeroed) cudaMemsetAsync(d_sync, 0, (1 + n_waves) * sizeof(u64), s);
+    if (!sync_zeroed) cudaMemsetAsync(d_sync, 0, (2 + n_waves) * sizeof(u64), s);
     const u64 want = (total_tiles + Cfg::kWarps - 1) / Cfg::kWarps;
     const u64 cap = static_cast<u64>(sm_count) * 2;
     const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
+    auto* sync = reinterpret_cast<unsigned long long*>(d_sync);
     copy_fp_kernel<Task, Cfg><<<blocks, Cfg::kWarps * 32, Cfg::kSmemBytes, s>>>(
-        d_tasks, n_tasks, total_tiles, d_sums, reinterpret_cast<unsigned long long*>(d_sync), d_need, verify_next());
+        d_tasks, n_tasks, total_tiles, d_sums, sync, d_need, verify_next(), d_digests, sync + 1 + n_waves);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 template <class Task>
-void load_kernel_launch(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_sync,
+void load_kernel_launch(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, u64* d_sync,
                         const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed,
                         bool writes) {
     if (!writes && !(std::getenv("TANGRAM_FP_NEXT") && std::strcmp(std::getenv("TANGRAM_FP_NEXT"), "0") == 0))
-        load_kernel_launch_cfg<Task, CfgFpNext>(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves,
+        load_kernel_launch_cfg<Task, CfgFpNext>(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, d_need, n_waves,
                                                 sm_count, s, sync_zeroed);
     else if (writes && pair_ring())
-        load_kernel_launch_cfg<Task, CfgPair>(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves,
+        load_kernel_launch_cfg<Task, CfgPair>(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, d_need, n_waves,
                                               sm_count, s, sync_zeroed);
     else
-        load_kernel_launch_cfg<Task, CfgSingle>(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves,
+        load_kernel_launch_cfg<Task, CfgSingle>(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, d_need, n_waves,
                                                 sm_count, s, sync_zeroed);
 }
 }  // namespace
@@ -722,10 +761,12 @@ void load_kernel_launch(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* 
 void copy_fp_launch(const CopyFpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, u64* d_sync,
                     const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed) {
     if (n_tasks == 0) return;
-    if (total_tiles > 0)
-        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, d_need, n_waves, sm_count, s, sync_zeroed,
-                           /*writes=*/true);
-    copy_fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);
+    if (total_tiles > 0) {
+        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, d_need, n_waves, sm_count, s,
+                           sync_zeroed, /*writes=*/true);
+        return;
+    }
+    copy_fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);  // empty tensors only
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
@@ -733,10 +774,12 @@ void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums,
                int sm_count, cudaStream_t s, bool sync_zeroed) {
     if (n_tasks == 0) return;
     // K1 is the load kernel with fingerprint-only tasks
-    if (total_tiles > 0)
-        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_sync, nullptr, 0, sm_count, s, sync_zeroed,
-                           /*writes=*/false);
-    fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);
+    if (total_tiles > 0) {
+        load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, nullptr, 0, sm_count, s,
+                           sync_zeroed, /*writes=*/false);
+        return;
+    }
+    fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);  // empty tensors only
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

@@ -24,10 +24,10 @@ struct FpTask {
     std::uint64_t tile0;       // first tile index of this task (prefix over tasks)
 };
 
-// sums: 2 u64 per task (must be zeroed), digests: 2 u64 per task, sync: one
-// u64 of device scratch private to this launch (zeroed by it unless the caller
-// did, sync_zeroed).  Runs the load
-// kernel below with fingerprint-only tasks.
+// sums: 2 u64 per task (must be zeroed), digests: 2 u64 per task, sync: two
+// u64 of device scratch private to this launch (tile dispenser, finished
+// CTAs; zeroed by it unless the caller did, sync_zeroed).  Runs the load
+// kernel below with fingerprint-only tasks; its last CTA writes the digests.
 void fp_launch(const FpTask* d_tasks, std::uint32_t n_tasks, std::uint64_t total_tiles, std::uint64_t* d_sums,
                std::uint64_t* d_digests, std::uint64_t* d_sync, int sm_count, cudaStream_t s,
                bool sync_zeroed = false);
@@ -48,9 +48,11 @@ struct CopyFpTask {
     std::int32_t gate;    // wave that must be complete before this task writes (-1: none)
     std::int32_t wave;    // wave this task belongs to (its tiles count towards need[wave]; -1: none)
 };
-// sync: 1 + n_waves u64 of device scratch (zeroed by the launch unless
-// sync_zeroed); need[w] =
-// tiles of wave w's tasks.  sums: 2 u64 per task (zeroed by the caller).
+// sync: 2 + n_waves u64 of device scratch — tile dispenser, the finished
+// tiles of each wave, finished CTAs — (zeroed by the launch unless
+// sync_zeroed); need[w] = tiles of wave w's tasks.  sums: 2 u64 per task
+// (zeroed by the caller).  The launch's last CTA to finish turns the sums
+// into digests (no second kernel).
 void copy_fp_launch(const CopyFpTask* d_tasks, std::uint32_t n_tasks, std::uint64_t total_tiles, std::uint64_t* d_sums,
                     std::uint64_t* d_digests, std::uint64_t* d_sync, const std::uint64_t* d_need,
                     std::uint32_t n_waves, int sm_count, cudaStream_t s, bool sync_zeroed = false);

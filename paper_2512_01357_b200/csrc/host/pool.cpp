@@ -235,8 +235,9 @@ Pool::~Pool() {
     if (ev_index_) cudaEventDestroy(ev_index_);
 }
 
-void Pool::publish_index() {
+void Pool::publish_index(cudaStream_t stream) {
     if (!has_device() || store_.epoch() == published_epoch_) return;
+    cudaStream_t st = stream ? stream : s_main_;
     DeviceScope ds(device_);
     const std::vector<IndexSlot> img = build_index_image(store_);
     const u64 cap = img.size(), bytes = cap * sizeof(IndexSlot);
@@ -256,8 +257,9 @@ void Pool::publish_index() {
         index_cap_ = cap;
     }
     std::memcpy(h_index_, img.data(), bytes);
-    TG_CUDA(cudaMemcpyAsync(d_index_, h_index_, bytes, cudaMemcpyHostToDevice, s_main_));
-    TG_CUDA(cudaEventRecord(ev_index_, s_main_));
+    TG_CUDA(cudaMemcpyAsync(d_index_, h_index_, bytes, cudaMemcpyHostToDevice, st));
+    TG_CUDA(cudaEventRecord(ev_index_, st));
+    if (st != s_main_) TG_CUDA(cudaStreamWaitEvent(s_main_, ev_index_));  // ordered for the pool stream's users
     published_epoch_ = store_.epoch();
 }
 
@@ -641,7 +643,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     const std::size_t sums_bytes = (nf + nc) * 2 * sizeof(u64);
     // stage: [descriptors][sums = 0][sync counters = 0][digests]; the first
     // three go up in one H2D, so no memset precedes the kernels
-    const std::size_t sync_bytes = (1 + waves + n_fp_launch) * sizeof(u64);
+    const std::size_t sync_bytes = (2 + waves + 2 * n_fp_launch) * sizeof(u64);
     ensure_stage(desc_bytes + 2 * sums_bytes + sync_bytes + 64);
     auto* h = static_cast<std::uint8_t*>(h_stage_);
     auto* dptr = static_cast<std::uint8_t*>(d_stage_);
@@ -655,7 +657,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     auto* d_sums = reinterpret_cast<u64*>(dptr + desc_bytes);
     auto* d_sync = reinterpret_cast<u64*>(dptr + desc_bytes + sums_bytes);
     auto* d_dig = reinterpret_cast<u64*>(dptr + desc_bytes + sums_bytes + sync_bytes);
-    u64* d_fp_sync = d_sync + 1 + waves;  // one tile counter per K1 launch
+    u64* d_fp_sync = d_sync + 2 + waves;  // two counters (tiles, finished CTAs) per K1 launch
     if (nf + nc)
         TG_CUDA(cudaMemcpyAsync(dptr, h, desc_bytes + sums_bytes + sync_bytes, cudaMemcpyHostToDevice, s_main_));
 
@@ -712,44 +714,93 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         }
         TG_CUDA(cudaStreamWaitEvent(s, ev(ev_wave + w)));
     };
+    // Device-sourced placements (peer pool, HBM cache, re-shard pieces), whole,
+    // in gate order on the peer stream (fused: inside the load kernel).
+    std::vector<std::size_t> land_order;  // placements in the order their last byte is enqueued
     for (std::size_t i : order) {
         const auto& pl = D.plan.placements[i];
         const u64 sz = D.miss_desc[pl.tensor].size;
-        const bool dev_src = rep->placement_src[i] != 0;
-        cudaStream_t s = dev_src ? s_peer_ : s_copy_;
-        int& waited = dev_src ? waited_peer : waited_copy;
-        if (dep[i] > waited) {
-            gate(s, dev_src ? zeroed_peer : zeroed_copy, dep[i]);
-            waited = dep[i];
-            if (!dev_src && !gate_recorded) {
-                TG_CUDA(cudaEventRecord(ev(ev_gate), s));
-                gate_recorded = true;
-            }
+        if (rep->placement_src[i] == 0) continue;
+        if (rep->placement_src[i] != 3 && fused) continue;  // in the load kernel
+        if (dep[i] > waited_peer) {
+            gate(s_peer_, zeroed_peer, dep[i]);
+            waited_peer = dep[i];
         }
         if (rep->placement_src[i] == 3) {
             std::vector<MoveDesc> mv = pieces[i];
             for (MoveDesc& md : mv) md.dst += reinterpret_cast<u64>(arena_ + pl.off);
             for (std::size_t at = 0; at < mv.size(); at += kMaxMovesPerLaunch) {
                 relocate_launch(mv.data() + at, static_cast<int>(std::min<std::size_t>(kMaxMovesPerLaunch, mv.size() - at)),
-                                sm_count_, s);
+                                sm_count_, s_peer_);
                 TG_CUDA(cudaGetLastError());
             }
-        } else if (dev_src && fused) {
-            continue;  // in the load kernel
-        } else if (dev_src) {
-            MoveDesc md{reinterpret_cast<u64>(peer_src[i]), reinterpret_cast<u64>(arena_ + pl.off), sz};
-            relocate_launch(&md, 1, sm_count_, s);
-            TG_CUDA(cudaGetLastError());
         } else {
-            if (src[i].is_file()) {
-                if (!stager_) stager_ = std::make_unique<FileStager>(device_, 16u << 20, 8, 4);
-                stager_->stage(src[i].path, src[i].file_off, sz, arena_ + pl.off, s);
-            } else {
-                if (Failpoints::hit("h2d")) throw DeviceError(kErrCuda, "failpoint h2d: injected copy failure");
-                TG_CUDA(cudaMemcpyAsync(arena_ + pl.off, src[i].ptr, sz, cudaMemcpyHostToDevice, s));
+            MoveDesc md{reinterpret_cast<u64>(peer_src[i]), reinterpret_cast<u64>(arena_ + pl.off), sz};
+            relocate_launch(&md, 1, sm_count_, s_peer_);
+            TG_CUDA(cudaGetLastError());
+        }
+        TG_CUDA(cudaEventRecord(ev(ev_land + i), s_peer_));
+        land_order.push_back(i);
+    }
+    // Host-sourced placements on the copy stream, split where relocation
+    // sources end: each piece waits only for the last wave that reads the
+    // bytes it overwrites (a placement usually overlaps a moved tensor's old
+    // range only in part), so the link starts at t = 0 with every ungated
+    // piece and the gated ones follow their waves.
+    struct Piece {
+        std::size_t pl;
+        u64 at, len;  // within the tensor
+        int dep;
+    };
+    std::vector<Piece> hp;
+    for (std::size_t i = 0; i < np; ++i) {
+        if (rep->placement_src[i] != 0) continue;
+        const u64 off = D.plan.placements[i].off, sz = D.miss_desc[D.plan.placements[i].tensor].size;
+        std::vector<u64> cuts{0, sz};
+        for (const Move& r : rel)
+            for (u64 c : {r.from, r.from + r.size})
+                if (c > off && c < off + sz) cuts.push_back(c - off);
+        std::sort(cuts.begin(), cuts.end());
+        cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+        for (std::size_t c = 0; c + 1 < cuts.size(); ++c) {
+            int w = -1;
+            for (std::size_t j = 0; j < rel.size(); ++j)
+                if (overlaps(off + cuts[c], cuts[c + 1] - cuts[c], rel[j].from, rel[j].size))
+                    w = std::max(w, static_cast<int>(rep->reloc_wave[j]));
+            if (!hp.empty() && hp.back().pl == i && hp.back().dep == w) hp.back().len += cuts[c + 1] - cuts[c];
+            else hp.push_back(Piece{i, cuts[c], cuts[c + 1] - cuts[c], w});
+        }
+        if (sz == 0) hp.push_back(Piece{i, 0, 0, -1});
+    }
+    std::stable_sort(hp.begin(), hp.end(), [](const Piece& a, const Piece& b) { return a.dep < b.dep; });
+    std::vector<std::size_t> last_piece(np, kNone);
+    for (std::size_t k = 0; k < hp.size(); ++k) last_piece[hp[k].pl] = k;
+    for (std::size_t k = 0; k < hp.size(); ++k) {
+        const Piece& pc = hp[k];
+        if (pc.dep > waited_copy) {
+            gate(s_copy_, zeroed_copy, pc.dep);
+            waited_copy = pc.dep;
+            if (!gate_recorded) {
+                TG_CUDA(cudaEventRecord(ev(ev_gate), s_copy_));
+                gate_recorded = true;
             }
         }
-        TG_CUDA(cudaEventRecord(ev(ev_land + i), s));
+        std::uint8_t* dst = arena_ + D.plan.placements[pc.pl].off + pc.at;
+        const HostSource& hs = src[pc.pl];
+        if (pc.len) {
+            if (hs.is_file()) {
+                if (!stager_) stager_ = std::make_unique<FileStager>(device_, 16u << 20, 8, 4);
+                stager_->stage(hs.path, hs.file_off + pc.at, pc.len, dst, s_copy_);
+            } else {
+                if (Failpoints::hit("h2d")) throw DeviceError(kErrCuda, "failpoint h2d: injected copy failure");
+                TG_CUDA(cudaMemcpyAsync(dst, static_cast<const std::uint8_t*>(hs.ptr) + pc.at, pc.len,
+                                        cudaMemcpyHostToDevice, s_copy_));
+            }
+        }
+        if (last_piece[pc.pl] == k) {
+            TG_CUDA(cudaEventRecord(ev(ev_land + pc.pl), s_copy_));
+            land_order.push_back(pc.pl);
+        }
     }
     TG_CUDA(cudaEventRecord(ev(5), s_copy_));
     TG_CUDA(cudaEventRecord(ev(7), s_peer_));
@@ -758,12 +809,12 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     std::size_t fp_i = 0;
     bool fp_stream_used = false;
     TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(1)));  // descriptors uploaded, sums zeroed
-    for (std::size_t i : order) {
+    for (std::size_t i : land_order) {
         const std::size_t k = fp_of_placement[i];
         if (k == kNone) continue;
         TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(ev_land + i)));
         TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s_fp_));
-        fp_launch(d_tasks + k, 1, new_tiles[k], d_sums + 2 * k, d_dig + 2 * k, d_fp_sync + fp_i, sm_count_, s_fp_,
+        fp_launch(d_tasks + k, 1, new_tiles[k], d_sums + 2 * k, d_dig + 2 * k, d_fp_sync + 2 * fp_i, sm_count_, s_fp_,
                   /*sync_zeroed=*/true);
         TG_CUDA(cudaGetLastError());
         TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s_fp_));
@@ -778,7 +829,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             if (!count) return;
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s));
             fp_launch(d_tasks + first, static_cast<u32>(count), tiles, d_sums + 2 * first, d_dig + 2 * first,
-                      d_fp_sync + fp_i, sm_count_, s, /*sync_zeroed=*/true);
+                      d_fp_sync + 2 * fp_i, sm_count_, s, /*sync_zeroed=*/true);
             TG_CUDA(cudaGetLastError());
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s));
             ++fp_i;
@@ -792,8 +843,11 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         TG_CUDA(cudaEventRecord(ev(8), s_verify_));
         TG_CUDA(cudaStreamWaitEvent(s_main_, ev(8)));
     }
-    // ---- device index: the committed map, published behind the data plane ------
-    publish_index();
+    // ---- device index: the committed map, uploaded on a side stream while the
+    // data plane runs (the pool stream joins it: valid for work ordered after
+    // the load on the pool stream) ---------------------------------------------
+    TG_CUDA(cudaStreamWaitEvent(s_verify_, ev(0)));
+    publish_index(s_verify_);
     // ---- join, read digests, end ------------------------------------------------
     TG_CUDA(cudaStreamWaitEvent(s_main_, ev(5)));
     TG_CUDA(cudaStreamWaitEvent(s_main_, ev(7)));
@@ -1183,7 +1237,7 @@ void fingerprint_device(const void* ptr, u64 n, int device, Digest* out) {
     cudaStream_t s;
     TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     void* d = nullptr;
-    TG_CUDA(cudaMallocAsync(&d, sizeof(FpTask) + 5 * sizeof(u64), s));
+    TG_CUDA(cudaMallocAsync(&d, sizeof(FpTask) + 6 * sizeof(u64), s));
     TG_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(FpTask), cudaMemcpyHostToDevice, s));
     auto* sums = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(d) + sizeof(FpTask));
     TG_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(u64), s));
@@ -1213,7 +1267,7 @@ double bench_fingerprint(const std::vector<std::pair<const void*, u64>>& bufs, i
     TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     void* d = nullptr;
     const std::size_t per = 4 * sizeof(u64) * nt;  // sums + digests per rep
-    TG_CUDA(cudaMalloc(&d, sizeof(FpTask) * nt + per * (reps + 1) + sizeof(u64)));
+    TG_CUDA(cudaMalloc(&d, sizeof(FpTask) * nt + per * (reps + 1) + 2 * sizeof(u64)));
     TG_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(FpTask) * nt, cudaMemcpyHostToDevice, s));
     auto* sums = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(d) + sizeof(FpTask) * nt);
     TG_CUDA(cudaMemsetAsync(sums, 0, per * (reps + 1), s));
@@ -1262,7 +1316,7 @@ double bench_copy_fp(const std::vector<MoveDesc>& moves, int device, int reps, s
     TG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     void* d = nullptr;
     const std::size_t per = 4 * sizeof(u64) * nt;
-    TG_CUDA(cudaMalloc(&d, sizeof(CopyFpTask) * nt + per * (reps + 1) + sizeof(u64)));
+    TG_CUDA(cudaMalloc(&d, sizeof(CopyFpTask) * nt + per * (reps + 1) + 2 * sizeof(u64)));
     TG_CUDA(cudaMemcpyAsync(d, t.data(), sizeof(CopyFpTask) * nt, cudaMemcpyHostToDevice, s));
     auto* sums = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(d) + sizeof(CopyFpTask) * nt);
     TG_CUDA(cudaMemsetAsync(sums, 0, per * (reps + 1), s));

@@ -221,7 +221,7 @@ public:
     // Device tensor index: republish the store's tensor map to
     // HBM on the pool stream when it changed since the last publish (no-op on
     // control-plane pools).  device_index() is the published table.
-    void publish_index();
+    void publish_index(cudaStream_t stream = nullptr);  // upload stream (null: the pool stream)
     const void* device_index(u64* capacity) const {
         *capacity = index_cap_;
         return d_index_;
