@@ -125,11 +125,11 @@ int main(int argc, char** argv) {
         const auto& b = l.value().device;
         std::fprintf(stderr,
                      "{\"repaired\": [%llu, %llu], \"suspect\": [%u, %u], \"fingerprinted\": [%llu, %llu], "
-                     "\"mismatches\": [%u, %u], \"second_pcie\": %llu}\n",
+                     "\"mismatches\": [%u, %u], \"second_placed\": %llu}\n",
                      (unsigned long long)a.repaired_bytes, (unsigned long long)b.repaired_bytes, a.suspect_tensors,
                      b.suspect_tensors, (unsigned long long)a.fingerprint_bytes,
                      (unsigned long long)b.fingerprint_bytes, a.verify_mismatches, b.verify_mismatches,
-                     (unsigned long long)w.value().device.pcie_bytes);
+                     (unsigned long long)(w.value().device.pcie_bytes + w.value().device.device_src_bytes));
     }
 #endif
     return 0;

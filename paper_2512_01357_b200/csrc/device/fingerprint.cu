@@ -658,21 +658,25 @@ __device__ __forceinline__ void digest_of(u64 sum_h, u64 sum_l, u64 n, u64* out)
     out[1] = h2;
 }
 
-// The last CTA of the launch to finish writes every task's digest, so a load
-// needs no second kernel (threadFenceReduction pattern: each CTA's sums are
-// device-visible before its ticket, the last ticket sees them all).
+// The last warp of the launch to finish writes every task's digest, so a load
+// needs no second kernel (threadFenceReduction pattern at warp granularity:
+// each warp's sums are device-visible before its ticket, the last ticket
+// sees them all).  No shared memory and no CTA barrier: a static __shared__
+// flag here shifts the dynamic stage ring and cost K1 8-12 % (A/B on one
+// box, 8 GiB: 5.6-5.9 vs 6.4-6.8 TB/s).
 template <class Task>
 __device__ __forceinline__ void finalize_if_last(const Task* __restrict__ tasks, u32 n_tasks,
                                                  const u64* __restrict__ sums, u64* __restrict__ digests,
                                                  unsigned long long* __restrict__ done) {
-    __shared__ int s_last;
+    const u32 lane = threadIdx.x & 31;
     __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(done, 1ull) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
+    __syncwarp();
+    unsigned long long ticket = 0;
+    if (lane == 0) ticket = atomicAdd(done, 1ull);
+    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    if (ticket != static_cast<unsigned long long>(gridDim.x) * (blockDim.x >> 5) - 1) return;
     __threadfence();
-    for (u32 i = threadIdx.x; i < n_tasks; i += blockDim.x)
+    for (u32 i = lane; i < n_tasks; i += 32)
         digest_of(__ldcg(sums + 2 * i), __ldcg(sums + 2 * i + 1), tasks[i].n, digests + 2 * i);
 }
 

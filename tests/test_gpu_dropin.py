@@ -50,7 +50,7 @@ def test_store_copy_semantics_on_a_device_pool():
     assert a.stdout == b.stdout
     rep = json.loads(b.stderr.decode().strip().splitlines()[-1])
     assert rep["suspect"] == [0, 0] and sum(rep["repaired"]) > 0 and min(rep["fingerprinted"]) > 0
-    assert rep["second_pcie"] > 0  # the surviving copy kept the device pool
+    assert rep["second_placed"] > 0  # the surviving copy kept the device pool (bytes really placed)
     print(rep)
 
 
