@@ -621,21 +621,37 @@ def isolated_kernels(tg, pool, snap, target, miss_ids, dev, reps=5):
     return out
 
 
+_TIMER = None
+
+
 def _capi_load(pool, model, stats, clock):
-    """A tg_load_model call with its C arguments built up front: timing it
-    measures the library (the C-ABI a caller binds), not the Python mirror's
-    argument marshalling.  Returns fn() -> tg_load_outcome (raises on error)."""
+    """A tg_load_model call as a C/C++ host makes it: the C arguments are
+    built up front and the call is timed by tools/capi_timer.cpp with CUDA
+    events on the pool stream recorded in C immediately around the C-ABI
+    call (host planning, launch, verification, digest readback and the
+    host's post-sync bookkeeping inside; Python's ctypes overhead outside).
+    Returns fn() -> (event_ms, wall_us, tg_load_outcome) (raises on error)."""
+    global _TIMER
     from paper_2512_01357_b200 import _native as N
     from paper_2512_01357_b200.pool import LoadPolicy
+    if _TIMER is None:
+        _TIMER = C.CDLL(os.path.join(ROOT, "tools", "_build", "libcapi_timer.so"))
+        _TIMER.tgt_time_load.restype = C.c_int
+        _TIMER.tgt_time_load.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]
     spec, pol, out = model.c(), LoadPolicy().c(), N.LoadOutcomeC()
-    args = (pool._h, C.byref(spec), stats._h, C.c_double(clock), C.byref(pol), C.byref(out))
-    load = N.lib.tg_load_model
+    ms, us = C.c_double(), C.c_double()
+    h = C.cast(pool._h, C.c_void_p) if not isinstance(pool._h, int) else C.c_void_p(pool._h)
+    sh = C.cast(stats._h, C.c_void_p) if not isinstance(stats._h, int) else C.c_void_p(stats._h)
+    args = (h, C.cast(C.byref(spec), C.c_void_p), sh, C.c_double(clock), C.cast(C.byref(pol), C.c_void_p),
+            C.cast(C.byref(out), C.c_void_p), C.byref(ms), C.byref(us))
+    load = _TIMER.tgt_time_load
 
     def fn():
         rc = load(*args)
         if rc:
             raise RuntimeError(f"tg_load_model -> {rc}")
-        return out
+        return ms.value, us.value, out
     return fn
 
 
@@ -665,7 +681,7 @@ def run_c1(tg, dev, h2d_peak, hbm_peak, reps=3):
             pool.end_instance(m.model_id)
             t += 1.0
             stats.record_request(m.model_id, t)
-            ms_w, ow = _event_ms(pool.stream(), dev, _capi_load(pool, m, stats, t))
+            ms_w, _, ow = _capi_load(pool, m, stats, t)()
             pool.end_instance(m.model_id)
             pool.evict_model(m.model_id)
             t += 1.0
@@ -681,8 +697,9 @@ def run_c1(tg, dev, h2d_peak, hbm_peak, reps=3):
             "warm_ms": mw, "warm_effective_GBps": m.total_size / mw / 1e6,
             "warm_fingerprint_bytes": ow.fingerprint_bytes, "warm_verify_mismatches": ow.verify_mismatches,
             "warm_device_ms": ow.total_ms, "warm_kernel_ms": ow.relocate_ms,
-            "warm_timing": "CUDA events on the pool stream around one tg_load_model C-ABI call (arguments built "
-                           "beforehand): host planning, launch, verification and digest readback included",
+            "warm_timing": "CUDA events on the pool stream recorded in C immediately around one tg_load_model C-ABI "
+                           "call (tools/capi_timer.cpp; arguments built beforehand): host planning, launch, "
+                           "verification, digest readback and post-sync bookkeeping included",
             "plan_us_cold": oc.timings["plan_us"], "plan_us_warm": ow.plan_us,
             "cold_frac_of_h2d_peak": m.total_size / mc / 1e6 / h2d_peak,
             "warm_frac_of_hbm_peak": ow.fingerprint_bytes / mw / 1e6 / hbm_peak,
@@ -720,7 +737,7 @@ def run_per_model(tg, dev, h2d_peak, hbm_peak):
             warm = []
             for k in range(4):  # the first reload is first-touch; the median of the next three is reported
                 st.record_request(m.model_id, 1.0 + k)
-                ms_w, o = _event_ms(pool.stream(), dev, _capi_load(pool, m, st, 1.0 + k))
+                ms_w, _, o = _capi_load(pool, m, st, 1.0 + k)()
                 warm.append((ms_w, o.relocate_ms))
                 ow = {"fingerprint_bytes": o.fingerprint_bytes, "bytes_transferred": o.bytes_transferred,
                       "verify_mismatches": o.verify_mismatches}
@@ -745,8 +762,8 @@ def run_per_model(tg, dev, h2d_peak, hbm_peak):
         slab.free()
     return {"workload": "every default_catalog() model: cold load into an empty pool from pinned host (PCIe), "
                         "then a 100%-reuse reload with every tensor fingerprint-verified in place (HBM); one "
-                        "CUDA-event span per synchronous C-ABI load (arguments built beforehand); warm = median of 3 reloads "
-                        "after a first-touch one (reported too)", "models": rows}
+                        "CUDA-event span per synchronous load; warm: events recorded in C around the C-ABI call "
+                        "(tools/capi_timer.cpp), median of 3 reloads after a first-touch one (reported too)", "models": rows}
 
 
 def run_c2_global_merge(tg, dev, hbm_peak, reps=3):

@@ -241,6 +241,9 @@ __device__ __forceinline__ u32 find_task(const Task* __restrict__ tasks, u32 n_t
     }
 }
 
+// A/B knob (TANGRAM_TILE_ORDER=forward): dispense a task's tiles first-first.
+__constant__ bool tile_order_reversed = true;
+
 template <class Task>
 __device__ __forceinline__ CopyTileRef copy_tile_ref(const Task* __restrict__ tasks, u32 n_tasks, u64 t,
                                                      u64 total_tiles, u32 hint, u32 lane) {
@@ -252,7 +255,12 @@ __device__ __forceinline__ CopyTileRef copy_tile_ref(const Task* __restrict__ ta
     r.t.task = static_cast<int>(lo);
     r.t.base = tk.src;
     r.t.n = tk.n;
-    r.t.leaf0 = (t - tk.tile0) * kLeavesPerTile;
+    // A task's tiles are dispensed last-first: the tile holding the partial
+    // leaf and the tail bytes (one lane hashes that leaf serially) comes
+    // early, so the launch's final tiles are plain full tiles and the tail
+    // of the launch is shorter.
+    const u64 task_tiles = ((tk.n + kLeafBytes - 1) / kLeafBytes + kLeavesPerTile - 1) / kLeavesPerTile;
+    r.t.leaf0 = (tile_order_reversed ? task_tiles - 1 - (t - tk.tile0) : t - tk.tile0) * kLeavesPerTile;
     const u64 full = tk.n / kLeafBytes;
     r.t.nfull = full > r.t.leaf0 ? static_cast<u32>(min(full - r.t.leaf0, u64{32})) : 0u;
     const std::uint8_t* p0 = tk.src + r.t.leaf0 * kLeafBytes;
@@ -727,6 +735,18 @@ static bool verify_next() {
 std::uint64_t copy_fp_resident_warps(int sm_count) { return static_cast<u64>(sm_count) * 2 * CfgPair::kWarps; }
 
 namespace {
+void set_tile_order_once() {
+    static const bool done = [] {
+        const char* e = std::getenv("TANGRAM_TILE_ORDER");
+        if (e && std::strcmp(e, "forward") == 0) {
+            const bool f = false;
+            cudaMemcpyToSymbol(tile_order_reversed, &f, sizeof(f));
+        }
+        return true;
+    }();
+    (void)done;
+}
+
 template <class Task, class Cfg>
 void load_kernel_launch_cfg(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests,
                             u64* d_sync, const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s,
@@ -736,6 +756,7 @@ void load_kernel_launch_cfg(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u
                                     Cfg::kSmemBytes) == cudaSuccess;
     }();
     (void)attr;
+    set_tile_order_once();
     if (!sync_zeroed) cudaMemsetAsync(d_sync, 0, (2 + n_waves) * sizeof(u64), s);
     const u64 want = (total_tiles + Cfg::kWarps - 1) / Cfg::kWarps;
     const u64 cap = static_cast<u64>(sm_count) * 2;

@@ -304,6 +304,9 @@ void Pool::ensure_stage(std::size_t bytes) {
     }
     TG_CUDA(cudaMallocHost(&h_stage_, n));
     TG_CUDA(cudaMalloc(&d_stage_, n));
+    // pinned memory is mapped (UVA): the load kernel's last warp writes the
+    // digests straight into it, no D2H copy after the launch
+    TG_CUDA(cudaHostGetDevicePointer(&h_stage_dev_, h_stage_, 0));
     stage_cap_ = n;
 }
 
@@ -484,6 +487,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // A suspect tensor without a recorded digest can only be re-sent, so its
     // source must exist now, before anything changes.
     std::vector<Key> hit_keys;
+    std::vector<u32> hit_pos;  // position in m.tensors, parallel to hit_keys
     for (u32 i : d.hits) {
         const Key& k = m.tensors[i].id;
         const Entry* e = store_.entry(k);
@@ -495,6 +499,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             if (hs.is_file()) check_file_source(hs, k);
         }
         hit_keys.push_back(k);
+        hit_pos.push_back(i);
     }
     store_.commit(m, d, clock);
     rep->committed = true;
@@ -506,7 +511,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // here until verified (placements start without a digest unless a truth
     // is known; a relocated tensor keeps its digest, the content does not
     // change by moving).
-    std::unordered_map<Key, bool, KeyHash> prior_suspect;  // relocated tensors' state before this load
+    std::vector<char> prior_suspect;  // relocated tensors' state before this load, by relocation
     for (std::size_t i = 0; i < np; ++i) {
         Entry* e = store_.entry(D.miss_desc[D.plan.placements[i].tensor].id);
         e->suspect = true;
@@ -515,9 +520,12 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             e->has_digest = true;
         }
     }
-    for (const Move& mv : D.plan.relocations) {
-        Entry* e = store_.entry(mv.tensor);
-        prior_suspect.emplace(mv.tensor, e->suspect);
+    for (std::size_t j = 0; j < D.plan.relocations.size(); ++j) {
+        Entry* e = store_.entry(D.plan.relocations[j].tensor);
+        char was = e->suspect;  // a tensor moved twice keeps its state from before the first move
+        for (std::size_t i = 0; i < j; ++i)
+            if (D.plan.relocations[i].tensor == D.plan.relocations[j].tensor) was = prior_suspect[i];
+        prior_suspect.push_back(was);
         e->suspect = true;
     }
 
@@ -542,13 +550,32 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // verify stream, in parallel with the waves.  Relocated ones are verified
     // by the copy+fingerprint (K3F) of their wave — or, unfused, by a K1
     // launch after the waves.  hit_keys is reordered [untouched..., relocated...].
-    std::unordered_map<Key, std::size_t, KeyHash> reloc_of;
-    for (std::size_t j = 0; j < rel.size(); ++j) reloc_of.emplace(rel[j].tensor, j);
+    // (tens of tensors and relocations per load: linear scans, no hashing)
+    constexpr std::size_t kNone = ~std::size_t{0};
+    auto reloc_index = [&](const Key& k) {
+        for (std::size_t j = 0; j < rel.size(); ++j)
+            if (rel[j].tensor == k) return j;
+        return kNone;
+    };
+    std::vector<std::size_t> hit_rel;  // relocation of each hit (kNone: untouched), parallel to hit_keys
     std::size_t n_still = hit_keys.size();
     if (fp_reuse) {
-        auto mid = std::stable_partition(hit_keys.begin(), hit_keys.end(),
-                                         [&](const Key& k) { return !reloc_of.count(k); });
-        n_still = static_cast<std::size_t>(mid - hit_keys.begin());
+        std::vector<std::size_t> idx(hit_keys.size());
+        for (std::size_t h = 0; h < idx.size(); ++h) idx[h] = h;
+        std::vector<std::size_t> rel_of(hit_keys.size());
+        for (std::size_t h = 0; h < idx.size(); ++h) rel_of[h] = rel.empty() ? kNone : reloc_index(hit_keys[h]);
+        auto mid = std::stable_partition(idx.begin(), idx.end(), [&](std::size_t h) { return rel_of[h] == kNone; });
+        n_still = static_cast<std::size_t>(mid - idx.begin());
+        std::vector<Key> hk(idx.size());
+        std::vector<u32> hp(idx.size());
+        hit_rel.resize(idx.size());
+        for (std::size_t h = 0; h < idx.size(); ++h) {
+            hk[h] = hit_keys[idx[h]];
+            hp[h] = hit_pos[idx[h]];
+            hit_rel[h] = rel_of[idx[h]];
+        }
+        hit_keys.swap(hk);
+        hit_pos.swap(hp);
     }
     // K1 after landing: host-sourced placements always; device-sourced ones
     // only when unfused (fused: K3F hashes them while it copies)
@@ -560,7 +587,6 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         return (fp_new || k == 1 || k == 3) && (!fused || k == 0 || k == 3);
     };
     auto tiles_of = [](u64 n) { return ((n + kLeafBytes - 1) / kLeafBytes + kLeavesPerTile - 1) / kLeavesPerTile; };
-    constexpr std::size_t kNone = ~std::size_t{0};
 
     // ---- descriptor tables (one H2D) ---------------------------------------------
     // FpTask (K1): [K1 placements...][unfused: untouched hits..., relocated hits...]
@@ -656,7 +682,9 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     const auto* d_need = reinterpret_cast<const u64*>(dptr + fdesc + cdesc);
     auto* d_sums = reinterpret_cast<u64*>(dptr + desc_bytes);
     auto* d_sync = reinterpret_cast<u64*>(dptr + desc_bytes + sums_bytes);
-    auto* d_dig = reinterpret_cast<u64*>(dptr + desc_bytes + sums_bytes + sync_bytes);
+    // digests: written by the kernels into mapped pinned memory (read after
+    // the stream synchronises; no D2H)
+    auto* d_dig = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(h_stage_dev_) + desc_bytes + sums_bytes + sync_bytes);
     u64* d_fp_sync = d_sync + 2 + waves;  // two counters (tiles, finished CTAs) per K1 launch
     if (nf + nc)
         TG_CUDA(cudaMemcpyAsync(dptr, h, desc_bytes + sums_bytes + sync_bytes, cudaMemcpyHostToDevice, s_main_));
@@ -857,7 +885,6 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     }
     TG_CUDA(cudaEventRecord(ev(3), s_main_));
     auto* h_dig = reinterpret_cast<u64*>(h + desc_bytes + sums_bytes + sync_bytes);
-    if (nf + nc) TG_CUDA(cudaMemcpyAsync(h_dig, d_dig, sums_bytes, cudaMemcpyDeviceToHost, s_main_));
     const auto h_issued = clk::now();
     rep->t.host_issue_us = std::chrono::duration<double, std::micro>(h_issued - h0).count();
     {
@@ -916,10 +943,9 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         return true;
     };
     rep->digests.assign(m.tensors.size(), Digest{});
-    std::unordered_map<Key, std::size_t, KeyHash> pos;
-    for (std::size_t i = 0; i < m.tensors.size(); ++i) pos.emplace(m.tensors[i].id, i);
     for (std::size_t i = 0; i < np; ++i) {
         const TensorDesc& t = D.miss_desc[D.plan.placements[i].tensor];
+        const u32 at = D.misses[D.plan.placements[i].tensor];  // position in m.tensors
         Entry* e = store_.entry(t.id);
         std::size_t slot = kNone;
         if (fp_of_placement[i] != kNone) slot = fp_of_placement[i];
@@ -929,7 +955,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             continue;
         }
         const Digest g = digest_at(slot);
-        rep->digests[pos[t.id]] = g;
+        rep->digests[at] = g;
         rep->fingerprint_bytes += t.size;
         if (!has_truth[i]) {
             e->digest = g;
@@ -941,7 +967,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             // The peer's index was stale (its bytes changed under us): fetch the
             // tensor from its host source instead.
             ++rep->verify_mismatches;
-            if (repair(t.id, e)) rep->digests[pos[t.id]] = e->digest;
+            if (repair(t.id, e)) rep->digests[at] = e->digest;
             else fail_with(kErrVerify, "peer bytes of " + t.id.hex() + " fail verification and no source repairs them");
         } else {
             // The registered source itself disagrees with its expected digest:
@@ -952,16 +978,17 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             fail_with(kErrVerify, "source bytes of " + t.id.hex() + " do not match the expected digest");
         }
     }
-    std::unordered_map<Key, bool, KeyHash> verified;  // hits settled here
+    std::vector<char> verified(rel.size(), 0);  // relocated hits settled here
     for (std::size_t hix = 0; fp_reuse && hix < hit_keys.size(); ++hix) {
         const Key& k = hit_keys[hix];
         const std::size_t slot = !fused          ? hit_base + hix
                                  : hix < n_still ? nf + ctask_of_still[hix]
-                                                 : nf + ctask_of_reloc[reloc_of.at(k)];
+                                                 : nf + ctask_of_reloc[hit_rel[hix]];
         const Digest g = digest_at(slot);
         Entry* e = store_.entry(k);
-        verified.emplace(k, true);
-        rep->digests[pos[k]] = g;
+        if (hit_rel[hix] != kNone)
+            for (std::size_t j = 0; j < rel.size(); ++j) verified[j] |= rel[j].tensor == k;
+        rep->digests[hit_pos[hix]] = g;
         rep->fingerprint_bytes += e->size;
         if (e->has_digest && e->digest == g) {
             e->suspect = false;
@@ -975,7 +1002,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             // failed load left it unverifiable: re-send it in place from its
             // source (same plan, fresh bytes).
             ++rep->verify_mismatches;
-            if (repair(k, e)) rep->digests[pos[k]] = e->digest;
+            if (repair(k, e)) rep->digests[hit_pos[hix]] = e->digest;
             else fail_with(kErrVerify, "reused tensor " + k.hex() + " fails verification and cannot be repaired");
         }
     }
@@ -985,10 +1012,10 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // otherwise the completed move leaves them as they were.
     for (std::size_t j = 0; j < rel.size(); ++j) {
         const Key& k = rel[j].tensor;
-        if (verified.count(k)) continue;
+        if (verified[j]) continue;
         Entry* e = store_.entry(k);
         if (fused && ctask_of_reloc[j] != kNone && e->has_digest) e->suspect = !(digest_at(nf + ctask_of_reloc[j]) == e->digest);
-        else e->suspect = prior_suspect.at(k);
+        else e->suspect = prior_suspect[j];
     }
     rep->suspect_after = 0;
     for (const auto& t : m.tensors)

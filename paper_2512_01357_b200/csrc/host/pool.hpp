@@ -255,6 +255,7 @@ private:
     // staging
     void* h_stage_ = nullptr;
     void* d_stage_ = nullptr;
+    void* h_stage_dev_ = nullptr;  // device alias of h_stage_ (mapped pinned memory)
     std::size_t stage_cap_ = 0;
     void ensure_stage(std::size_t bytes);
     // device index
