@@ -151,6 +151,17 @@ def peaks():
 
 
 # ---- CPU path (reference arm and cpu_baseline) ------------------------------------------------
+def host_ram_gib():
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal:"):
+                    return round(int(ln.split()[1]) / (1 << 20), 1)
+    except OSError:
+        pass
+    return None
+
+
 def cpu_load_once(ref, cpu, rcat, arena, sources, threads):
     """The reference's CPU path for load #3: ReuseStore::load_model (compiled
     reference) + apply_plan's bytes on a host arena (oracle port), all threads.
@@ -207,7 +218,7 @@ def cpu_setup(ref, cpu, threads):
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return 0
     from oracle import cpu, ref
@@ -235,7 +246,8 @@ def run_reference_arm(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": "C2 OPT-6.7B->OPT-13B switch, load #3, 32 GiB pool (host arena)",
                        "threads": threads},
-            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample,
+                             "host_ram_gib": host_ram_gib()},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -401,7 +413,7 @@ def run_ours(args):
         if c4_secondary:
             free_c2_working_set()
             try:
-                c4_measure(tg, rank, world, local, 2, 1)
+                c4_measure(tg, rank, world, local, max(5, args.steps), max(1, min(args.warmup, 2)))
             except Exception as e:  # pragma: no cover
                 print(f"rank {rank}: C4 secondary failed: {e}", file=sys.stderr)
         if world > 1:
@@ -437,12 +449,13 @@ def run_ours(args):
 
     cpu_base = None
     extras = {}
+    c4 = None
     if c4_secondary:
         free_c2_working_set()
         try:
-            extras["c4"] = c4_measure(tg, rank, world, local, 2, 1)
+            c4 = c4_measure(tg, rank, world, local, max(5, args.steps), max(1, min(args.warmup, 2)))
         except Exception as e:  # pragma: no cover
-            extras["c4"] = {"error": f"{type(e).__name__}: {e}"}
+            c4 = {"error": f"{type(e).__name__}: {e}"}
     if not args.profile and world == 1:
         free_c2_working_set()  # before the secondary configs
         for key, fn in (("c1", lambda: run_c1(tg, local, h2d_peak, hbm_peak)), ("c3", lambda: run_c3(tg, local)),
@@ -482,8 +495,11 @@ def run_ours(args):
             "frac": (kernels.get("k1", {}).get("GBps") or 0) / hbm_peak, "traffic": None,
             "algorithmic_bytes_per_launch": fp_bytes, "ms_per_launch": kernels.get("k1", {}).get("ms_per_launch"),
             "peak_source": peak_src, "in_step": {"GBps": fp_ach}}
+    metric = METRIC if not shared_gpu() else (
+        f"effective load GB/s, {SEQ[1]}->{SEQ[2]} switch (load #3, {1 - o_v.bytes_transferred / total:.1%} tensor "
+        f"reuse, {POOL >> 30} GiB pool)")
     line = {
-        "metric": METRIC,
+        "metric": metric,
         "value": world * total / (mv / 1e3) / 1e9,
         "unit": "GB/s",
         "n_gpus": world,
@@ -496,7 +512,7 @@ def run_ours(args):
         "dtype": "u8",
         "data": "synthetic: reference catalog tensor lists, splitmix64 bytes keyed by TensorId",
         "config": {
-            "workload": "C2 OPT-6.7B->OPT-13B switch, load #3 (opt13B) in a 32 GiB pool",
+            "workload": f"C2 switch {SEQ[0]} -> {SEQ[1]} -> {SEQ[2]}, load #3 ({SEQ[2]}) in a {POOL >> 30} GiB pool",
             "model_bytes": total, "reuse_ratio": round(1 - o_v.bytes_transferred / total, 4),
             "bytes_transferred": o_v.bytes_transferred, "bytes_merged": o_v.bytes_merged,
             "relocations": len(o_d.plan.relocations), "waves": o_v.waves, "placements": len(miss_ids),
@@ -504,7 +520,8 @@ def run_ours(args):
             else "K3 waves + K1 passes (TANGRAM_UNFUSED)",
             "value_sources": "missing tensors resident in HBM (model cache), placed by the load kernel",
             "e2e_sources": "missing tensors in pinned host memory, cudaMemcpyAsync H2D",
-            "fingerprint": "tgfp1 over all 41 tensors (13 placed + 28 reused verified)",
+            "fingerprint": f"tgfp1 over all {len(target.tensors)} tensors ({len(miss_ids)} placed + {len(hits)} reused "
+                           f"verified)",
             "l2": "no flush: every step streams >= 20 GB, >> 126 MB L2; arena restored (D2D 32 GiB) between steps",
             "timing": "CUDA events on the pool stream around each synchronous load; snapshot restore untimed; "
                       "mean over steps, max over ranks",
@@ -516,8 +533,9 @@ def run_ours(args):
         "e2e": {"value": world * total / (me / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": me,
                 "h2d_bytes_per_step": o_e.pcie_bytes, "d2h_bytes_per_step": 16 * len(target.tensors)},
         "roofline": roofline_main,
-        "roofline_k1": {"bound": "hbm", "kernel": "K1 = load kernel with fingerprint-only tasks over the step's "
-                                                  "28 reused tensors at their final offsets, one launch, timed alone",
+        "roofline_k1": {"bound": "hbm", "kernel": f"K1 = load kernel with fingerprint-only tasks over the step's "
+                                                  f"{len(hits)} reused tensors at their final offsets, one launch, "
+                                                  f"timed alone",
                         "achieved": kernels.get("k1", {}).get("GBps"), "peak": hbm_peak, "unit": "GB/s",
                         "frac": (kernels.get("k1", {}).get("GBps") or 0) / hbm_peak,
                         "algorithmic_bytes_per_launch": fp_bytes,
@@ -527,7 +545,8 @@ def run_ours(args):
                                                   "tensor no copy streams) / step time",
                           "achieved": step_ach, "peak": hbm_peak, "unit": "GB/s", "frac": step_ach / hbm_peak,
                           "algorithmic_bytes_per_step": step_bytes},
-        "roofline_relocate": {"bound": "hbm", "kernel": "K3 relocate_kernel, the step's 3 WAR waves timed alone",
+        "roofline_relocate": {"bound": "hbm", "kernel": f"K3 relocate_bulk_kernel (TMA bulk copies), the step's "
+                                                        f"{o_v.waves} WAR waves timed alone",
                               "achieved": kernels.get("k3", {}).get("GBps_rw"), "peak": hbm_peak, "unit": "GB/s",
                               "frac": (kernels.get("k3", {}).get("GBps_rw") or 0) / hbm_peak,
                               "algorithmic_bytes_per_load": 2 * o_v.bytes_merged,
@@ -540,6 +559,12 @@ def run_ours(args):
         "clocks": clk,
         "parity": parity,
     }
+    if c4 is not None:
+        # N > 1: the sharded cold load (N PCIe links) and the neighbour peer
+        # pull (NVLink) lead the secondary results
+        line = {**{k: line[k] for k in list(line)[:12]}, "c4_sharded_and_peer": c4,
+                **{k: line[k] for k in list(line)[12:]}}
+        line["parity"]["c4_verify_mismatches_per_rank"] = c4.get("verify_mismatches_per_rank")
     if cpu_base:
         line["cpu_baseline"] = cpu_base
     if extras:
@@ -1081,14 +1106,40 @@ def cpu_baseline(args):
     threads = args.cpu_threads or os.cpu_count()
     rcat, arena, sources, keep = cpu_setup(ref, cpu, threads)
     cpu_load_once(ref, cpu, rcat, arena, sources, threads)
-    times = [cpu_load_once(ref, cpu, rcat, arena, sources, threads)[0] for _ in range(2)]
-    sec = min(times)
+    times = [cpu_load_once(ref, cpu, rcat, arena, sources, threads)[0] for _ in range(5)]
+    sec = statistics.median(times)
     total = rcat[SEQ[2]]["total_size"]
     return {"value": total / sec / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
-            "ms_per_step": sec * 1e3,
-            "sample": "2 timed replays of load #3 on a 32 GiB host arena: reference ReuseStore::load_model "
-                      "(oracle/_ref) + CPU data plane port (memmove relocations, memcpy placements, tgfp1 of all "
-                      "41 tensors)"}
+            "ms_per_step": sec * 1e3, "ms_all": [t * 1e3 for t in times], "host_ram_gib": host_ram_gib(),
+            "sample": f"median of 5 timed replays of load #3 (after 1 untimed) on a {POOL >> 30} GiB host arena: "
+                      f"reference ReuseStore::load_model (oracle/_ref) + CPU data plane port (memmove relocations, "
+                      f"memcpy placements, tgfp1 of all {len(rcat[SEQ[2]]['tensors'])} tensors), {threads} threads"}
+
+
+def measure_p2p_peak(local, peer, n=1 << 30, reps=5):
+    """The NVLink roofline of the peer pull, measured in this run: a plain
+    copy-engine copy (torch, cudaMemcpyPeerAsync underneath) of n bytes from
+    the neighbour GPU's memory into this GPU's, best of `reps`, CUDA events on
+    the local stream.  Every rank runs it at the same time, reading its right
+    neighbour — the peer pull's own traffic pattern.  On a shared-GPU flow
+    check the "peer" is this device (a D2D copy, labelled as such)."""
+    import torch
+    src = torch.empty(n, dtype=torch.uint8, device=f"cuda:{peer}")
+    dst = torch.empty(n, dtype=torch.uint8, device=f"cuda:{local}")
+    s = torch.cuda.current_stream(local)
+    best = 1e9
+    for r in range(reps + 1):
+        torch.cuda.synchronize(local)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        dst.copy_(src, non_blocking=True)
+        b.record(s)
+        b.synchronize()
+        if r:
+            best = min(best, a.elapsed_time(b))
+    del src, dst
+    torch.cuda.empty_cache()
+    return n / (best / 1e3) / 1e9
 
 
 def c4_measure(tg, rank, world, local, steps, warmup):
@@ -1098,15 +1149,22 @@ def c4_measure(tg, rank, world, local, steps, warmup):
     and indexes (all_gather_object), then each rank loads its right
     neighbour's shard — every byte is pulled from the neighbour's pool over
     NVLink by the load kernel and fingerprint-verified against the
-    neighbour's digest.  Collective calls match on every rank; returns the
-    max-over-ranks result (all ranks)."""
+    neighbour's digest.  The NVLink roofline is a copy-engine peer copy
+    measured in the same run.  Collective calls match on every rank; returns
+    the max-over-ranks result (all ranks)."""
     import torch.distributed as dist
     from paper_2512_01357_b200.checkpoint import HostCheckpoint
     gpt = catalog(tg)["gpt20B"]
     mine = tg.shard_model(gpt, rank, world)
     right = tg.shard_model(gpt, (rank + 1) % world, world)
+    peer_dev = local if shared_gpu() else (local + 1) % world  # one node: device = local rank
+    p2p_peak = None
+    if world > 1:
+        dist.barrier()
+        p2p_peak = measure_p2p_peak(local, peer_dev)
+    h2d_peak = measured_h2d_peak(local)
     pool = tg.ReuseStore(tg.GpuSpec(f"gpu{local}", mine.total_size + right.total_size + GIB), device=local)
-    cold_ms, peer_ms, peer_bytes, verify = [], [], 0, 0
+    cold_ms, peer_ms, peer_bytes, verify, kernel_ms = [], [], 0, 0, []
     with HostCheckpoint([mine], device=local):
         for step in range(warmup + steps):
             pool.evict_model(right.model_id)
@@ -1134,25 +1192,41 @@ def c4_measure(tg, rank, world, local, steps, warmup):
                     right, st, 1.0, tg.LoadPolicy(flags=1 | 2 | 4 | 8), details=False).value())
                 if step >= warmup:
                     peer_ms.append(ms)
+                    kernel_ms.append(o.timings["relocate_ms"])
                 peer_bytes = o.peer_bytes
                 verify += o.verify_mismatches
                 dist.barrier()
     mc = statistics.mean(cold_ms)
     mp_ = statistics.mean(peer_ms) if peer_ms else None
+    mk = statistics.mean(kernel_ms) if kernel_ms else None
+    per_rank_verify = [verify]
     if world > 1:
-        mc, mp_, v = reduce_max([mc, mp_ or 0.0, float(verify)], local)
-        verify = int(v)
+        per_rank_verify = [None] * world
+        dist.all_gather_object(per_rank_verify, verify)
+        mc, mp_, mk = reduce_max([mc, mp_ or 0.0, mk or 0.0], local)
+        p2p_peak = reduce_max([-p2p_peak], local)[0] * -1  # the slowest rank's link
+        h2d_peak = reduce_max([-h2d_peak], local)[0] * -1
     pool.close()
+    peer = None
+    if mp_:
+        ach = peer_bytes / (mp_ / 1e3) / 1e9
+        peer = {"what": "each rank loads its right neighbour's shard from the neighbour's pool (CUDA IPC + the load "
+                        "kernel over NVLink), every byte fingerprint-verified against the neighbour's digest",
+                "bytes_per_rank": peer_bytes, "ms": mp_, "load_kernel_ms": mk,
+                "per_rank_GBps": ach, "aggregate_GBps": world * ach,
+                "roofline": {"bound": "nvlink", "achieved": ach, "peak": p2p_peak, "unit": "GB/s",
+                             "frac": ach / p2p_peak if p2p_peak else None,
+                             "peak_source": ("D2D copy on the shared GPU (flow check, not NVLink)" if shared_gpu()
+                                             else "copy-engine peer copy of 1 GiB from the right neighbour, all ranks "
+                                                  "at once, measured in this run (min over ranks)")}}
     return {"workload": "C4 GPT-20B sharded 1/N per rank (shard r = bytes [r*ceil(n/N), ...) of every tensor)",
-            "n_ranks": world, "shard_bytes_rank0": mine.total_size,
+            "n_ranks": world, "steps": steps, "warmup": warmup, "shard_bytes_rank0": mine.total_size,
             "cold_ms": mc, "cold_aggregate_GBps": gpt.total_size / (mc / 1e3) / 1e9,
             "cold_per_rank_GBps": mine.total_size / (mc / 1e3) / 1e9,
-            "peer": None if mp_ is None else {
-                "what": "each rank loads its right neighbour's shard from the neighbour's pool (CUDA IPC + the load "
-                        "kernel over NVLink), fingerprint-verified",
-                "ms": mp_, "per_rank_GBps": peer_bytes / (mp_ / 1e3) / 1e9, "peak_GBps": 770.0,
-                "peak_source": "B200_PROFILING.md measured peer copy per direction"},
-            "verify_mismatches": verify}
+            "cold_roofline": {"bound": "pcie", "achieved": mine.total_size / (mc / 1e3) / 1e9, "peak": h2d_peak,
+                              "unit": "GB/s", "frac": mine.total_size / (mc / 1e3) / 1e9 / h2d_peak,
+                              "peak_source": "pinned H2D 2 GiB per rank in this run (min over ranks)"},
+            "peer": peer, "verify_mismatches_per_rank": per_rank_verify}
 
 
 def run_c4(args):
@@ -1176,9 +1250,37 @@ def run_c4(args):
     return 0
 
 
+def free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args):
+    """`--gpus N` without torchrun: launch the N ranks ourselves (one process
+    per GPU, the same command line) and pass rank 0's line through."""
+    if not shared_gpu():
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible "
+                             f"(TANGRAM_BENCH_SHARED_GPU=1 runs the N-rank flow on one GPU)")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     global POOL, SEQ
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if args.impl == "reference" and world_env is None:
+        return run_reference_arm(args)  # the CPU path: one process, no ranks to launch
+    if world_env is None and args.gpus > 1:
+        return self_launch(args)
+    if world_env is not None and int(world_env) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}: launch one rank per GPU")
     if shared_gpu():  # flow check of N > 1 on one GPU: a switch small enough for N copies
         POOL, SEQ = 7 * GIB, ["qwen3B", "opt1.3B", "qwen3B"]  # 9 relocations, 1.2 GB placed
     if args.impl == "reference":
