@@ -462,6 +462,7 @@ def run_ours(args):
                         ("c5", lambda: run_c5(local)),
                         ("c2_global_merge", lambda: run_c2_global_merge(tg, local, hbm_peak)),
                         ("reuse_sweep", lambda: run_reuse_sweep(tg, local, h2d_peak)),
+                        ("model_store", lambda: run_model_store(tg, local, h2d_peak)),
                         ("per_model", lambda: run_per_model(tg, local, h2d_peak, hbm_peak))):
             try:  # a secondary config never takes the headline line down
                 extras[key] = fn()
@@ -731,6 +732,95 @@ def run_c1(tg, dev, h2d_peak, hbm_peak, reps=3):
             "roofline_note": "cold: whole-load latency vs the measured pinned-H2D peak; warm: fingerprint bytes "
                              "read once / whole-load latency (plan, launch, digest readback included) vs the "
                              "measured HBM copy peak"}
+
+
+def _pread_rate(path, size, threads, chunk=16 << 20):
+    """GB/s of reading `size` bytes of `path` with `threads` concurrent pread
+    streams of `chunk` bytes into reused buffers (the stager's read pattern
+    without the copy engine)."""
+    import concurrent.futures as cf
+    import time
+    import numpy as np
+    bufs = [np.empty(chunk, np.uint8) for _ in range(threads)]
+    fd = os.open(path, os.O_RDONLY)
+    try:
+        offs = list(range(0, size, chunk))
+        def work(k):
+            b = memoryview(bufs[k])
+            for o in offs[k::threads]:
+                n = min(chunk, size - o)
+                got = 0
+                while got < n:
+                    r = os.preadv(fd, [b[got:n]], o + got)
+                    if r <= 0:
+                        raise IOError("short read")
+                    got += r
+        t0 = time.perf_counter()
+        with cf.ThreadPoolExecutor(threads) as ex:
+            list(ex.map(work, range(threads)))
+        return size / (time.perf_counter() - t0) / 1e9
+    finally:
+        os.close(fd)
+
+
+def run_model_store(tg, dev, h2d_peak, reps=3):
+    """§8(f) row 2, Model Store → GPU (model.hpp:24 ModelLocation::ModelStore,
+    scheduler.hpp:43-47 min(store, pcie)): OPT-6.7B written to one checkpoint
+    file, every tensor registered as a file range (tg_file_register), then
+    cold-loaded into an empty pool: the pool's stager preads 16 MiB chunks
+    with 4 threads into a pinned ring while the copy engine drains it into
+    HBM, and the load kernel fingerprints every placed tensor.  Compared with
+    the plain pread rate of the same file (same threads and chunks, no
+    copy) and the pinned-H2D peak: the load is bounded by min(file read,
+    H2D)."""
+    import shutil
+    from paper_2512_01357_b200 import _native as N
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    m = {x.model_id: x for x in tg.default_catalog()}["opt6.7B"]
+    d = os.environ.get("TANGRAM_STORE_DIR", "/tmp")
+    if shutil.disk_usage(d).free < m.total_size + (4 << 30):
+        return {"unavailable": f"{d}: less than {m.total_size / 1e9:.1f} GB + 4 GiB free"}
+    path = os.path.join(d, f"tangram_store_{os.getpid()}.bin")
+    offs = {}
+    try:
+        with HostCheckpoint([m], device=dev, register=False) as ck, open(path, "wb") as f:
+            f.write(b"TGCK" * 3)  # odd header: file offsets of tensors unaligned, like a real checkpoint
+            for t in m.tensors:
+                offs[t.id] = f.tell()
+                f.write(memoryview(ck.view(t.id)))
+        for t in m.tensors:
+            N.check_runtime(N.lib.tg_file_register(t.id.c(), path.encode(), offs[t.id], t.size, None))
+        pool = tg.ReuseStore(tg.GpuSpec("gpu0", 16 * GIB), device=dev)
+        stats = tg.ModelStatsTable()
+        ms, fps, t = [], [], 0.0
+        for r in range(reps + 1):
+            stats.record_request(m.model_id, t)
+            ms_l, o = _event_ms(pool.stream(), dev, lambda: pool.load_model(m, stats, t, details=False).value())
+            assert o.pcie_bytes == m.total_size and o.verify_mismatches == 0
+            pool.end_instance(m.model_id)
+            pool.evict_model(m.model_id)
+            t += 1.0
+            if r:
+                ms.append(ms_l)
+        pool.close()
+        for t_ in m.tensors:
+            N.lib.tg_host_unregister(t_.id.c())
+        size = os.path.getsize(path)
+        pread4 = statistics.median(_pread_rate(path, size, 4) for _ in range(2))
+        pread8 = _pread_rate(path, size, 8)
+    finally:
+        if os.path.exists(path):
+            os.remove(path)
+    mean = statistics.mean(ms)
+    gbps = m.total_size / mean / 1e6
+    bound = min(max(pread4, pread8), h2d_peak)
+    return {"workload": f"Model Store cold load: opt6.7B ({m.total_size / 1e9:.1f} GB, {len(m.tensors)} tensors) "
+                        f"from one checkpoint file in {d} into an empty 16 GiB pool, every tensor fingerprinted",
+            "load_ms": mean, "file_to_hbm_GBps": gbps,
+            "pread_GBps_4_threads": pread4, "pread_GBps_8_threads": pread8, "h2d_peak_GBps": h2d_peak,
+            "frac_of_min_file_h2d": gbps / bound,
+            "note": "page-cache state: the file was just written (hot where RAM holds it); the pread rates are "
+                    "measured on the same file right after the loads, same chunking"}
 
 
 def run_per_model(tg, dev, h2d_peak, hbm_peak):
@@ -1031,43 +1121,103 @@ def run_c3(tg, dev):
             "bursts": out}
 
 
+def _replay(bin_, args, env, timeout=900):
+    """One simulator run: (stdout bytes, the binding's stderr report or None, rc)."""
+    r = subprocess.run([bin_] + args, capture_output=True, timeout=timeout, env=env)
+    rep = None
+    try:
+        rep = json.loads(r.stderr.decode().strip().splitlines()[-1])
+    except Exception:
+        pass
+    return r.stdout, rep, r.returncode
+
+
+C5_REAL_MODELS = ["opt1.3B", "qwen3B", "llama3B", "opt6.7B", "llama8B", "yi9B"]
+
+
 def run_c5(dev):
     """C5: the reference's own Simulator (unmodified
-    simulator.hpp) replays the Zipf trace over the drop-in bindings; pool gpu0
-    lives on this GPU and really moves and fingerprints bytes (every catalog
-    tensor's source synthesised in HBM), the other seven pools are
-    control-plane only.  RunMetrics must equal the pure-reference build's."""
+    simulator.hpp) replays Zipf traces over the drop-in bindings.
+
+    * full: the C5 config (8 x 48 GiB, 2,000 requests) with asynchronous loads
+      (TG_LOAD_ASYNC); pool gpuK lives on CUDA device K when it exists (so on
+      an 8-GPU box every pool moves real bytes and loads overlap across GPUs),
+      else control-plane only; sources synthesised in HBM on device 0.
+      RunMetrics must equal the pure-reference build's.
+    * real4: every pool real — 4 x 24 GiB pools on this GPU (one per GPU where
+      4 exist), the six smallest catalog models (62 GB, so models migrate
+      between pools), sources in pinned host memory: synchronous loads,
+      asynchronous loads (both byte-identical RunMetrics to the reference),
+      and the peer-aware schedule (TANGRAM_PEER_SCHEDULE: misses resident on
+      another pool come over NVLink / the SM copy instead of PCIe; decisions
+      differ from the reference's by design)."""
     import time
+    import torch
     build = os.path.join(ROOT, "integration", "_build")
     ref_bin, tg_bin = os.path.join(build, "sim_reference"), os.path.join(build, "sim_tangram")
     if not (os.path.exists(ref_bin) and os.path.exists(tg_bin)):
         return {"unavailable": "integration/_build binaries absent (built by build() where the reference exists)"}
+    out = {}
     args = ["reuse_odkv", "8", "48", "4", "2", "2000", "42", "0", "0", "L3"]
-    a = subprocess.run([ref_bin] + args, capture_output=True, timeout=600)
-    env = dict(os.environ, TANGRAM_DEVICE="auto", TANGRAM_SYNTH_SOURCES="1")  # gpu0 -> device 0
+    ref_out = subprocess.run([ref_bin] + args, capture_output=True, timeout=600).stdout
+    env = dict(os.environ, TANGRAM_DEVICE="auto", TANGRAM_SYNTH_SOURCES="1", TANGRAM_ASYNC_LOADS="1")
     t0 = time.perf_counter()
-    b = subprocess.run([tg_bin] + args, capture_output=True, timeout=600, env=env)
+    b_out, rep, rc = _replay(tg_bin, args, env)
     wall = time.perf_counter() - t0
-    try:
-        pools = json.loads(b.stderr.decode().strip().splitlines()[-1])["pools"]
-        g0 = [p for p in pools if p["gpu_id"] == "gpu0"][0]
-    except Exception as e:  # pragma: no cover
-        return {"unavailable": f"replay failed: {e}"}
-    moved = g0["relocated_bytes"] + g0["device_src_bytes"] + g0["pcie_bytes"]
-    ms = g0["data_plane_ms"]
-    return {"workload": "C5 Zipf trace (2,000 requests, seed 42, L3) on 8 x 48 GiB pools, ReuseOdkv, batch 4, "
-                        "keep-alive 2 s; reference Simulator over the drop-in bindings; gpu0 on this GPU with real "
-                        "bytes (HBM-resident sources), gpu1..7 control-plane only",
-            "run_metrics_equal_reference": a.returncode == 0 and b.returncode == 0 and a.stdout == b.stdout,
-            "gpu0_loads": g0["loads"], "gpu0_relocated_bytes": g0["relocated_bytes"],
-            "gpu0_placed_bytes": g0["device_src_bytes"] + g0["pcie_bytes"],
-            "gpu0_fingerprint_bytes": g0["fingerprint_bytes"], "gpu0_data_plane_ms": ms,
-            "gpu0_moved_GBps": moved / ms / 1e6 if ms > 0 else None,
-            "gpu0_hbm_rw_GBps": (2 * moved + g0["fingerprint_bytes"] - g0["device_src_bytes"]
-                                 - g0["relocated_bytes"]) / ms / 1e6 if ms > 0 else None,
-            "replay_wall_s": wall,
-            "note": "data_plane_ms = sum over gpu0's loads of the CUDA-event span of each synchronous load; "
-                    "hbm_rw counts moves r+w plus fingerprint reads not already covered by a move's read"}
+    if rep is None:
+        return {"unavailable": f"replay failed rc={rc}"}
+    real = [p for p in rep["pools"] if p["device"] >= 0]
+    moved = sum(p["relocated_bytes"] + p["device_src_bytes"] + p["pcie_bytes"] + p["peer_bytes"] for p in real)
+    out["full"] = {
+        "workload": "C5 Zipf trace (2,000 requests, seed 42, L3) on 8 x 48 GiB pools, ReuseOdkv, batch 4, "
+                    "keep-alive 2 s; reference Simulator over the drop-in bindings, asynchronous loads; pools on "
+                    f"devices: {[p['gpu_id'] for p in real]} (the rest control-plane only), HBM-resident sources",
+        "run_metrics_equal_reference": rc == 0 and b_out == ref_out,
+        "pools_with_bytes": len(real),
+        "loads": sum(p["loads"] for p in real),
+        "moved_bytes": moved,
+        "fingerprint_bytes": sum(p["fingerprint_bytes"] for p in real),
+        "verify_mismatches": sum(p["verify_mismatches"] for p in real),
+        "failed_loads": sum(p["failed_loads"] for p in real),
+        "data_plane_ms_per_pool": {p["gpu_id"]: p["data_plane_ms"] for p in real},
+        "replay_run_s": rep.get("run_s"), "replay_wall_s": wall}
+    ngpu = torch.cuda.device_count()
+    args4 = ["reuse_odkv", "4", "24", "4", "2", "400", "42", "0", "0", "L3", ",".join(C5_REAL_MODELS)]
+    ref4 = subprocess.run([ref_bin] + args4, capture_output=True, timeout=600).stdout
+    base_env = dict(os.environ, TANGRAM_SYNTH_SOURCES="host", TANGRAM_DEVICE="auto" if ngpu >= 4 else "0")
+    modes = {}
+    for name, extra in (("sync", {"TANGRAM_ASYNC_LOADS": "0"}), ("async", {"TANGRAM_ASYNC_LOADS": "1"}),
+                        ("peer", {"TANGRAM_ASYNC_LOADS": "1", "TANGRAM_PEER_SCHEDULE": "700"})):
+        o, r, rc = _replay(tg_bin, args4, dict(base_env, **extra))
+        if r is None:
+            modes[name] = {"error": f"rc={rc}"}
+            continue
+        pools = r["pools"]
+        pcie = sum(p["pcie_bytes"] for p in pools)
+        peer = sum(p["peer_bytes"] for p in pools)
+        dp = sum(p["pcie_bytes"] + p["peer_bytes"] + p["device_src_bytes"] + p["relocated_bytes"] for p in pools)
+        modes[name] = {
+            "run_metrics_equal_reference": rc == 0 and o == ref4,
+            "loads": sum(p["loads"] for p in pools), "pcie_bytes": pcie, "peer_bytes": peer,
+            "fingerprint_bytes": sum(p["fingerprint_bytes"] for p in pools),
+            "verify_mismatches": sum(p["verify_mismatches"] for p in pools),
+            "failed_loads": sum(p["failed_loads"] for p in pools),
+            "replay_run_s": r.get("run_s"), "replay_s": r.get("replay_s"),
+            "data_plane_ms_sum": sum(p["data_plane_ms"] for p in pools),
+            "placed_GBps_over_run": (pcie + peer) / r["run_s"] / 1e9 if r.get("run_s") else None,
+            "data_plane_GBps_over_run": dp / r["run_s"] / 1e9 if r.get("run_s") else None}
+    if "pcie_bytes" in modes.get("peer", {}) and "pcie_bytes" in modes.get("sync", {}):
+        modes["peer"]["pcie_bytes_saved_vs_reference_schedule"] = modes["sync"]["pcie_bytes"] - modes["peer"]["pcie_bytes"]
+    out["real4"] = {
+        "workload": "C5-shaped replay, every pool with real bytes: 4 x 24 GiB pools, models "
+                    f"{','.join(C5_REAL_MODELS)} (62 GB), 400 requests, seed 42, L3, ReuseOdkv, batch 4, keep-alive "
+                    f"2 s; sources in pinned host memory; pools on {'devices 0..3' if ngpu >= 4 else 'this one GPU'}",
+        "modes": modes,
+        "note": "run_s = wall time of Simulator::run (every pool's data plane included: async loads complete "
+                "before the pools report); peer mode uses the peer-aware schedule (estimate (S-S'-S'_peer)/B_pcie + "
+                "S'_peer/B_nvlink, B_nvlink = 700 GB/s) and TG_LOAD_PEER — its RunMetrics differ from the "
+                "reference's by design"}
+    return out
 
 
 def check_parity(tg, pool, target, host, cache, dev):

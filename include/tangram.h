@@ -53,6 +53,9 @@ extern "C" {
 #define TG_LOAD_FINGERPRINT_NEW 2u /* fingerprint placed tensors, record the digest */
 #define TG_LOAD_PEER 4u            /* pull misses resident on a peer pool over NVLink */
 #define TG_LOAD_FUSED 8u           /* one load-kernel launch (move + fingerprint in one pass) instead of K3 waves then K1 */
+#define TG_LOAD_ASYNC 16u           /* return once the decision is committed and the data plane enqueued;
+                                       the wait and the digest bookkeeping run at the pool's next operation
+                                       (or tg_pool_sync), so loads on different pools / GPUs overlap */
 #define TG_LOAD_DEFAULT 11u
 /* flags carrying this bit are taken literally: TG_LOAD_EXPLICIT alone asks for
  * no optional work (flags == 0 without it means TG_LOAD_DEFAULT) */
@@ -173,6 +176,9 @@ typedef struct {
     double data_plane_ms;
     uint64_t pcie_bytes, peer_bytes, device_src_bytes, fingerprint_bytes, relocated_bytes;
     uint64_t epoch; /* changes whenever the tensor map does (unique process-wide) */
+    /* integrity totals: reused / peer bytes that failed their fingerprint, bytes
+     * re-sent to repair them, loads that ended with a runtime error */
+    uint64_t verify_mismatches, repaired_bytes, failed_loads;
 } tg_pool_info;
 
 /* ReuseStore::tensor_map() entry (reuse_store.hpp:26-32); model_id valid while the pool is unchanged */
@@ -360,6 +366,15 @@ int tg_host_free(void* p);
  * would; nth <= 0 disarms.  "file_read": a checkpoint-file chunk reads short;
  * "h2d": the host->device copy of a placement fails with TG_ERR_CUDA.
  * One-shot; process-wide. */
+/* Finish an asynchronous load (TG_LOAD_ASYNC) still in flight on p: wait for its
+ * data plane, record / verify its digests.  out (nullable) receives that load's
+ * completed outcome (all zero when none was pending).  Returns 0, or the
+ * runtime error the load ended with (its unverified tensors are then suspect
+ * and re-sent on their next reuse, as after a failed synchronous load).  Every
+ * call that mutates p or reads digests finishes a pending load first; reads of
+ * the committed decisions (tg_reuse_size, tg_lookup, tg_dump, tg_pool_info_get
+ * ...) do not wait. */
+int tg_pool_sync(tg_pool* p, tg_load_outcome* out);
 int tg_failpoint(const char* name, int64_t nth);
 
 /* ---- raw device helpers ------------------------------------------------------ */

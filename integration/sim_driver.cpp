@@ -4,9 +4,12 @@
 // headers, once with integration/ first on the include path so that
 // "warmsim/reuse_store.hpp" and "warmsim/kv_engine.hpp" resolve to the B200
 // bindings.  tests/test_dropin.py requires byte-identical output.
+#include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <iostream>
+#include <sstream>
 #include <string>
 
 #include "json.hpp"
@@ -18,14 +21,25 @@ int main(int argc, char** argv) {
     using namespace warmsim;
     if (argc < 11) {
         std::fprintf(stderr,
-                     "usage: %s mode n_gpus pool_gib batch keep_alive n_requests seed eviction merge locality\n",
+                     "usage: %s mode n_gpus pool_gib batch keep_alive n_requests seed eviction merge locality "
+                     "[model,model,...]\n",
                      argv[0]);
         return 2;
     }
     const std::string mode = argv[1];
     const int n = std::atoi(argv[2]);
     const double pool_gib = std::atof(argv[3]);
-    const auto catalog = default_catalog();
+    // optional 11th argument: the catalog models the trace draws from
+    // (default: all of default_catalog())
+    auto catalog = default_catalog();
+    if (argc > 11) {
+        std::vector<ModelSpec> keep;
+        std::stringstream ss(argv[11]);
+        for (std::string id; std::getline(ss, id, ',');)
+            for (const auto& m : catalog)
+                if (m.model_id == id) keep.push_back(m);
+        catalog = keep;
+    }
     TraceSpec ts;
     ts.seed = std::strtoull(argv[7], nullptr, 10);
     ts.num_requests = std::strtoull(argv[6], nullptr, 10);
@@ -46,40 +60,82 @@ int main(int argc, char** argv) {
     cfg.emit_sched_log = true;
     cfg.emit_timeseries = true;
 #ifdef TANGRAM_BINDING
-    // Byte sources for every catalog tensor, synthesised in HBM on device 0
-    // (TANGRAM_SYNTH_SOURCES=1): pools that own a device then move real bytes.
-    std::vector<void*> sources;
-    if (std::getenv("TANGRAM_SYNTH_SOURCES")) {
+    // Byte sources for every catalog tensor (TANGRAM_SYNTH_SOURCES): "1" or
+    // "device" synthesises them in HBM on device 0 (an HBM model cache: pools
+    // place them with the load kernel); "host" in pinned host memory (pools
+    // load them over their PCIe link).  Pools that own a device then move
+    // real bytes.
+    std::vector<void*> sources, host_sources;
+    if (const char* mode = std::getenv("TANGRAM_SYNTH_SOURCES")) {
+        const bool host = std::string(mode) == "host";
+        void* scratch = nullptr;
+        Bytes biggest = 0;
+        for (const auto& model : catalog)
+            for (const auto& t : model.tensors) biggest = std::max(biggest, t.size);
+        if (host && tg_device_alloc(0, biggest, &scratch)) return 3;
         for (const auto& model : catalog)
             for (const auto& t : model.tensors) {
                 void* d = nullptr;
                 const tg_tensor_id id{t.id.hi, t.id.lo};
-                if (tg_device_alloc(0, t.size, &d) || tg_synth_fill_device(id, 0, t.size, d, 0) ||
-                    tg_host_register(id, d, t.size, nullptr)) {
+                int rc = 0;
+                if (host) {
+                    rc = tg_host_alloc(t.size, &d);
+                    if (!rc) rc = tg_synth_fill_device(id, 0, t.size, scratch, 0);
+                    if (!rc) rc = tg_memcpy(d, scratch, t.size);
+                    if (!rc) host_sources.push_back(d);
+                } else {
+                    rc = tg_device_alloc(0, t.size, &d);
+                    if (!rc) rc = tg_synth_fill_device(id, 0, t.size, d, 0);
+                    if (!rc) sources.push_back(d);
+                }
+                if (rc || tg_host_register(id, d, t.size, nullptr)) {
                     std::fprintf(stderr, "source setup failed: %s\n", tg_last_error_detail());
                     return 3;
                 }
-                sources.push_back(d);
             }
+        if (scratch) tg_device_free(0, scratch);
     }
 #endif
     RunMetrics m;
+    double replay_s = 0, setup_s = 0, run_s = 0;
     try {
-        Simulator sim(cfg, catalog);
-        m = sim.run(trace);
+        using sclk = std::chrono::steady_clock;
+        auto secs = [](sclk::time_point a, sclk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
+        const auto t0 = sclk::now();
+        auto t1 = t0;
+        {
+            Simulator sim(cfg, catalog);  // creates the pools (arena allocation)
+            t1 = sclk::now();
+            m = sim.run(trace);
+        }  // the stores' destructors land any load still in flight
+        const auto t3 = sclk::now();
+        replay_s = secs(t0, t3);
+        setup_s = secs(t0, t1);
+        run_s = secs(t1, t3);  // the run plus landing every load still in flight
     } catch (const std::exception& e) {  // ConfigError / RuntimeInfeasible: compare those too
         std::cout << nlohmann::json{{"exception", e.what()}}.dump() << "\n";
         return 0;
     }
+#ifndef TANGRAM_BINDING
+    (void)replay_s;
+    (void)setup_s;
+    (void)run_s;
+#endif
 #ifdef TANGRAM_BINDING
     // data-plane totals per pool (stderr, so stdout stays comparable)
     auto pools = nlohmann::json::array();
     for (const auto& [gid, i] : tgb::finished_pools())
         pools.push_back({{"gpu_id", gid}, {"device", i.device}, {"loads", i.loads}, {"data_plane_ms", i.data_plane_ms},
-                         {"pcie_bytes", i.pcie_bytes}, {"device_src_bytes", i.device_src_bytes},
-                         {"fingerprint_bytes", i.fingerprint_bytes}, {"relocated_bytes", i.relocated_bytes}});
-    std::cerr << nlohmann::json{{"pools", pools}}.dump() << "\n";
+                         {"pcie_bytes", i.pcie_bytes}, {"peer_bytes", i.peer_bytes},
+                         {"device_src_bytes", i.device_src_bytes}, {"fingerprint_bytes", i.fingerprint_bytes},
+                         {"relocated_bytes", i.relocated_bytes}, {"verify_mismatches", i.verify_mismatches},
+                         {"repaired_bytes", i.repaired_bytes}, {"failed_loads", i.failed_loads}});
+    // replay_s: wall time of the simulator's construction, run and
+    // destruction (every pool's data plane has finished inside it)
+    std::cerr << nlohmann::json{{"pools", pools}, {"replay_s", replay_s}, {"setup_s", setup_s}, {"run_s", run_s}}.dump()
+              << "\n";
     for (void* d : sources) tg_device_free(0, d);
+    for (void* d : host_sources) tg_host_free(d);
 #endif
     nlohmann::json j;
     auto recs = nlohmann::json::array();

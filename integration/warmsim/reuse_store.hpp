@@ -27,6 +27,15 @@
 // So `ReuseStore backup = s; s.load_model(...)` leaves backup the old state
 // and s on the GPU, and containers that copy stores on reallocation keep the
 // device with the surviving copy.
+//
+// Trace replay at full speed (§8(f) row 1):
+//  * TANGRAM_ASYNC_LOADS=1: loads return once the decision is committed
+//    (TG_LOAD_ASYNC) — the simulator only reads the decision — and each
+//    pool's data plane finishes in the background until that pool's next
+//    operation, so loads on different GPUs overlap;
+//  * TANGRAM_PEER_SCHEDULE=<GB/s> (warmsim/scheduler.hpp): every device pool
+//    is an NVLink peer of every other and loads with TG_LOAD_PEER, misses
+//    resident on another pool are pulled from it instead of over PCIe.
 #pragma once
 
 #include <cstdlib>
@@ -43,6 +52,7 @@
 #include "warmsim/packing.hpp"
 #include "warmsim/region_pool.hpp"
 #include "warmsim/rng.hpp"
+#include "warmsim/scheduler.hpp"  // the binding's (live device pools, peer term)
 #include "warmsim/types.hpp"
 
 namespace warmsim {
@@ -117,6 +127,14 @@ struct StatsHandle {
     StatsHandle& operator=(const StatsHandle&) = delete;
 };
 
+inline bool async_loads() {
+    static const bool on = [] {
+        const char* e = std::getenv("TANGRAM_ASYNC_LOADS");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
 inline int pick_device(const std::string& gpu_id) {
     const char* env = std::getenv("TANGRAM_DEVICE");
     const std::string mode = env ? env : "auto";
@@ -142,7 +160,14 @@ struct PoolDeleter {
     std::string gpu_id;
     bool record = true;  // snapshots (control-plane clones) are not reported
     void operator()(tg_pool* p) const {
+        auto& live = tgs::live_pools();
+        for (auto it = live.begin(); it != live.end(); ++it)
+            if (it->second == p) {
+                live.erase(it);
+                break;
+            }
         if (record) {
+            tg_pool_sync(p, nullptr);  // an asynchronous load still in flight lands first
             tg_pool_info i{};
             tg_pool_info_get(p, &i);
             finished_pools().push_back({gpu_id, i});
@@ -170,6 +195,15 @@ public:
         tg_pool* p = nullptr;
         if (int rc = tg_pool_create(&g, tgb::pick_device(gpu_.gpu_id), &p)) tgb::fail(rc, "tg_pool_create");
         box_ = std::make_shared<tgb::Box>(tgb::Box{std::shared_ptr<tg_pool>(p, tgb::PoolDeleter{gpu_.gpu_id}), this});
+        tg_pool_info i{};
+        tg_pool_info_get(p, &i);
+        if (i.device >= 0 && tgs::peer_bandwidth() > 0) {  // every device pool peers with every other
+            for (const auto& [gid, q] : tgs::live_pools()) {
+                tg_pool_add_peer(p, q);
+                tg_pool_add_peer(q, p);
+            }
+            tgs::live_pools()[gpu_.gpu_id] = p;
+        }
     }
 
     ReuseStore(const ReuseStore& o) : gpu_(o.gpu_), box_(o.box_) {}
@@ -306,6 +340,8 @@ public:
             pol.uniform_below = [](void* c, std::uint64_t n) { return static_cast<Rng*>(c)->uniform_below(n); };
             pol.rng_ctx = policy.rng;
         }
+        pol.flags = TG_LOAD_DEFAULT | (tgb::async_loads() ? TG_LOAD_ASYNC : 0u) |
+                    (tgs::peer_bandwidth() > 0 ? TG_LOAD_PEER : 0u);
         LoadOutcome out;
         const int rc = tgb::domain(tg_load_model(mutable_handle(), &v.spec, sh.h, clock, &pol, &out.device), "tg_load_model");
         if (rc) return static_cast<Error>(rc - 1);

@@ -83,7 +83,8 @@ class PoolInfoC(C.Structure):
                 ("bytes_transferred_total", u64), ("evictions_total", u64), ("region_count", u64),
                 ("extent_count", u64), ("tensor_count", u64), ("largest_free", u64), ("device", i32),
                 ("arena", vp), ("loads", u64), ("data_plane_ms", dbl), ("pcie_bytes", u64), ("peer_bytes", u64),
-                ("device_src_bytes", u64), ("fingerprint_bytes", u64), ("relocated_bytes", u64), ("epoch", u64)]
+                ("device_src_bytes", u64), ("fingerprint_bytes", u64), ("relocated_bytes", u64), ("epoch", u64),
+                ("verify_mismatches", u64), ("repaired_bytes", u64), ("failed_loads", u64)]
 
 
 class TensorEntryC(C.Structure):
@@ -153,6 +154,7 @@ _SIGS = {
     "tg_pool_stream": (C.c_int, [vp, P(vp)]),
     "tg_set_model_alpha": (C.c_int, [vp, cp, dbl]),
     "tg_load_model": (C.c_int, [vp, P(ModelSpecC), vp, dbl, P(LoadPolicyC), P(LoadOutcomeC)]),
+    "tg_pool_sync": (C.c_int, [vp, P(LoadOutcomeC)]),
     "tg_last_hits": (u32, [vp, P(TensorIdC), u32]),
     "tg_last_misses": (u32, [vp, P(TensorIdC), u32]),
     "tg_last_evictions": (u32, [vp, P(EvictionC), u32]),

@@ -274,6 +274,13 @@ void tg_rng_destroy(tg_rng* r) { delete r; }
 uint64_t tg_rng_uniform_below(tg_rng* r, uint64_t n) { return r->r.uniform_below(n); }
 
 // ---- pool ---------------------------------------------------------------------------
+// An asynchronous load (TG_LOAD_ASYNC) still in flight is finished before
+// any operation that mutates the pool or reads digests / suspect state
+// (a deferred failure is reported by tg_pool_sync).
+static void settle(const tg_pool* p) {
+    if (p && p->pool && p->pool->has_pending()) p->pool->complete_pending();
+}
+
 int tg_pool_create(const tg_gpu_spec* g, int32_t device, tg_pool** out) {
     return guard([&] {
         if (!g || !out) return TG_ERR_BAD_ARG;
@@ -297,6 +304,7 @@ int tg_pool_create(const tg_gpu_spec* g, int32_t device, tg_pool** out) {
 void tg_pool_destroy(tg_pool* p) { delete p; }
 
 int tg_pool_clone(const tg_pool* p, tg_pool** out) {
+    settle(p);
     return guard([&] {
         if (!p || !out) return TG_ERR_BAD_ARG;
         auto c = std::make_unique<tg_pool>();
@@ -308,6 +316,7 @@ int tg_pool_clone(const tg_pool* p, tg_pool** out) {
 }
 
 int tg_pool_assign(tg_pool* dst, const tg_pool* src) {
+    settle(dst);
     return guard([&] {
         if (!dst || !src) return TG_ERR_BAD_ARG;
         if (dst == src) return 0;
@@ -319,6 +328,7 @@ int tg_pool_assign(tg_pool* dst, const tg_pool* src) {
 }
 
 int tg_pool_tensors(const tg_pool* p, tg_tensor_entry* buf, uint64_t cap, uint64_t* n) {
+    settle(p);
     if (!p || !n) return TG_ERR_BAD_ARG;
     const auto& t = p->pool->store().tensors();
     *n = t.size();
@@ -340,7 +350,7 @@ int tg_pool_info_get(const tg_pool* p, tg_pool_info* o) {
                       s.merged_total(),    s.transferred_total(), s.evictions_total(),
                       s.map().region_count(), s.map().extent_count(), s.tensors().size(),
                       s.map().largest_free(), p->pool->device(),  p->pool->arena(),
-                      0, 0.0, 0, 0, 0, 0, 0, 0};
+                      0, 0.0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     const Pool::Totals& t = p->pool->totals();
     o->loads = t.loads;
     o->data_plane_ms = t.data_plane_ms;
@@ -350,6 +360,9 @@ int tg_pool_info_get(const tg_pool* p, tg_pool_info* o) {
     o->fingerprint_bytes = t.fingerprint_bytes;
     o->relocated_bytes = t.relocated_bytes;
     o->epoch = s.epoch();
+    o->verify_mismatches = t.verify_mismatches;
+    o->repaired_bytes = t.repaired_bytes;
+    o->failed_loads = t.failed_loads;
     return 0;
 }
 
@@ -362,6 +375,46 @@ int tg_pool_stream(const tg_pool* p, void** s) {
 int tg_set_model_alpha(tg_pool* p, const char* m, double a) {
     p->pool->store().set_alpha(m, a);
     return 0;
+}
+
+static void fill_outcome(const LoadReport& r, tg_load_outcome* out) {
+    const Plan& pl = r.decision.plan;
+    std::memset(out, 0, sizeof *out);
+    out->n_hits = static_cast<uint32_t>(r.decision.hits.size());
+    out->n_misses = static_cast<uint32_t>(r.decision.misses.size());
+    out->n_evictions = static_cast<uint32_t>(pl.evictions.size());
+    out->n_relocations = static_cast<uint32_t>(pl.relocations.size());
+    out->n_placements = static_cast<uint32_t>(pl.placements.size());
+    out->n_waves = r.waves;
+    out->fallback_evictions = pl.fallback_evictions;
+    out->bytes_transferred = r.decision.bytes_transferred;
+    out->bytes_merged = r.decision.misses.empty() ? 0 : pl.total_merge_cost;
+    out->eviction_cost_total = r.decision.misses.empty() ? 0.0 : pl.total_eviction_cost;
+    out->total_merge_cost = pl.total_merge_cost;
+    out->pgp_merge_cost = pl.pgp_merge_cost;
+    out->initial_merge_cost = pl.initial_merge_cost;
+    out->total_eviction_cost = pl.total_eviction_cost;
+    out->pcie_bytes = r.pcie_bytes;
+    out->peer_bytes = r.peer_bytes;
+    out->device_src_bytes = r.device_src_bytes;
+    out->fingerprint_bytes = r.fingerprint_bytes;
+    out->repaired_bytes = r.repaired_bytes;
+    out->verify_mismatches = r.verify_mismatches;
+    out->expected_mismatches = r.expected_mismatches;
+    out->plan_us = r.t.plan_us;
+    out->total_ms = r.t.total_ms;
+    out->relocate_ms = r.t.relocate_ms;
+    out->h2d_ms = r.t.h2d_ms;
+    out->peer_ms = r.t.peer_ms;
+    out->fp_kernel_ms = r.t.fp_kernel_ms;
+    out->fp_reuse_ms = r.t.fp_reuse_ms;
+    out->fp_reuse_max_ms = r.t.fp_reuse_max_ms;
+    out->host_issue_us = r.t.host_issue_us;
+    out->host_wait_us = r.t.host_wait_us;
+    out->host_total_us = r.t.host_total_us;
+    out->suspect_tensors = r.suspect_after;
+    out->kernel_end_ms = r.t.kernel_end_ms;
+    out->gated_h2d_start_ms = r.t.gated_h2d_start_ms;
 }
 
 int tg_load_model(tg_pool* p, const tg_model_spec* ms, const tg_stats* s, double clock, const tg_load_policy* pol,
@@ -386,46 +439,23 @@ int tg_load_model(tg_pool* p, const tg_model_spec* ms, const tg_stats* s, double
             g_detail = e.what();
             rc = e.code;
         }
-        if (out) {
-            const Plan& pl = r.decision.plan;
-            std::memset(out, 0, sizeof *out);
-            out->n_hits = static_cast<uint32_t>(r.decision.hits.size());
-            out->n_misses = static_cast<uint32_t>(r.decision.misses.size());
-            out->n_evictions = static_cast<uint32_t>(pl.evictions.size());
-            out->n_relocations = static_cast<uint32_t>(pl.relocations.size());
-            out->n_placements = static_cast<uint32_t>(pl.placements.size());
-            out->n_waves = r.waves;
-            out->fallback_evictions = pl.fallback_evictions;
-            out->bytes_transferred = r.decision.bytes_transferred;
-            out->bytes_merged = r.decision.misses.empty() ? 0 : pl.total_merge_cost;
-            out->eviction_cost_total = r.decision.misses.empty() ? 0.0 : pl.total_eviction_cost;
-            out->total_merge_cost = pl.total_merge_cost;
-            out->pgp_merge_cost = pl.pgp_merge_cost;
-            out->initial_merge_cost = pl.initial_merge_cost;
-            out->total_eviction_cost = pl.total_eviction_cost;
-            out->pcie_bytes = r.pcie_bytes;
-            out->peer_bytes = r.peer_bytes;
-            out->device_src_bytes = r.device_src_bytes;
-            out->fingerprint_bytes = r.fingerprint_bytes;
-            out->repaired_bytes = r.repaired_bytes;
-            out->verify_mismatches = r.verify_mismatches;
-            out->expected_mismatches = r.expected_mismatches;
-            out->plan_us = r.t.plan_us;
-            out->total_ms = r.t.total_ms;
-            out->relocate_ms = r.t.relocate_ms;
-            out->h2d_ms = r.t.h2d_ms;
-            out->peer_ms = r.t.peer_ms;
-            out->fp_kernel_ms = r.t.fp_kernel_ms;
-            out->fp_reuse_ms = r.t.fp_reuse_ms;
-            out->fp_reuse_max_ms = r.t.fp_reuse_max_ms;
-            out->host_issue_us = r.t.host_issue_us;
-            out->host_wait_us = r.t.host_wait_us;
-            out->host_total_us = r.t.host_total_us;
-            out->suspect_tensors = r.suspect_after;
-            out->kernel_end_ms = r.t.kernel_end_ms;
-            out->gated_h2d_start_ms = r.t.gated_h2d_start_ms;
-        }
+        if (out) fill_outcome(r, out);
         if (p->pool->has_device()) p->pool->publish_index();
+        return rc;
+    });
+}
+
+int tg_pool_sync(tg_pool* p, tg_load_outcome* out) {
+    return guard([&] {
+        if (!p) return TG_ERR_BAD_ARG;
+        const bool had = p->pool->has_pending();
+        const int rc = p->pool->complete_pending();
+        if (rc) g_detail = p->pool->last_completed_error();
+        if (had) p->last = p->pool->last_completed();  // tg_last_* now describe the completed load
+        if (out) {
+            if (had) fill_outcome(p->last, out);
+            else std::memset(out, 0, sizeof *out);
+        }
         return rc;
     });
 }
@@ -491,6 +521,7 @@ uint32_t tg_last_digests(const tg_pool* p, tg_digest* buf, uint32_t cap) {
 }
 
 int tg_end_instance(tg_pool* p, const char* m) {
+    settle(p);
     return guard([&] {
         p->pool->store().end_instance(m);
         p->pool->publish_index();
@@ -498,6 +529,7 @@ int tg_end_instance(tg_pool* p, const char* m) {
     });
 }
 int tg_evict_tensor(tg_pool* p, tg_tensor_id id) {
+    settle(p);
     return guard([&] {
         if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         const int rc = code_of(p->pool->store().evict_tensor(key_of(id)));
@@ -506,6 +538,7 @@ int tg_evict_tensor(tg_pool* p, tg_tensor_id id) {
     });
 }
 int tg_evict_model(tg_pool* p, const char* m) {
+    settle(p);
     return guard([&] {
         if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         p->pool->store().evict_model(m);
@@ -514,6 +547,7 @@ int tg_evict_model(tg_pool* p, const char* m) {
     });
 }
 int tg_move_tensor(tg_pool* p, tg_tensor_id id, uint64_t to) {
+    settle(p);
     return guard([&] {
         if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         const int rc = code_of(p->pool->move_tensor(key_of(id), to));
@@ -522,6 +556,7 @@ int tg_move_tensor(tg_pool* p, tg_tensor_id id, uint64_t to) {
     });
 }
 int tg_alloc_kv_region(tg_pool* p, uint64_t size, uint64_t block_id, uint64_t* off) {
+    settle(p);
     if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
     auto r = p->pool->store().alloc_kv_region(size, block_id);
     if (!r) return code_of(r.error());
@@ -529,6 +564,7 @@ int tg_alloc_kv_region(tg_pool* p, uint64_t size, uint64_t block_id, uint64_t* o
     return 0;
 }
 int tg_free_kv_region(tg_pool* p, uint64_t off) {
+    settle(p);
     if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
     return code_of(p->pool->store().free_kv_region(off));
 }
@@ -567,7 +603,10 @@ int tg_eviction_candidates(tg_pool* p, const tg_stats* s, const char* exclude, t
     return *n > cap && buf ? TG_ERR_BUFFER : 0;
 }
 
-int tg_validate(const tg_pool* p) { return code_of(p->pool->store().validate()); }
+int tg_validate(const tg_pool* p) {
+    settle(p);
+    return code_of(p->pool->store().validate());
+}
 
 int tg_dump(const tg_pool* p, char* buf, uint64_t cap, uint64_t* needed) {
     const std::string s = p->pool->store().dump_json();
@@ -587,6 +626,7 @@ int tg_regions(const tg_pool* p, tg_region* buf, uint64_t cap, uint64_t* n) {
 }
 
 int tg_tensor_info_get(const tg_pool* p, tg_tensor_id id, tg_tensor_info* o) {
+    settle(p);
     const auto& t = p->pool->store().tensors();
     auto it = t.find(key_of(id));
     if (it == t.end()) return code_of(Err::NotFound);
@@ -607,6 +647,7 @@ int tg_pool_index_image(const tg_pool* p, tg_index_slot* buf, uint64_t cap_slots
     });
 }
 int tg_pool_device_index(tg_pool* p, const tg_index_slot** table, uint64_t* capacity) {
+    settle(p);
     return guard([&] {
         if (!p || !table || !capacity) return TG_ERR_BAD_ARG;
         if (!p->pool->has_device()) return TG_ERR_NO_DEVICE;
@@ -616,6 +657,7 @@ int tg_pool_device_index(tg_pool* p, const tg_index_slot** table, uint64_t* capa
     });
 }
 int tg_index_lookup(tg_pool* p, const tg_tensor_id* ids, uint32_t n, tg_index_hit* out) {
+    settle(p);
     return guard([&] {
         if (!p || (n && (!ids || !out))) return TG_ERR_BAD_ARG;
         if (!p->pool->has_device()) return TG_ERR_NO_DEVICE;
@@ -631,6 +673,7 @@ int tg_index_lookup(tg_pool* p, const tg_tensor_id* ids, uint32_t n, tg_index_hi
 }
 
 int tg_fingerprint_tensor(tg_pool* p, tg_tensor_id id, tg_digest* out) {
+    settle(p);
     return guard([&] {
         if (!p->pool->store().tensors().count(key_of(id))) return code_of(Err::NotFound);
         const Digest d = p->pool->fingerprint_resident(key_of(id));
@@ -640,6 +683,7 @@ int tg_fingerprint_tensor(tg_pool* p, tg_tensor_id id, tg_digest* out) {
 }
 
 int tg_pool_add_peer(tg_pool* p, tg_pool* peer) {
+    settle(p);
     return guard([&] {
         if (!p || !peer || p == peer) return TG_ERR_BAD_ARG;
         p->pool->add_peer(peer->pool.get());
@@ -656,6 +700,7 @@ static std::vector<RemoteEntry> entries_of(const tg_index_entry* idx, uint64_t n
 }
 
 int tg_pool_export_ipc(const tg_pool* p, void* handle) {
+    settle(p);
     return guard([&] {
         static_assert(sizeof(cudaIpcMemHandle_t) == TG_IPC_HANDLE_BYTES, "IPC handle size");
         cudaIpcMemHandle_t h;
@@ -666,6 +711,7 @@ int tg_pool_export_ipc(const tg_pool* p, void* handle) {
 }
 
 int tg_pool_index(const tg_pool* p, tg_index_entry* buf, uint64_t cap, uint64_t* n) {
+    settle(p);
     const auto idx = p->pool->index();
     *n = idx.size();
     for (uint64_t i = 0; buf && i < idx.size() && i < cap; ++i)
@@ -674,6 +720,7 @@ int tg_pool_index(const tg_pool* p, tg_index_entry* buf, uint64_t cap, uint64_t*
 }
 
 int tg_pool_attach_remote(tg_pool* p, const void* handle, const tg_index_entry* idx, uint64_t n, int32_t* peer_id) {
+    settle(p);
     return guard([&] {
         cudaIpcMemHandle_t h;
         std::memcpy(&h, handle, sizeof h);
@@ -684,6 +731,7 @@ int tg_pool_attach_remote(tg_pool* p, const void* handle, const tg_index_entry* 
 }
 
 int tg_pool_update_remote(tg_pool* p, int32_t peer_id, const tg_index_entry* idx, uint64_t n) {
+    settle(p);
     return guard([&] {
         p->pool->update_remote(peer_id, entries_of(idx, n));
         return 0;
@@ -691,6 +739,7 @@ int tg_pool_update_remote(tg_pool* p, int32_t peer_id, const tg_index_entry* idx
 }
 
 int tg_pool_snapshot(tg_pool* p, tg_snapshot** out) {
+    settle(p);
     return guard([&] {
         if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         *out = new tg_snapshot{p->pool->snapshot()};
@@ -698,6 +747,7 @@ int tg_pool_snapshot(tg_pool* p, tg_snapshot** out) {
     });
 }
 int tg_pool_restore(tg_pool* p, const tg_snapshot* s) {
+    settle(p);
     return guard([&] {
         if (p->pool->store().kv_armed()) return TG_ERR_KV_ARMED;
         p->pool->restore(s->s);
@@ -720,7 +770,10 @@ int tg_host_register(tg_tensor_id id, const void* ptr, uint64_t size, const tg_d
     s.has_expected = expected != nullptr;
     if (expected) s.expected = Digest{expected->hi, expected->lo};
     cudaPointerAttributes a{};
-    if (ptr && cudaPointerGetAttributes(&a, ptr) == cudaSuccess) s.on_device = a.type == cudaMemoryTypeDevice;
+    if (ptr && cudaPointerGetAttributes(&a, ptr) == cudaSuccess && a.type == cudaMemoryTypeDevice) {
+        s.on_device = true;
+        s.device = a.device;
+    }
     cudaGetLastError();
     SourceRegistry::get().put(key_of(id), s);
     return 0;
@@ -872,6 +925,7 @@ int tg_kv_clone(const tg_kv* kv, tg_kv** out) {
 
 int tg_kv_ensure_capacity(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t rid, uint64_t tokens, uint64_t* granted,
                           uint64_t cap, uint64_t* n_granted) {
+    settle(p);
     return guard([&] {
         if (int rc = bind_kv(kv, p)) return rc;
         std::vector<u64> g;
@@ -888,6 +942,7 @@ int tg_kv_ensure_capacity(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t rid
 
 int tg_kv_batch_allocate(tg_kv* kv, tg_pool* p, const tg_stats* s, const uint64_t* rids, const uint64_t* tokens,
                          uint64_t n, uint64_t* counts, uint64_t* pbns, uint64_t cap, uint64_t* total) {
+    settle(p);
     return guard([&] {
         if (int rc = bind_kv(kv, p)) return rc;
         std::vector<std::pair<u64, u64>> reqs(n);
@@ -913,6 +968,7 @@ int tg_kv_release_request(tg_kv* kv, uint64_t rid) {
     return guard([&] { return code_of(kv->a->release_request(rid)); });
 }
 int tg_kv_teardown(tg_kv* kv, tg_pool* p) {
+    settle(p);
     return guard([&] {
         if (int rc = bind_kv(kv, p)) return rc;
         kv->a->teardown(p->pool->store());
@@ -920,6 +976,7 @@ int tg_kv_teardown(tg_kv* kv, tg_pool* p) {
     });
 }
 int tg_kv_urgent_reclaim(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t blocks) {
+    settle(p);
     return guard([&] {
         if (int rc = bind_kv(kv, p)) return rc;
         const int rc = code_of(kv->a->urgent_reclaim(p->pool->store(), s->s_view(), blocks));
@@ -1007,6 +1064,7 @@ int tg_kv_wait_tables(tg_kv* kv, void* stream) {
 }
 int tg_kv_reserve(tg_kv* kv, tg_pool* p, uint32_t max_requests, uint64_t max_blocks_per_request,
                   uint64_t max_blocks) {
+    settle(p);
     return guard([&] {
         if (!kv || !p) return TG_ERR_BAD_ARG;
         if (int rc = bind_kv(kv, p)) return rc;
@@ -1017,10 +1075,12 @@ int tg_kv_reserve(tg_kv* kv, tg_pool* p, uint32_t max_requests, uint64_t max_blo
 }
 int tg_kv_write_tokens(tg_kv* kv, tg_pool* p, const uint64_t* slots, const uint64_t* pos, const void* buf, uint32_t n,
                        void* stream) {
+    settle(p);
     return kv_tokens(kv, p, slots, pos, const_cast<void*>(buf), n, stream, true);
 }
 int tg_kv_read_tokens(tg_kv* kv, tg_pool* p, const uint64_t* slots, const uint64_t* pos, void* buf, uint32_t n,
                       void* stream) {
+    settle(p);
     return kv_tokens(kv, p, slots, pos, buf, n, stream, false);
 }
 
@@ -1032,6 +1092,7 @@ int tg_kv_request_slot(const tg_kv* kv, uint64_t rid, uint32_t* slot) {
 }
 int tg_kv_device_arm(tg_kv* kv, tg_pool* p, uint64_t max_blocks_per_request, uint32_t max_requests,
                      uint32_t max_batches) {
+    settle(p);
     return guard([&] {
         if (max_requests > kKvDevMaxRequests) {
             g_detail = "max_requests above the per-batch limit";
@@ -1052,6 +1113,7 @@ int tg_kv_batch_allocate_device(tg_kv* kv, const uint64_t* d_slots, const uint64
     });
 }
 int tg_kv_device_sync(tg_kv* kv, tg_pool* p, const tg_stats* s, uint64_t* applied, uint64_t* replayed) {
+    settle(p);
     return guard([&] {
         if (!kv->a->armed()) return TG_ERR_BAD_ARG;
         KvAllocator::SyncReport r;

@@ -221,7 +221,17 @@ Pool::Pool(GpuDesc gpu, int device) : store_(std::move(gpu)), device_(device) {
 Pool::~Pool() {
     if (device_ < 0) return;
     DeviceScope ds(device_);
+    try {
+        complete_pending();
+    } catch (...) {
+    }
     cudaDeviceSynchronize();
+    for (Pool* p : peers_) {
+        p->peer_of_.erase(std::remove(p->peer_of_.begin(), p->peer_of_.end(), this), p->peer_of_.end());
+        p->reader_events_.erase(this);
+    }
+    for (Pool* q : peer_of_) q->peers_.erase(std::remove(q->peers_.begin(), q->peers_.end(), this), q->peers_.end());
+    if (ev_reader_) cudaEventDestroy(ev_reader_);
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
     for (cudaStream_t s : {s_main_, s_copy_, s_fp_, s_peer_, s_verify_})
         if (s) cudaStreamDestroy(s);
@@ -354,9 +364,11 @@ void Pool::sync_all_streams() noexcept {
 // registered source: no unverified bytes are ever reused.
 St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, const LoadOptions& opt, u32 flags,
                     LoadReport* rep) {
+    complete_pending();  // a deferred failure stays reported by tg_pool_sync; its tensors are suspect
     try {
         return load_model_impl(m, stats, clock, opt, flags, rep);
     } catch (...) {
+        ++totals_.failed_loads;
         if (rep->committed && has_device()) {
             sync_all_streams();  // nothing of this load may still be writing when we return
             rep->suspect_after = 0;
@@ -376,6 +388,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     if (has_device()) {
         ds = std::make_unique<DeviceScope>(device_);
         ensure_events(9);
+        wait_readers();
         TG_CUDA(cudaEventRecord(ev(0), s_main_));  // t0: entry
     }
     const auto h0 = clk::now();
@@ -402,6 +415,15 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     std::vector<Digest> truth(np);
     std::vector<char> has_truth(np, 0);
     rep->placement_src.assign(np, 0);
+    if (has_device() && (flags & kLoadPeer) && np) {
+        // A peer whose asynchronous load is still placing tensors we miss
+        // lands first: its digests are the truth our pulls are checked
+        // against.  Peers busy with unrelated models keep running.
+        std::vector<Key> want;
+        for (const Place& pl : d.plan.placements) want.push_back(d.miss_desc[pl.tensor].id);
+        for (Pool* p : peers_)
+            if (p->pending_shares(want)) p->complete_pending();
+    }
     if (has_device()) {
         for (std::size_t i = 0; i < np; ++i) {
             const TensorDesc& t = d.miss_desc[d.plan.placements[i].tensor];
@@ -442,6 +464,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
                 has_truth[i] = 1;
             }
             if (src[i].on_device) {  // HBM-resident model cache: SM copy, not the PCIe engine
+                if (src[i].device >= 0 && src[i].device != device_) enable_peer_access(src[i].device);
                 peer_src[i] = static_cast<const std::uint8_t*>(src[i].ptr);
                 rep->placement_src[i] = 2;
             }
@@ -885,8 +908,28 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     }
     TG_CUDA(cudaEventRecord(ev(3), s_main_));
     auto* h_dig = reinterpret_cast<u64*>(h + desc_bytes + sums_bytes + sync_bytes);
+    // Peers this load reads from must not overwrite those bytes before the
+    // reads are done: each records our end-of-load event and waits on it
+    // before its own next data plane (cross-device stream wait, no host sync).
+    for (std::size_t i = 0; i < np; ++i)
+        if (!peers_.empty() && (rep->placement_src[i] == 1 || rep->placement_src[i] == 3)) {
+            note_readers();
+            break;
+        }
     const auto h_issued = clk::now();
     rep->t.host_issue_us = std::chrono::duration<double, std::micro>(h_issued - h0).count();
+
+    // ---- completion: wait for the data plane, then record / verify digests.
+    // Runs now, or — with kLoadAsync — before the next operation on this pool
+    // (complete_pending), so loads on different pools overlap.
+    auto finish = [this, h_dig, np, nf, fused, hit_base, n_still, fp_reuse, waves, nc, gate_recorded, ev_gate, ev_fp,
+                   fp_i, fp_reuse_slot, fp_reuse_launches, h0, h_issued, fp_of_placement = std::move(fp_of_placement),
+                   ctask_of_placement = std::move(ctask_of_placement), has_truth = std::move(has_truth),
+                   truth = std::move(truth), hit_keys = std::move(hit_keys), hit_pos = std::move(hit_pos),
+                   hit_rel = std::move(hit_rel), ctask_of_still = std::move(ctask_of_still),
+                   ctask_of_reloc = std::move(ctask_of_reloc), rel = std::move(rel),
+                   prior_suspect = std::move(prior_suspect)](LoadReport* rep, const ModelDesc& m) -> int {
+    LoadDecision& D = rep->decision;
     {
         NvtxRange r("tg.wait_data_plane");
         TG_CUDA(cudaStreamSynchronize(s_main_));
@@ -1028,7 +1071,19 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     totals_.device_src_bytes += rep->device_src_bytes;
     totals_.fingerprint_bytes += rep->fingerprint_bytes;
     totals_.relocated_bytes += D.plan.total_merge_cost;
+    totals_.verify_mismatches += rep->verify_mismatches;
+    totals_.repaired_bytes += rep->repaired_bytes;
     if (fail) throw DeviceError(fail, fail_what);
+    return 0;
+    };
+    if (flags & kLoadAsync) {
+        pending_ = std::make_unique<PendingLoad>();
+        pending_->report = *rep;  // the caller keeps the decision; digests / timings land here
+        pending_->model = m;
+        pending_->finish = std::move(finish);
+        return ok();
+    }
+    finish(rep, m);
     return ok();
 }
 
@@ -1107,6 +1162,7 @@ void Pool::fetch(const HostSource& hs, std::uint8_t* dst, u64 size, cudaStream_t
 }
 
 St Pool::move_tensor(const Key& k, u64 to) {
+    complete_pending();
     const Entry* e = store_.entry(k);
     const u64 from = e ? e->off : 0, size = e ? e->size : 0;
     St st = store_.move_tensor(k, to);
@@ -1115,6 +1171,7 @@ St Pool::move_tensor(const Key& k, u64 to) {
     Entry* moved = store_.entry(k);
     const bool prior = moved->suspect;
     moved->suspect = true;  // until the bytes have moved (a failure leaves it suspect)
+    wait_readers();
     MoveDesc md{reinterpret_cast<u64>(arena_ + from), reinterpret_cast<u64>(arena_ + to), size};
     relocate_launch(&md, 1, sm_count_, s_main_);
     TG_CUDA(cudaGetLastError());
@@ -1132,20 +1189,88 @@ Digest Pool::fingerprint_resident(const Key& k) {
     return d;
 }
 
-void Pool::add_peer(Pool* p) {
-    if (!has_device() || !p->has_device()) throw DeviceError(kErrNoDevice, "peer pools need devices");
-    if (p->device_ != device_) {
-        DeviceScope ds(device_);
-        int can = 0;
-        TG_CUDA(cudaDeviceCanAccessPeer(&can, device_, p->device_));
-        if (!can) throw DeviceError(kErrCuda, "no P2P path between devices");
-        cudaError_t e = cudaDeviceEnablePeerAccess(p->device_, 0);
-        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_check(e, "cudaDeviceEnablePeerAccess");
-        cudaGetLastError();
-    }
-    peers_.push_back(p);
+// Let this pool's kernels read (and write) HBM of device `other` over NVLink.
+void Pool::enable_peer_access(int other) {
+    if (other == device_ || std::find(peer_devices_.begin(), peer_devices_.end(), other) != peer_devices_.end())
+        return;
+    DeviceScope ds(device_);
+    int can = 0;
+    TG_CUDA(cudaDeviceCanAccessPeer(&can, device_, other));
+    if (!can) throw DeviceError(kErrCuda, "no P2P path between devices");
+    cudaError_t e = cudaDeviceEnablePeerAccess(other, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_check(e, "cudaDeviceEnablePeerAccess");
+    cudaGetLastError();
+    peer_devices_.push_back(other);
 }
 
+void Pool::add_peer(Pool* p) {
+    if (!has_device() || !p->has_device()) throw DeviceError(kErrNoDevice, "peer pools need devices");
+    enable_peer_access(p->device_);
+    peers_.push_back(p);
+    p->peer_of_.push_back(this);
+}
+
+// This load read peer arenas: record the end of its data plane for them.
+void Pool::note_readers() {
+    if (!ev_reader_) TG_CUDA(cudaEventCreateWithFlags(&ev_reader_, cudaEventDisableTiming));
+    TG_CUDA(cudaEventRecord(ev_reader_, s_main_));
+    for (Pool* p : peers_) p->reader_events_[this] = ev_reader_;
+}
+
+// Before this pool's data plane writes its arena: wait (on the device) for
+// every peer that read from it.
+void Pool::wait_readers() {
+    for (const auto& [q, e] : reader_events_) TG_CUDA(cudaStreamWaitEvent(s_main_, e));
+}
+
+int Pool::complete_pending() {
+    if (!pending_) return 0;
+    std::unique_ptr<PendingLoad> p = std::move(pending_);
+    DeviceScope ds(device_);
+    int rc = 0;
+    last_async_err_.clear();
+    try {
+        p->finish(&p->report, p->model);
+    } catch (const DeviceError& e) {
+        rc = e.code;
+        last_async_err_ = e.what();
+    } catch (const std::exception& e) {
+        rc = kErrCuda;
+        last_async_err_ = e.what();
+    }
+    if (rc) {
+        ++totals_.failed_loads;
+        sync_all_streams();
+        p->report.suspect_after = 0;
+        for (const auto& t : p->model.tensors)
+            if (const Entry* e = store_.entry(t.id); e && e->suspect) ++p->report.suspect_after;
+    }
+    last_async_ = std::move(p->report);
+    last_async_rc_ = rc;
+    return rc;
+}
+
+// Does this pool's in-flight asynchronous load place any of `keys`, or a
+// shard sibling of one (same lineage parent)?
+bool Pool::pending_shares(const std::vector<Key>& keys) const {
+    if (!pending_) return false;
+    std::unordered_map<Key, bool, KeyHash> mine, parents;
+    for (const auto& t : pending_->model.tensors) {
+        mine[t.id] = true;
+        ShardOf s;
+        if (ShardLineage::get().find(t.id, &s)) parents[s.parent] = true;
+    }
+    for (const Key& k : keys) {
+        if (mine.count(k)) return true;
+        ShardOf s;
+        if (!parents.empty() && ShardLineage::get().find(k, &s) && parents.count(s.parent)) return true;
+    }
+    return false;
+}
+
+// S'_peer: bytes of m missing here but resident on a peer — verified there,
+// or being placed by the peer's in-flight asynchronous load (which a load of
+// ours lands before pulling, see load_model_impl).
 u64 Pool::peer_reuse_size(const ModelDesc& m) const {
     u64 s = 0;
     for (const auto& t : m.tensors) {
@@ -1153,7 +1278,8 @@ u64 Pool::peer_reuse_size(const ModelDesc& m) const {
         bool found = false;
         for (Pool* p : peers_)
             if (const auto it = p->store_.tensors().find(t.id);
-                it != p->store_.tensors().end() && it->second.has_digest && !it->second.suspect) {
+                it != p->store_.tensors().end() &&
+                ((it->second.has_digest && !it->second.suspect) || p->pending_shares({t.id}))) {
                 found = true;
                 break;
             }

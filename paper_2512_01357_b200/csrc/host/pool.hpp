@@ -11,6 +11,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -35,6 +36,7 @@ struct HostSource {
     bool has_expected = false;
     Digest expected;
     bool on_device = false;  // HBM-resident source: placed by the K3 copy kernel
+    int device = -1;         // ... on this device (another pool's device reads it over NVLink)
     // Model Store source (model.hpp:24 ModelLocation::ModelStore): bytes live
     // in a checkpoint file and stream file → pinned ring → HBM
     std::string path;
@@ -129,6 +131,11 @@ constexpr u32 kLoadPeer = 4u;            // pull misses from peer pools that hol
 // 9.4 ms for the separate K3 waves + K1 passes, which remain available by
 // leaving this flag out).
 constexpr u32 kLoadFused = 8u;
+// Return once the decision is committed and the data plane is enqueued; the
+// wait and the digest bookkeeping run before the next operation on the pool
+// (Pool::complete_pending), so loads on different pools — different GPUs —
+// overlap while the caller carries on (trace replay, §8(f) row 1).
+constexpr u32 kLoadAsync = 16u;
 constexpr u32 kLoadDefault = kLoadVerifyReuse | kLoadFingerprintNew | kLoadFused;
 // tg_load_policy.flags with this bit are taken literally (0 | explicit = no
 // optional work); without it, 0 means kLoadDefault.
@@ -166,6 +173,13 @@ struct LoadReport {
     u32 suspect_after = 0;           // tensors of this load left suspect (0 on success)
 };
 
+// A load whose data plane is still running (kLoadAsync).
+struct PendingLoad {
+    LoadReport report;
+    ModelDesc model;
+    std::function<int(LoadReport*, const ModelDesc&)> finish;
+};
+
 class Pool {
 public:
     // device < 0: control plane only (no arena; moves no bytes).
@@ -186,12 +200,23 @@ public:
         u64 loads = 0;
         double data_plane_ms = 0;
         u64 pcie_bytes = 0, peer_bytes = 0, device_src_bytes = 0, fingerprint_bytes = 0, relocated_bytes = 0;
+        u64 verify_mismatches = 0, repaired_bytes = 0, failed_loads = 0;
     };
     const Totals& totals() const { return totals_; }
 
     St load_model(const ModelDesc& m, const StatsView& stats, double clock, const LoadOptions& opt, u32 flags,
                   LoadReport* rep);
     St move_tensor(const Key& k, u64 to);  // metadata + bytes
+    // Finish an asynchronous load (kLoadAsync): wait for its data plane, then
+    // record / verify its digests.  Returns 0 or the runtime error the load
+    // ended with (its tensors are then suspect, as after a failed synchronous
+    // load).  Every mutating operation calls it first.
+    int complete_pending();
+    bool has_pending() const { return pending_ != nullptr; }
+    bool pending_shares(const std::vector<Key>& keys) const;
+    const LoadReport& last_completed() const { return last_async_; }
+    int last_completed_rc() const { return last_async_rc_; }
+    const std::string& last_completed_error() const { return last_async_err_; }
 
     Digest fingerprint_resident(const Key& k);  // K1 over the resident bytes
     void add_peer(Pool* p);
@@ -245,6 +270,20 @@ private:
     std::vector<cudaEvent_t> events_;
     bool assemble_shard(const TensorDesc& t, std::vector<MoveDesc>* pieces, const Plan* plan, u64* local_bytes) const;
     std::vector<Pool*> peers_;
+    std::vector<Pool*> peer_of_;  // pools that have this one as a peer
+    std::vector<int> peer_devices_;  // devices whose HBM this pool's kernels may access
+    void enable_peer_access(int other);
+    // Events of in-process pools that read this arena (peer pulls), recorded
+    // after their loads; this pool's next data plane waits on them, so bytes
+    // a peer is still reading are never overwritten.
+    std::unordered_map<const Pool*, cudaEvent_t> reader_events_;
+    cudaEvent_t ev_reader_ = nullptr;
+    void note_readers();
+    void wait_readers();
+    std::unique_ptr<PendingLoad> pending_;
+    LoadReport last_async_;
+    int last_async_rc_ = 0;
+    std::string last_async_err_;
     struct RemotePeer {
         std::uint8_t* base = nullptr;  // IPC-mapped peer arena
         std::unordered_map<Key, RemoteEntry, KeyHash> index;

@@ -273,7 +273,7 @@ class PackingStrictness(enum.IntEnum):
     LiteralGuard = 1
 
 
-LOAD_VERIFY_REUSE, LOAD_FINGERPRINT_NEW, LOAD_PEER, LOAD_FUSED = 1, 2, 4, 8
+LOAD_VERIFY_REUSE, LOAD_FINGERPRINT_NEW, LOAD_PEER, LOAD_FUSED, LOAD_ASYNC = 1, 2, 4, 8, 16
 LOAD_EXPLICIT = 0x80000000  # flags taken literally (LOAD_EXPLICIT alone: no optional work)
 
 
@@ -432,6 +432,18 @@ class ReuseStore:
         if rc:
             return Result(error=Error(rc - 1))
         return Result(self._outcome(out, details))
+
+    def sync(self, details=False):
+        """Finish an asynchronous load (LoadPolicy(flags=... | LOAD_ASYNC)) still
+        in flight: its completed outcome (digests verified, timings), or None
+        when none was pending.  Raises TangramRuntimeError if it failed."""
+        out = N.LoadOutcomeC()
+        rc = lib.tg_pool_sync(self._h, C.byref(out))
+        if rc >= 100:
+            raise N.TangramRuntimeError(rc, "tg_pool_sync", None)
+        if out.n_hits + out.n_misses == 0:
+            return None
+        return self._outcome(out, details)
 
     def _outcome(self, o, details):
         h = self._h

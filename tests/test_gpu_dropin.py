@@ -15,8 +15,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "integration", "_build")
 
 
-@pytest.mark.parametrize("mode", ["reuse_odkv", "reuse", "baseline"])
-def test_c5_replay_moves_bytes_and_matches_reference(mode):
+@pytest.mark.parametrize("mode,async_loads", [("reuse_odkv", "0"), ("reuse_odkv", "1"), ("reuse", "1"),
+                                              ("baseline", "0")])
+def test_c5_replay_moves_bytes_and_matches_reference(mode, async_loads):
     """reuse_odkv is C5 (on-demand KV through KvEngine); reuse and baseline
     take the simulator's reserve_kv pre-reservation path (simulator.hpp:606-637:
     eviction_candidates, evict_tensor, alloc_kv_region, free runs) against the
@@ -26,14 +27,54 @@ def test_c5_replay_moves_bytes_and_matches_reference(mode):
         pytest.skip("drop-in binaries not built (make -C integration)")
     args = [mode, "8", "48", "4", "2", "2000", "42", "0", "0", "L3"]
     a = subprocess.run([ref_bin] + args, capture_output=True, check=True, timeout=600)
-    env = dict(os.environ, TANGRAM_DEVICE="auto", TANGRAM_SYNTH_SOURCES="1")
+    env = dict(os.environ, TANGRAM_DEVICE="auto", TANGRAM_SYNTH_SOURCES="1", TANGRAM_ASYNC_LOADS=async_loads)
     b = subprocess.run([tg_bin] + args, capture_output=True, check=True, timeout=600, env=env)
     assert a.stdout == b.stdout
     pools = json.loads(b.stderr.decode().strip().splitlines()[-1])["pools"]
     g0 = [p for p in pools if p["gpu_id"] == "gpu0"][0]
     assert g0["device"] == 0 and g0["loads"] > 0
     assert g0["device_src_bytes"] > 0 and g0["fingerprint_bytes"] > 0
+    assert g0["verify_mismatches"] == 0 and g0["failed_loads"] == 0
     print(json.dumps(g0))
+
+
+SMALL = ["opt1.3B", "qwen3B", "llama3B", "opt6.7B", "llama8B", "yi9B"]
+
+
+def _small_replay(extra_env, args):
+    tg_bin = os.path.join(BUILD, "sim_tangram")
+    env = dict(os.environ, TANGRAM_DEVICE="0", TANGRAM_SYNTH_SOURCES="host", **extra_env)
+    b = subprocess.run([tg_bin] + args, capture_output=True, check=True, timeout=900, env=env)
+    rep = json.loads(b.stderr.decode().strip().splitlines()[-1])
+    return b.stdout, rep
+
+
+def test_c5_small_all_pools_real_async_and_peer_schedule():
+    """A C5-shaped replay whose every pool holds real bytes on this one GPU
+    (4 pools x 24 GiB, the six smallest catalog models — 62 GB, so models
+    migrate between pools — sources in pinned host memory): synchronous and asynchronous loads give the reference's
+    RunMetrics byte for byte; with the peer-aware schedule
+    (TANGRAM_PEER_SCHEDULE) misses resident on another pool come from it
+    instead of over PCIe — PCIe bytes saved, nothing fails verification."""
+    ref_bin, tg_bin = os.path.join(BUILD, "sim_reference"), os.path.join(BUILD, "sim_tangram")
+    if not (os.path.exists(ref_bin) and os.path.exists(tg_bin)):
+        pytest.skip("drop-in binaries not built (make -C integration)")
+    args = ["reuse_odkv", "4", "24", "4", "2", "400", "42", "0", "0", "L3", ",".join(SMALL)]
+    a = subprocess.run([ref_bin] + args, capture_output=True, check=True, timeout=600)
+    out_sync, r_sync = _small_replay({"TANGRAM_ASYNC_LOADS": "0"}, args)
+    out_async, r_async = _small_replay({"TANGRAM_ASYNC_LOADS": "1"}, args)
+    assert out_sync == a.stdout and out_async == a.stdout
+    out_peer, r_peer = _small_replay({"TANGRAM_ASYNC_LOADS": "1", "TANGRAM_PEER_SCHEDULE": "700"}, args)
+    for r in (r_sync, r_async, r_peer):
+        assert all(p["device"] == 0 for p in r["pools"]) and len(r["pools"]) == 4
+        assert sum(p["verify_mismatches"] + p["failed_loads"] for p in r["pools"]) == 0
+    pcie = {k: sum(p["pcie_bytes"] for p in r["pools"]) for k, r in (("sync", r_sync), ("peer", r_peer))}
+    peer = sum(p["peer_bytes"] for p in r_peer["pools"])
+    assert sum(p["peer_bytes"] for p in r_sync["pools"]) == 0
+    assert peer > 0  # misses pulled from another pool
+    assert pcie["peer"] < pcie["sync"]  # ... instead of over PCIe
+    print(json.dumps({"replay_s": {"sync": r_sync["replay_s"], "async": r_async["replay_s"],
+                                   "peer": r_peer["replay_s"]}, "pcie_bytes": pcie, "peer_bytes": peer}))
 
 
 def test_store_copy_semantics_on_a_device_pool():
