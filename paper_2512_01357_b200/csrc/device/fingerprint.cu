@@ -672,10 +672,17 @@ __device__ __forceinline__ void digest_of(u64 sum_h, u64 sum_l, u64 n, u64* out)
 // sees them all).  No shared memory and no CTA barrier: a static __shared__
 // flag here shifts the dynamic stage ring and cost K1 8-12 % (A/B on one
 // box, 8 GiB: 5.6-5.9 vs 6.4-6.8 TB/s).
+__device__ __forceinline__ u64 globaltimer_ns() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 template <class Task>
 __device__ __forceinline__ void finalize_if_last(const Task* __restrict__ tasks, u32 n_tasks,
                                                  const u64* __restrict__ sums, u64* __restrict__ digests,
-                                                 unsigned long long* __restrict__ done) {
+                                                 unsigned long long* __restrict__ done, u64* __restrict__ stamps,
+                                                 u64* clean_sums, unsigned long long* clean_sync) {
     const u32 lane = threadIdx.x & 31;
     __threadfence();
     __syncwarp();
@@ -686,15 +693,28 @@ __device__ __forceinline__ void finalize_if_last(const Task* __restrict__ tasks,
     __threadfence();
     for (u32 i = lane; i < n_tasks; i += 32)
         digest_of(__ldcg(sums + 2 * i), __ldcg(sums + 2 * i + 1), tasks[i].n, digests + 2 * i);
+    if (clean_sums) {  // every other warp is done with them: leave the stage zeroed for the next launch
+        __syncwarp();      // (every lane has read its tasks' sums)
+        for (u32 i = lane; i < 2 * n_tasks; i += 32) clean_sums[i] = 0;
+        for (u32 i = lane; clean_sync + i <= done; i += 32) clean_sync[i] = 0;
+    }
+    if (stamps) {  // the launch's end, after the digests (the host may poll it)
+        __threadfence_system();
+        if (lane == 0) *reinterpret_cast<volatile u64*>(stamps + 1) = globaltimer_ns();
+    }
 }
 
 template <class Task, class Cfg>
 __global__ void __launch_bounds__(Cfg::kWarps * 32, 2)
     copy_fp_kernel(const Task* __restrict__ tasks, u32 n_tasks, u64 total_tiles, u64* __restrict__ sums,
                    unsigned long long* __restrict__ sync, const u64* __restrict__ need, bool verify_next,
-                   u64* __restrict__ digests, unsigned long long* __restrict__ done) {
+                   u64* __restrict__ digests, unsigned long long* __restrict__ done, u64* __restrict__ stamps,
+                   bool clean) {
+    // stamps (nullable, host-mapped): globaltimer at the first CTA's start and
+    // at the finalizer's end — the kernel's span without an event query
+    if (stamps && blockIdx.x == 0 && threadIdx.x == 0) stamps[0] = globaltimer_ns();
     load_tiles<Task, Cfg>(tasks, n_tasks, total_tiles, sums, sync, need, verify_next);
-    finalize_if_last(tasks, n_tasks, sums, digests, done);
+    finalize_if_last(tasks, n_tasks, sums, digests, done, stamps, clean ? sums : nullptr, clean ? sync : nullptr);
 }
 
 __global__ void copy_fp_finalize_kernel(const CopyFpTask* __restrict__ tasks, u32 n_tasks,
@@ -750,7 +770,7 @@ void set_tile_order_once() {
 template <class Task, class Cfg>
 void load_kernel_launch_cfg(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests,
                             u64* d_sync, const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s,
-                            bool sync_zeroed) {
+                            bool sync_zeroed, u64* stamps, bool clean) {
     static const bool attr = [] {
         return cudaFuncSetAttribute(copy_fp_kernel<Task, Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     Cfg::kSmemBytes) == cudaSuccess;
@@ -763,32 +783,33 @@ void load_kernel_launch_cfg(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u
     const unsigned blocks = static_cast<unsigned>(want < cap ? want : cap);
     auto* sync = reinterpret_cast<unsigned long long*>(d_sync);
     copy_fp_kernel<Task, Cfg><<<blocks, Cfg::kWarps * 32, Cfg::kSmemBytes, s>>>(
-        d_tasks, n_tasks, total_tiles, d_sums, sync, d_need, verify_next(), d_digests, sync + 1 + n_waves);
+        d_tasks, n_tasks, total_tiles, d_sums, sync, d_need, verify_next(), d_digests, sync + 1 + n_waves, stamps, clean);
     g_kernel_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 template <class Task>
 void load_kernel_launch(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, u64* d_sync,
                         const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed,
-                        bool writes) {
+                        bool writes, u64* stamps = nullptr, bool clean = false) {
     if (!writes && !(std::getenv("TANGRAM_FP_NEXT") && std::strcmp(std::getenv("TANGRAM_FP_NEXT"), "0") == 0))
         load_kernel_launch_cfg<Task, CfgFpNext>(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, d_need, n_waves,
-                                                sm_count, s, sync_zeroed);
+                                                sm_count, s, sync_zeroed, stamps, clean);
     else if (writes && pair_ring())
         load_kernel_launch_cfg<Task, CfgPair>(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, d_need, n_waves,
-                                              sm_count, s, sync_zeroed);
+                                              sm_count, s, sync_zeroed, stamps, clean);
     else
         load_kernel_launch_cfg<Task, CfgSingle>(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, d_need, n_waves,
-                                                sm_count, s, sync_zeroed);
+                                                sm_count, s, sync_zeroed, stamps, clean);
 }
 }  // namespace
 
 void copy_fp_launch(const CopyFpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, u64* d_sync,
-                    const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed) {
+                    const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed, u64* stamps,
+                    bool clean) {
     if (n_tasks == 0) return;
     if (total_tiles > 0) {
         load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, d_need, n_waves, sm_count, s,
-                           sync_zeroed, /*writes=*/true);
+                           sync_zeroed, /*writes=*/true, stamps, clean);
         return;
     }
     copy_fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);  // empty tensors only

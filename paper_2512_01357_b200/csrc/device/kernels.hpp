@@ -55,7 +55,9 @@ struct CopyFpTask {
 // into digests (no second kernel).
 void copy_fp_launch(const CopyFpTask* d_tasks, std::uint32_t n_tasks, std::uint64_t total_tiles, std::uint64_t* d_sums,
                     std::uint64_t* d_digests, std::uint64_t* d_sync, const std::uint64_t* d_need,
-                    std::uint32_t n_waves, int sm_count, cudaStream_t s, bool sync_zeroed = false);
+                    std::uint32_t n_waves, int sm_count, cudaStream_t s, bool sync_zeroed = false,
+                    std::uint64_t* stamps = nullptr,  // nullable: globaltimer ns at start / end
+                    bool clean = false);  // zero sums and sync counters after the digests (no gated waiters)
 // Warps one load-kernel launch keeps resident (tile-count sizing of the
 // independent work placed between gated waves).
 std::uint64_t copy_fp_resident_warps(int sm_count);

@@ -21,6 +21,7 @@
 
 namespace tg {
 
+
 namespace {
 // cuStreamWaitValue64 through the runtime's driver entry point (no -lcuda):
 // lets a copy stream wait on a counter the load kernel bumps, so a placement
@@ -142,6 +143,7 @@ FileStager::FileStager(int device, std::size_t chunk, int slots, int threads)
 }
 
 FileStager::~FileStager() {
+    end();
     DeviceScope ds(device_);
     for (cudaEvent_t e : free_) {
         cudaEventSynchronize(e);
@@ -150,60 +152,122 @@ FileStager::~FileStager() {
     for (std::uint8_t* p : slot_) cudaFreeHost(p);
 }
 
-void FileStager::stage(const std::string& path, u64 off, u64 size, std::uint8_t* dst, cudaStream_t s) {
-    const int fd = ::open(path.c_str(), O_RDONLY);
-    if (fd < 0) throw DeviceError(kErrNoSource, "cannot open " + path);
-    const int nslots = static_cast<int>(slot_.size());
-    // Read up to `threads_` chunks concurrently into free slots, then queue
-    // their H2D copies in order.
-    for (u64 base = 0; base < size;) {
-        struct Job {
-            int slot;
-            u64 at, n;
-            std::thread th;
-            bool ok = true;
-        };
-        std::vector<Job> jobs;
-        for (int k = 0; k < threads_ && base < size; ++k) {
-            const int sl = next_;
-            next_ = (next_ + 1) % nslots;
-            TG_CUDA(cudaEventSynchronize(free_[sl]));  // previous H2D from this slot drained
-            const u64 n = std::min<u64>(chunk_, size - base);
-            jobs.push_back(Job{sl, base, n, {}});
-            base += n;
-        }
-        for (Job& j : jobs)
-            j.th = std::thread([&, jp = &j] {
-                u64 done = 0;
-                if (Failpoints::hit("file_read")) {  // injected short read
-                    jp->ok = false;
-                    return;
-                }
-                while (done < jp->n) {
-                    const ssize_t r = ::pread(fd, slot_[jp->slot] + done, jp->n - done, static_cast<off_t>(off + jp->at + done));
-                    if (r <= 0) {
-                        jp->ok = false;
-                        return;
-                    }
-                    done += static_cast<u64>(r);
-                }
-            });
-        bool ok = true;
-        for (Job& j : jobs) {
-            j.th.join();
-            ok = ok && j.ok;
-        }
-        if (!ok) {
-            ::close(fd);
-            throw DeviceError(kErrNoSource, "short read from " + path);
-        }
-        for (Job& j : jobs) {
-            TG_CUDA(cudaMemcpyAsync(dst + j.at, slot_[j.slot], j.n, cudaMemcpyHostToDevice, s));
-            TG_CUDA(cudaEventRecord(free_[j.slot], s));
-            bytes_read_ += j.n;
-        }
+void FileStager::begin(std::vector<Range> ranges) {
+    end();
+    ranges_ = std::move(ranges);
+    chunks_.clear();
+    first_chunk_.clear();
+    fd_.assign(ranges_.size(), -1);
+    std::unordered_map<std::string, int> fds;
+    for (std::size_t r = 0; r < ranges_.size(); ++r) {
+        auto it = fds.find(ranges_[r].path);
+        if (it == fds.end()) it = fds.emplace(ranges_[r].path, ::open(ranges_[r].path.c_str(), O_RDONLY)).first;
+        fd_[r] = it->second;  // -1: reported by issue() as a missing file
+        first_chunk_.push_back(chunks_.size());
+        for (u64 at = 0; at < ranges_[r].size; at += chunk_)
+            chunks_.push_back(Chunk{r, at, std::min<u64>(chunk_, ranges_[r].size - at)});
     }
-    ::close(fd);
+    first_chunk_.push_back(chunks_.size());
+    state_.assign(chunks_.size(), 0);
+    next_read_ = issued_ = 0;
+    stop_ = false;
+    const int n = static_cast<int>(std::min<std::size_t>(threads_, chunks_.size()));
+    for (int t = 0; t < n; ++t) pool_.emplace_back([this] { reader(); });
+}
+
+// Reader thread: claim the next chunk, wait until its ring slot is free (the
+// H2D of the chunk `slots` earlier was issued and has completed), pread it.
+void FileStager::reader() {
+    cudaSetDevice(device_);
+    const std::size_t nslots = slot_.size();
+    for (;;) {
+        std::size_t k;
+        {
+            std::unique_lock<std::mutex> g(mu_);
+            if (stop_ || next_read_ >= chunks_.size()) return;
+            k = next_read_++;
+            cv_.wait(g, [&] { return stop_ || k < issued_ + nslots; });
+            if (stop_) return;
+        }
+        cudaEventSynchronize(free_[k % nslots]);  // the slot's previous H2D (this load's or an earlier one's) drained
+        const Chunk& c = chunks_[k];
+        const Range& r = ranges_[c.range];
+        const int fd = fd_[c.range];
+        std::uint8_t* buf = slot_[k % nslots];
+        bool ok = fd >= 0 && !Failpoints::hit("file_read");  // injected short read
+        for (u64 done = 0; ok && done < c.n;) {
+            const ssize_t got = ::pread(fd, buf + done, c.n - done, static_cast<off_t>(r.off + c.at + done));
+            if (got <= 0) ok = false;
+            else done += static_cast<u64>(got);
+        }
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            state_[k] = ok ? 1 : 2;
+        }
+        cv_.notify_all();
+    }
+}
+
+void FileStager::issue(std::size_t i, std::uint8_t* dst, cudaStream_t s) {
+    const std::size_t nslots = slot_.size();
+    for (std::size_t k = first_chunk_[i]; k < first_chunk_[i + 1]; ++k) {
+        {
+            std::unique_lock<std::mutex> g(mu_);
+            if (k != issued_) throw DeviceError(kErrCuda, "file stager: ranges issued out of order");
+            cv_.wait(g, [&] { return state_[k] != 0; });
+            if (state_[k] == 2) {
+                const std::string what = (fd_[i] < 0 ? "cannot open " : "short read from ") + ranges_[i].path;
+                g.unlock();
+                end();
+                throw DeviceError(kErrNoSource, what);
+            }
+        }
+        const Chunk& c = chunks_[k];
+        TG_CUDA(cudaMemcpyAsync(dst + c.at, slot_[k % nslots], c.n, cudaMemcpyHostToDevice, s));
+        TG_CUDA(cudaEventRecord(free_[k % nslots], s));
+        bytes_read_ += c.n;
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            ++issued_;
+        }
+        cv_.notify_all();
+    }
+    if (issued_ == chunks_.size()) end();
+}
+
+void FileStager::end() noexcept {
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        stop_ = true;
+    }
+    cv_.notify_all();
+    for (std::thread& t : pool_) t.join();
+    pool_.clear();
+    std::vector<int> closed;
+    for (int fd : fd_)
+        if (fd >= 0 && std::find(closed.begin(), closed.end(), fd) == closed.end()) {
+            ::close(fd);
+            closed.push_back(fd);
+        }
+    fd_.clear();
+}
+
+void FileStager::stage(const std::string& path, u64 off, u64 size, std::uint8_t* dst, cudaStream_t s) {
+    begin({Range{path, off, size}});
+    issue(0, dst, s);
+    end();
+}
+
+// 8 MiB chunks, a 256 MiB ring, 3/4 of the host threads reading (4..16;
+// TANGRAM_STAGER_THREADS overrides): page-cache preads run ~6 GB/s a thread,
+// so a dozen saturate the PCIe link.
+int stager_threads() {
+    if (const char* e = std::getenv("TANGRAM_STAGER_THREADS")) return std::max(1, std::atoi(e));
+    return std::clamp(static_cast<int>(std::thread::hardware_concurrency() * 3 / 4), 4, 16);
+}
+std::unique_ptr<FileStager> make_stager(int device) {
+    const int threads = stager_threads();
+    return std::make_unique<FileStager>(device, 8u << 20, 32, threads);
 }
 
 // ---- pool --------------------------------------------------------------------
@@ -281,6 +345,7 @@ void Pool::index_lookup(const std::vector<Key>& keys, std::vector<u64>* out) {
     out->assign(3 * n, 0);
     if (!n) return;
     ensure_stage(n * 5 * sizeof(u64) + 64);
+    resident_clean_ = false;  // the stage now holds keys, not a load's descriptors
     auto* h = static_cast<u64*>(h_stage_);
     auto* d = static_cast<u64*>(d_stage_);
     for (std::size_t i = 0; i < n; ++i) {
@@ -314,6 +379,7 @@ void Pool::ensure_stage(std::size_t bytes) {
     }
     TG_CUDA(cudaMallocHost(&h_stage_, n));
     TG_CUDA(cudaMalloc(&d_stage_, n));
+    resident_clean_ = false;
     // pinned memory is mapped (UVA): the load kernel's last warp writes the
     // digests straight into it, no D2H copy after the launch
     TG_CUDA(cudaHostGetDevicePointer(&h_stage_dev_, h_stage_, 0));
@@ -369,6 +435,7 @@ St Pool::load_model(const ModelDesc& m, const StatsView& stats, double clock, co
         return load_model_impl(m, stats, clock, opt, flags, rep);
     } catch (...) {
         ++totals_.failed_loads;
+        if (stager_) stager_->end();  // readers still ahead of a failed issue loop
         if (rep->committed && has_device()) {
             sync_all_streams();  // nothing of this load may still be writing when we return
             rep->suspect_after = 0;
@@ -709,15 +776,42 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // the stream synchronises; no D2H)
     auto* d_dig = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(h_stage_dev_) + desc_bytes + sums_bytes + sync_bytes);
     u64* d_fp_sync = d_sync + 2 + waves;  // two counters (tiles, finished CTAs) per K1 launch
-    if (nf + nc)
+    // the load kernel's globaltimer stamps (start, end), mapped like the digests
+    const std::size_t stamp_off = desc_bytes + 2 * sums_bytes + sync_bytes;
+    auto* h_stamps = reinterpret_cast<u64*>(h + stamp_off);
+    auto* d_stamps = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(h_stage_dev_) + stamp_off);
+    h_stamps[0] = h_stamps[1] = 0;
+    // Side streams join only when they carry work: a load with neither host
+    // nor peer-stream placements (a warm reload) is the load kernel alone on
+    // the pool stream, with no cross-stream dependency to resolve at its end
+    // and no events around the kernel (its span comes from its stamps).
+    bool copy_used = false, peer_used = false, fp_used = false;
+    for (std::size_t i = 0; i < np; ++i) {
+        copy_used = copy_used || rep->placement_src[i] == 0;
+        peer_used = peer_used || rep->placement_src[i] == 3 || (rep->placement_src[i] != 0 && !fused);
+        fp_used = fp_used || fp_of_placement[i] != kNone;
+    }
+    const bool lone = fused && ctiles && !copy_used && !peer_used && !fp_used;
+    // Resident descriptors: a lone load kernel leaves its sums and counters
+    // zeroed (it cleans up after its digests), so a load whose descriptors
+    // equal the ones already on the device (a reload of an unchanged model)
+    // launches with no upload in front of the kernel.
+    const bool resident = lone && resident_clean_ && resident_desc_.size() == desc_bytes &&
+                          resident_layout_ == std::make_pair(sums_bytes, sync_bytes) &&
+                          std::memcmp(resident_desc_.data(), h, desc_bytes) == 0;
+    resident_clean_ = false;  // until this load's kernel has cleaned up
+    if (nf + nc && !resident) {
         TG_CUDA(cudaMemcpyAsync(dptr, h, desc_bytes + sums_bytes + sync_bytes, cudaMemcpyHostToDevice, s_main_));
+        resident_desc_.assign(h, h + desc_bytes);
+        resident_layout_ = {sums_bytes, sync_bytes};
+    }
 
     // ---- device work on the main stream: the load kernel (fused) or the K3
     // relocation waves (unfused) ----------------------------------------------------
-    TG_CUDA(cudaEventRecord(ev(1), s_main_));
+    if (!lone) TG_CUDA(cudaEventRecord(ev(1), s_main_));
     if (fused) {
         copy_fp_launch(d_ctasks, static_cast<u32>(nc), ctiles, d_sums + 2 * nf, d_dig + 2 * nf, d_sync, d_need, waves,
-                       sm_count_, s_main_, /*sync_zeroed=*/true);
+                       sm_count_, s_main_, /*sync_zeroed=*/true, d_stamps, /*clean=*/lone);
         TG_CUDA(cudaGetLastError());
         for (u32 w = 0; w < waves; ++w) TG_CUDA(cudaEventRecord(ev(ev_wave + w), s_main_));
         for (std::size_t i = 0; i < np; ++i)
@@ -733,7 +827,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         TG_CUDA(cudaGetLastError());
         TG_CUDA(cudaEventRecord(ev(ev_wave + w), s_main_));
     }
-    TG_CUDA(cudaEventRecord(ev(2), s_main_));
+    if (!lone) TG_CUDA(cudaEventRecord(ev(2), s_main_));
 
     // ---- placements: host→device on the copy stream, device sources (peer pool,
     // HBM cache) on the peer stream.  Independent placements first, then those
@@ -741,10 +835,14 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     std::vector<std::size_t> order(np);
     for (std::size_t i = 0; i < np; ++i) order[i] = i;
     std::stable_sort(order.begin(), order.end(), [&](std::size_t a, std::size_t b) { return dep[a] < dep[b]; });
-    TG_CUDA(cudaStreamWaitEvent(s_copy_, ev(0)));
-    TG_CUDA(cudaStreamWaitEvent(s_peer_, ev(1)));  // K3F reads its descriptors
-    TG_CUDA(cudaEventRecord(ev(4), s_copy_));
-    TG_CUDA(cudaEventRecord(ev(6), s_peer_));
+    if (copy_used) {
+        TG_CUDA(cudaStreamWaitEvent(s_copy_, ev(0)));
+        TG_CUDA(cudaEventRecord(ev(4), s_copy_));
+    }
+    if (peer_used) {
+        TG_CUDA(cudaStreamWaitEvent(s_peer_, ev(1)));  // K3F reads its descriptors
+        TG_CUDA(cudaEventRecord(ev(6), s_peer_));
+    }
     // Gates: unfused, the event after wave w's K3 launch.  Fused, the load
     // kernel's own counter of wave w's finished tiles (each bumped with a
     // release after the tile's last read of its source): the stream waits
@@ -824,6 +922,21 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         if (sz == 0) hp.push_back(Piece{i, 0, 0, -1});
     }
     std::stable_sort(hp.begin(), hp.end(), [](const Piece& a, const Piece& b) { return a.dep < b.dep; });
+    // Model Store pieces: the stager's readers start on all of them now and
+    // run ahead of the issue loop below.
+    std::vector<std::size_t> file_range(hp.size(), kNone);
+    {
+        std::vector<FileStager::Range> ranges;
+        for (std::size_t k = 0; k < hp.size(); ++k)
+            if (hp[k].len && src[hp[k].pl].is_file()) {
+                file_range[k] = ranges.size();
+                ranges.push_back(FileStager::Range{src[hp[k].pl].path, src[hp[k].pl].file_off + hp[k].at, hp[k].len});
+            }
+        if (!ranges.empty()) {
+            if (!stager_) stager_ = make_stager(device_);
+            stager_->begin(std::move(ranges));
+        }
+    }
     std::vector<std::size_t> last_piece(np, kNone);
     for (std::size_t k = 0; k < hp.size(); ++k) last_piece[hp[k].pl] = k;
     for (std::size_t k = 0; k < hp.size(); ++k) {
@@ -840,8 +953,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         const HostSource& hs = src[pc.pl];
         if (pc.len) {
             if (hs.is_file()) {
-                if (!stager_) stager_ = std::make_unique<FileStager>(device_, 16u << 20, 8, 4);
-                stager_->stage(hs.path, hs.file_off + pc.at, pc.len, dst, s_copy_);
+                stager_->issue(file_range[k], dst, s_copy_);
             } else {
                 if (Failpoints::hit("h2d")) throw DeviceError(kErrCuda, "failpoint h2d: injected copy failure");
                 TG_CUDA(cudaMemcpyAsync(dst, static_cast<const std::uint8_t*>(hs.ptr) + pc.at, pc.len,
@@ -853,16 +965,16 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             land_order.push_back(pc.pl);
         }
     }
-    TG_CUDA(cudaEventRecord(ev(5), s_copy_));
-    TG_CUDA(cudaEventRecord(ev(7), s_peer_));
+    if (copy_used) TG_CUDA(cudaEventRecord(ev(5), s_copy_));
+    if (peer_used) TG_CUDA(cudaEventRecord(ev(7), s_peer_));
 
     // ---- K1 over placed tensors, trailing the copies ------------------------------
     std::size_t fp_i = 0;
     bool fp_stream_used = false;
-    TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(1)));  // descriptors uploaded, sums zeroed
     for (std::size_t i : land_order) {
         const std::size_t k = fp_of_placement[i];
         if (k == kNone) continue;
+        if (!fp_stream_used) TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(1)));  // descriptors uploaded, sums zeroed
         TG_CUDA(cudaStreamWaitEvent(s_fp_, ev(ev_land + i)));
         TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s_fp_));
         fp_launch(d_tasks + k, 1, new_tiles[k], d_sums + 2 * k, d_dig + 2 * k, d_fp_sync + 2 * fp_i, sm_count_, s_fp_,
@@ -875,7 +987,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // ---- K1 over reused tensors: untouched ones now (verify stream); relocated
     // ones after the waves (main stream) unless K3F already hashed them --------
     std::size_t fp_reuse_slot = fp_i, fp_reuse_launches = 0;
-    if (fp_reuse) {
+    if (fp_reuse && !fused) {  // fused: the load kernel verifies them
         auto launch = [&](cudaStream_t s, std::size_t first, std::size_t count, u64 tiles) {
             if (!count) return;
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s));
@@ -887,21 +999,21 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             ++fp_reuse_launches;
         };
         TG_CUDA(cudaStreamWaitEvent(s_verify_, ev(1)));
-        if (!fused) {
-            launch(s_verify_, hit_base, n_still, still_tiles);
-            launch(s_main_, hit_base + n_still, hit_keys.size() - n_still, moved_tiles);
-        }
+        launch(s_verify_, hit_base, n_still, still_tiles);
+        launch(s_main_, hit_base + n_still, hit_keys.size() - n_still, moved_tiles);
         TG_CUDA(cudaEventRecord(ev(8), s_verify_));
         TG_CUDA(cudaStreamWaitEvent(s_main_, ev(8)));
     }
     // ---- device index: the committed map, uploaded on a side stream while the
     // data plane runs (the pool stream joins it: valid for work ordered after
     // the load on the pool stream) ---------------------------------------------
-    TG_CUDA(cudaStreamWaitEvent(s_verify_, ev(0)));
-    publish_index(s_verify_);
+    if (store_.epoch() != published_epoch_) {
+        TG_CUDA(cudaStreamWaitEvent(s_verify_, ev(0)));
+        publish_index(s_verify_);
+    }
     // ---- join, read digests, end ------------------------------------------------
-    TG_CUDA(cudaStreamWaitEvent(s_main_, ev(5)));
-    TG_CUDA(cudaStreamWaitEvent(s_main_, ev(7)));
+    if (copy_used) TG_CUDA(cudaStreamWaitEvent(s_main_, ev(5)));
+    if (peer_used) TG_CUDA(cudaStreamWaitEvent(s_main_, ev(7)));
     if (fp_stream_used) {
         TG_CUDA(cudaEventRecord(ev(3), s_fp_));
         TG_CUDA(cudaStreamWaitEvent(s_main_, ev(3)));
@@ -922,7 +1034,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // ---- completion: wait for the data plane, then record / verify digests.
     // Runs now, or — with kLoadAsync — before the next operation on this pool
     // (complete_pending), so loads on different pools overlap.
-    auto finish = [this, h_dig, np, nf, fused, hit_base, n_still, fp_reuse, waves, nc, gate_recorded, ev_gate, ev_fp,
+    auto finish = [this, h_dig, h_stamps, ctiles, lone, np, nf, fused, copy_used, peer_used, hit_base, n_still, fp_reuse, waves, nc, gate_recorded, ev_gate, ev_fp,
                    fp_i, fp_reuse_slot, fp_reuse_launches, h0, h_issued, fp_of_placement = std::move(fp_of_placement),
                    ctask_of_placement = std::move(ctask_of_placement), has_truth = std::move(has_truth),
                    truth = std::move(truth), hit_keys = std::move(hit_keys), hit_pos = std::move(hit_pos),
@@ -932,18 +1044,32 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     LoadDecision& D = rep->decision;
     {
         NvtxRange r("tg.wait_data_plane");
+        // A load that is the load kernel alone: poll its end stamp in mapped
+        // memory (written after the digests) — the host sees the end a few
+        // microseconds before a stream synchronize would return; the
+        // synchronize that follows then finds the stream (nearly) drained.
+        if (lone) {
+            const volatile u64* end = h_stamps + 1;
+            for (std::uint32_t spin = 0; *end == 0 && spin < (1u << 26); ++spin) {
+            }
+        }
         TG_CUDA(cudaStreamSynchronize(s_main_));
     }
     rep->t.host_wait_us = std::chrono::duration<double, std::micro>(clk::now() - h_issued).count();
     NvtxRange nvtx_verify("tg.record_verify_digests");
 
+    // (each event query costs ~3 us of host time: the load kernel's span comes
+    // from its own globaltimer stamps, and a load that is that kernel alone
+    // on the pool stream ends with it)
     rep->t.total_ms = ms_between(ev(0), ev(3));
+    const bool stamped = fused && ctiles && h_stamps[1] > h_stamps[0] && h_stamps[0];
     // fused: the whole load kernel (waves, device-source placements, verification)
-    rep->t.relocate_ms = (waves || (fused && nc)) ? ms_between(ev(1), ev(2)) : 0.0;
-    rep->t.kernel_end_ms = ms_between(ev(0), ev(2));
+    rep->t.relocate_ms = stamped ? (h_stamps[1] - h_stamps[0]) * 1e-6
+                                 : (!lone && (waves || (fused && nc))) ? ms_between(ev(1), ev(2)) : 0.0;
+    rep->t.kernel_end_ms = lone ? rep->t.total_ms : ms_between(ev(0), ev(2));
     rep->t.gated_h2d_start_ms = gate_recorded ? ms_between(ev(0), ev(ev_gate)) : 0.0;
-    rep->t.h2d_ms = rep->pcie_bytes ? ms_between(ev(4), ev(5)) : 0.0;
-    rep->t.peer_ms = (rep->peer_bytes || rep->device_src_bytes) ? ms_between(ev(6), ev(7)) : 0.0;
+    rep->t.h2d_ms = copy_used && rep->pcie_bytes ? ms_between(ev(4), ev(5)) : 0.0;
+    rep->t.peer_ms = peer_used ? ms_between(ev(6), ev(7)) : 0.0;
     for (std::size_t f = 0; f < fp_i; ++f) {
         const double t = ms_between(ev(ev_fp + 2 * f), ev(ev_fp + 2 * f + 1));
         rep->t.fp_kernel_ms += t;
@@ -1074,6 +1200,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     totals_.verify_mismatches += rep->verify_mismatches;
     totals_.repaired_bytes += rep->repaired_bytes;
     if (fail) throw DeviceError(fail, fail_what);
+    resident_clean_ = lone;  // the kernel zeroed its sums and counters
     return 0;
     };
     if (flags & kLoadAsync) {
@@ -1154,7 +1281,7 @@ bool Pool::assemble_shard(const TensorDesc& t, std::vector<MoveDesc>* pieces, co
 // Bytes of a registered source into the arena (repair paths).
 void Pool::fetch(const HostSource& hs, std::uint8_t* dst, u64 size, cudaStream_t s) {
     if (hs.is_file()) {
-        if (!stager_) stager_ = std::make_unique<FileStager>(device_, 16u << 20, 8, 4);
+        if (!stager_) stager_ = make_stager(device_);
         stager_->stage(hs.path, hs.file_off, size, dst, s);
     } else {
         TG_CUDA(cudaMemcpyAsync(dst, hs.ptr, size, cudaMemcpyDefault, s));

@@ -11,10 +11,12 @@
 
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -44,26 +46,57 @@ struct HostSource {
     bool is_file() const { return !path.empty(); }
 };
 
-// Pinned staging ring for file-backed placements: reader threads pread chunks
-// into free slots while the copy engine drains filled ones, so storage and
-// PCIe overlap.  One per pool, created on first use.
+// Pinned staging ring for file-backed placements (Model Store → GPU).  A
+// load hands the stager every file range it will place, in issue order
+// (begin); reader threads then pread fixed-size chunks into the ring ahead
+// of the caller — each slot reused once the H2D that drained it completed —
+// while the caller issues the H2D of each range in turn (issue), so storage
+// reads, PCIe copies and the fingerprint kernels trailing them all overlap
+// across tensors.  One per pool, created on first use; the ring stays
+// allocated, the reader threads live for one load (end / destructor join
+// them).
 class FileStager {
 public:
     FileStager(int device, std::size_t chunk, int slots, int threads);
     ~FileStager();
-    // Enqueue `size` bytes of `path` at `off` into dst on stream s (stream
-    // order is preserved; returns once every chunk has been read and queued).
+    struct Range {
+        std::string path;
+        u64 off = 0, size = 0;
+    };
+    // Start reading `ranges` (in the order they will be issued).
+    void begin(std::vector<Range> ranges);
+    // Enqueue range i's H2D into dst on stream s, chunk by chunk as the
+    // readers fill them (ranges must be issued in order).  Throws
+    // DeviceError(kErrNoSource) on a short read / missing file.
+    void issue(std::size_t i, std::uint8_t* dst, cudaStream_t s);
+    void end() noexcept;  // stop and join the readers (idempotent)
+    // begin + issue + end of one range
     void stage(const std::string& path, u64 off, u64 size, std::uint8_t* dst, cudaStream_t s);
     u64 bytes_read() const { return bytes_read_; }
 
 private:
+    struct Chunk {
+        std::size_t range;
+        u64 at, n;  // within the range
+    };
+    void reader();
     int device_;
     std::size_t chunk_;
     std::vector<std::uint8_t*> slot_;
     std::vector<cudaEvent_t> free_;  // recorded after the H2D that drained the slot
     int threads_;
-    int next_ = 0;
     u64 bytes_read_ = 0;
+    // one load's session
+    std::vector<Range> ranges_;
+    std::vector<int> fd_;  // per range (shared per path)
+    std::vector<Chunk> chunks_;
+    std::vector<std::size_t> first_chunk_;  // per range
+    std::vector<std::uint8_t> state_;       // per chunk: 0 pending, 1 ready, 2 failed
+    std::size_t next_read_ = 0, issued_ = 0;
+    bool stop_ = false;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::vector<std::thread> pool_;
 };
 
 // Test failpoints (tg_failpoint, include/tangram.h): arm a named point so that
@@ -280,6 +313,11 @@ private:
     cudaEvent_t ev_reader_ = nullptr;
     void note_readers();
     void wait_readers();
+    // descriptors of the last upload still on the device, and whether the
+    // stage's sums / counters are zero (a lone load kernel cleaned them)
+    std::vector<std::uint8_t> resident_desc_;
+    std::pair<std::size_t, std::size_t> resident_layout_{0, 0};
+    bool resident_clean_ = false;
     std::unique_ptr<PendingLoad> pending_;
     LoadReport last_async_;
     int last_async_rc_ = 0;

@@ -337,6 +337,48 @@ def test_model_store_file_sources(tg, cpu, tmp_path):
     pool.close()
 
 
+def test_model_store_pipelined_ranges_across_files(tg, cpu, tmp_path):
+    """The stager's readers run ahead of the issue loop over every file range
+    of a load: tensors from 0 B to several 8 MiB chunks, split over two files
+    at unaligned offsets, a second model's ranges interleaved in the same
+    files.  Every placed byte equals the CPU restatement."""
+    from paper_2512_01357_b200 import _native as N
+    sizes = [0, 1, 4095, 8 << 20, (8 << 20) + 17, 3 * (8 << 20) - 5, 50_000_011, 123_457, 33_554_433, 7]
+    m = tg.make_model("store-pipe", sum(sizes), len(sizes), 0, location=tg.ModelLocation.ModelStore)
+    # make_model splits the total evenly; re-cut it to the sizes above
+    ts = [tg.TensorSpec(id=t.id, model_id=m.model_id, name=t.name, size=sz) for t, sz in zip(m.tensors, sizes)]
+    m = tg.ModelSpec(model_id=m.model_id, tensors=ts, total_size=sum(sizes), location=tg.ModelLocation.ModelStore)
+    files = [tmp_path / "a.bin", tmp_path / "b.bin"]
+    handles = [open(f, "wb") for f in files]
+    for i, h in enumerate(handles):
+        h.write(b"x" * (3 + 5 * i))
+    offs = {}
+    for i, t in enumerate(m.tensors):
+        h = handles[i % 2]
+        offs[t.id] = (str(files[i % 2]), h.tell())
+        h.write(cpu.synth(t.id.hi, t.id.lo, t.size).tobytes() if t.size else b"")
+        h.write(b"pad")
+    for h in handles:
+        h.close()
+    for t in m.tensors:
+        path, off = offs[t.id]
+        assert N.lib.tg_file_register(t.id.c(), path.encode(), off, t.size, None) == 0
+    pool = tg.ReuseStore(tg.GpuSpec(pool_size=256 << 20), device=0)
+    st = tg.ModelStatsTable()
+    st.record_request(m.model_id, 0.0)
+    try:
+        o = pool.load_model(m, st, 0.0).value()
+        assert o.pcie_bytes == m.total_size and o.verify_mismatches == 0
+        for i, t in enumerate(m.tensors):
+            want = cpu.content_fingerprint(cpu.synth(t.id.hi, t.id.lo, t.size), threads=8)[0]
+            assert o.digests[i] == want, t.name
+            assert pool.fingerprint_tensor(t.id) == want, t.name
+    finally:
+        for t in m.tensors:
+            N.lib.tg_host_unregister(t.id.c())
+        pool.close()
+
+
 @pytest.mark.parametrize("source", ["hbm", "host"])
 @pytest.mark.parametrize("seed", [52, 51, 13, 7, 99, 1234])
 def test_fused_load_kernel_fuzz(tg, cpu, seed, source):
