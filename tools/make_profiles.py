@@ -71,13 +71,12 @@ def _bytes(v):
     return float(val.replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}[unit]
 
 
-def traffic(rep, out_path):
+def traffic(rep, out_path, algo=None, source=None):
     """DRAM traffic of the bench step's load-kernel launch against the step's
     algorithmic bytes (printed by the same bench --profile run)."""
     launches = summarise(rep)
-    algo = None
     log = os.path.join(OUT, "prof_load.log")
-    if os.path.exists(log):
+    if algo is None and os.path.exists(log):
         for ln in open(log):
             if ln.startswith("{"):
                 algo = json.loads(ln).get("roofline_step", {}).get("algorithmic_bytes_per_step")
@@ -89,7 +88,7 @@ def traffic(rep, out_path):
     with open(out_path, "w") as f:
         json.dump({"traffic_bytes_per_launch": t, "algorithmic_bytes": algo,
                    "ratio": t / algo if algo else None,
-                   "source": "ncu --set full --clock-control none of the bench step's load-kernel launch "
+                   "source": source or "ncu --set full --clock-control none of the bench step's load-kernel launch "
                              "(bench.py --profile --steps 1 --warmup 0); dram__bytes_read.sum + dram__bytes_write.sum",
                    "per_launch": per}, f, indent=1)
 
@@ -115,6 +114,13 @@ def main():
         traffic(lk, os.path.join(PROF, "load_kernel_traffic.json"))
         with open(os.path.join(PROF, f"{tag}_load_kernel_stalls.json"), "w") as f:
             json.dump(load_kernel_stalls(lk), f, indent=1)
+    k3 = os.path.join(OUT, "prof_k3.ncu-rep")
+    if os.path.exists(k3):
+        traffic(k3, os.path.join(PROF, f"{tag}_k3_traffic.json"), algo=2 * (4 << 30),
+                source="ncu --set full --clock-control none of K3 relocate_bulk_kernel moving 4 GiB src+0 -> dst+5 "
+                       "(tools/kernel_bench.py --only reloc --gib 8); algorithmic = 4 GiB read + 4 GiB written")
+        with open(os.path.join(PROF, f"{tag}_k3_stalls.json"), "w") as f:
+            json.dump(load_kernel_stalls(k3), f, indent=1)
     for extra in ("kernel_bench.json", "bench.json"):
         p = os.path.join(OUT, extra)
         if os.path.exists(p):

@@ -4,6 +4,7 @@
 #                         (cold-cache, serialised: compare SHARES)
 #   prof_load.ncu-rep   — ncu --set full of the bench step's load-kernel launch
 #   prof_k1.ncu-rep     — ncu --set full of a fingerprint-only (K1) launch, unfused A/B run
+#   prof_k3.ncu-rep     — ncu --set full of K3 (relocate_bulk_kernel), misaligned src0 -> dst5, 4 GiB
 #   kernel_bench.json   — isolated kernel bandwidths
 set -x
 mkdir -p gpurun_out
@@ -20,4 +21,8 @@ ncu --set full --clock-control none --import-source on -k regex:copy_fp_kernel -
 TANGRAM_UNFUSED=1 ncu --set full --clock-control none --import-source on -k regex:copy_fp_kernel -s 15 -c 1 \
     -o gpurun_out/prof_k1 -f python bench.py --profile --steps 1 --warmup 0 --no-cpu-baseline \
     > gpurun_out/prof_k1.log 2>&1
+# K3 alone: kernel_bench --only reloc launches warm-up + 1 rep per (src, dst)
+# class; launch 2 is the (0, 5) class's first
+ncu --set full --clock-control none --import-source on -k regex:relocate -s 2 -c 1 -o gpurun_out/prof_k3 -f \
+    python tools/kernel_bench.py --only reloc --gib 8 --reps 1 > gpurun_out/prof_k3.log 2>&1
 ls -la gpurun_out
