@@ -830,12 +830,12 @@ void copy_fp_launch(const CopyFpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64
 }
 
 void fp_launch(const FpTask* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, u64* d_sync,
-               int sm_count, cudaStream_t s, bool sync_zeroed) {
+               int sm_count, cudaStream_t s, bool sync_zeroed, u64* stamps, bool clean) {
     if (n_tasks == 0) return;
     // K1 is the load kernel with fingerprint-only tasks
     if (total_tiles > 0) {
         load_kernel_launch(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, nullptr, 0, sm_count, s,
-                           sync_zeroed, /*writes=*/false);
+                           sync_zeroed, /*writes=*/false, stamps, clean);
         return;
     }
     fp_finalize_kernel<<<(n_tasks + 127) / 128, 128, 0, s>>>(d_tasks, n_tasks, d_sums, d_digests);  // empty tensors only

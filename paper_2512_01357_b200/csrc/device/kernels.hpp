@@ -30,7 +30,7 @@ struct FpTask {
 // kernel below with fingerprint-only tasks; its last CTA writes the digests.
 void fp_launch(const FpTask* d_tasks, std::uint32_t n_tasks, std::uint64_t total_tiles, std::uint64_t* d_sums,
                std::uint64_t* d_digests, std::uint64_t* d_sync, int sm_count, cudaStream_t s,
-               bool sync_zeroed = false);
+               bool sync_zeroed = false, std::uint64_t* stamps = nullptr, bool clean = false);
 
 // ---- K3F: copy + fingerprint in one pass — the load kernel ---------------
 // Moves every task's n bytes src -> dst (any alignments) and produces the
