@@ -280,6 +280,11 @@ Pool::Pool(GpuDesc gpu, int device) : store_(std::move(gpu)), device_(device) {
     TG_CUDA(cudaMalloc(reinterpret_cast<void**>(&arena_), store_.pool_size() + 256));
     for (cudaStream_t* s : {&s_main_, &s_copy_, &s_fp_, &s_peer_, &s_verify_})
         TG_CUDA(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+    // One-time setup here, not inside the first load's latency: the pinned /
+    // device descriptor stage (a pinned allocation costs milliseconds) and
+    // the events a load of up to ~100 tensors records.
+    ensure_stage(1 << 20);
+    ensure_events(256);
 }
 
 Pool::~Pool() {
