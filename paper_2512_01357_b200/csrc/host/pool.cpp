@@ -258,6 +258,14 @@ void FileStager::stage(const std::string& path, u64 off, u64 size, std::uint8_t*
     end();
 }
 
+bool verify_split() {
+    static const bool on = [] {
+        const char* e = std::getenv("TANGRAM_VERIFY_SPLIT");
+        return e && std::strcmp(e, "1") == 0;
+    }();
+    return on;
+}
+
 // 8 MiB chunks, a 256 MiB ring, 3/4 of the host threads reading (4..16;
 // TANGRAM_STAGER_THREADS overrides): page-cache preads run ~6 GB/s a thread,
 // so a dozen saturate the PCIe link.
@@ -703,9 +711,12 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     }
     const std::size_t hit_base = tasks.size();
     u64 still_tiles = 0, moved_tiles = 0;
-    if (fp_reuse && !fused) {
+    // A/B (TANGRAM_VERIFY_SPLIT=1): a fused load verifies its untouched hits
+    // in a concurrent K1 launch instead of inside the load kernel.
+    const bool split = fused && fp_reuse && verify_split();
+    if (fp_reuse && (!fused || split)) {
         std::vector<FpTask> still, moved_hits;
-        for (std::size_t h = 0; h < hit_keys.size(); ++h) {
+        for (std::size_t h = 0; h < (split ? n_still : hit_keys.size()); ++h) {
             const Entry* e = store_.entry(hit_keys[h]);
             (h < n_still ? still : moved_hits).push_back(FpTask{arena_ + e->off, e->size, 0});
         }
@@ -730,7 +741,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             return e ? std::strtoull(e, nullptr, 10) : 8ull;
         }();
         const u64 share = rounds * copy_fp_resident_warps(sm_count_);
-        const std::size_t n_verify = fp_reuse ? n_still : 0;
+        const std::size_t n_verify = fp_reuse && !split ? n_still : 0;
         std::size_t next_verify = 0;
         for (u32 g = 0; g <= waves; ++g) {
             const int gate = static_cast<int>(g) - 1;
@@ -807,7 +818,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         peer_used = peer_used || rep->placement_src[i] == 3 || (rep->placement_src[i] != 0 && !fused);
         fp_used = fp_used || fp_of_placement[i] != kNone;
     }
-    const bool lone = fused && ctiles && !copy_used && !peer_used && !fp_used;
+    const bool lone = fused && ctiles && !copy_used && !peer_used && !fp_used && !split;
     // Resident descriptors: a lone load kernel leaves its sums and counters
     // zeroed (it cleans up after its digests), so a load whose descriptors
     // equal the ones already on the device (a reload of an unchanged model)
@@ -1007,7 +1018,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // ---- K1 over reused tensors: untouched ones now (verify stream); relocated
     // ones after the waves (main stream) unless K3F already hashed them --------
     std::size_t fp_reuse_slot = fp_i, fp_reuse_launches = 0;
-    if (fp_reuse && !fused) {  // fused: the load kernel verifies them
+    if (fp_reuse && (!fused || split)) {  // fused: the load kernel verifies them
         auto launch = [&](cudaStream_t s, std::size_t first, std::size_t count, u64 tiles) {
             if (!count) return;
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s));
@@ -1020,7 +1031,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         };
         TG_CUDA(cudaStreamWaitEvent(s_verify_, ev(1)));
         launch(s_verify_, hit_base, n_still, still_tiles);
-        launch(s_main_, hit_base + n_still, hit_keys.size() - n_still, moved_tiles);
+        if (!fused) launch(s_main_, hit_base + n_still, hit_keys.size() - n_still, moved_tiles);
         TG_CUDA(cudaEventRecord(ev(8), s_verify_));
         TG_CUDA(cudaStreamWaitEvent(s_main_, ev(8)));
     }
@@ -1054,7 +1065,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // ---- completion: wait for the data plane, then record / verify digests.
     // Runs now, or — with kLoadAsync — before the next operation on this pool
     // (complete_pending), so loads on different pools overlap.
-    auto finish = [this, h_dig, h_stamps, ctiles, lone, np, nf, fused, copy_used, peer_used, hit_base, n_still, fp_reuse, waves, nc, gate_recorded, ev_gate, ev_fp,
+    auto finish = [this, h_dig, h_stamps, ctiles, lone, split, np, nf, fused, copy_used, peer_used, hit_base, n_still, fp_reuse, waves, nc, gate_recorded, ev_gate, ev_fp,
                    fp_i, fp_reuse_slot, fp_reuse_launches, h0, h_issued, fp_of_placement = std::move(fp_of_placement),
                    ctask_of_placement = std::move(ctask_of_placement), has_truth = std::move(has_truth),
                    truth = std::move(truth), hit_keys = std::move(hit_keys), hit_pos = std::move(hit_pos),
@@ -1170,8 +1181,8 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     std::vector<char> verified(rel.size(), 0);  // relocated hits settled here
     for (std::size_t hix = 0; fp_reuse && hix < hit_keys.size(); ++hix) {
         const Key& k = hit_keys[hix];
-        const std::size_t slot = !fused          ? hit_base + hix
-                                 : hix < n_still ? nf + ctask_of_still[hix]
+        const std::size_t slot = !fused || (split && hix < n_still) ? hit_base + hix
+                                 : hix < n_still                       ? nf + ctask_of_still[hix]
                                                  : nf + ctask_of_reloc[hit_rel[hix]];
         const Digest g = digest_at(slot);
         Entry* e = store_.entry(k);
