@@ -49,6 +49,24 @@ def test_simulator_runmetrics_identical(binaries, cfg):
     assert a == b
 
 
+@pytest.mark.parametrize("async_loads", ["0", "1"])
+def test_peer_term_without_peer_bytes_is_the_reference(binaries, async_loads):
+    """integration/warmsim/scheduler.hpp routes schedule / estimate_load_time
+    through tg_schedule.  With the peer term switched on
+    (TANGRAM_PEER_SCHEDULE) but no device pool holding bytes, S'_peer = 0 for
+    every (GPU, model) and the estimate (S - S' - S'_peer)/B + S'_peer/B_nvlink
+    reduces to the reference's (S - S')/B (scheduler.hpp:41-48): RunMetrics
+    stay byte-identical.  TG_LOAD_ASYNC on control-plane pools is a no-op."""
+    ref_bin, tg_bin = binaries
+    args = [str(x) for x in ("reuse_odkv", 4, 24, 4, 2, 400, 42, 0, 0, "L3")] + [
+        "opt1.3B,qwen3B,llama3B,opt6.7B,llama8B,yi9B"]
+    env = dict(os.environ, TANGRAM_DEVICE="none", TANGRAM_PEER_SCHEDULE="700", TANGRAM_ASYNC_LOADS=async_loads)
+    a = subprocess.run([ref_bin] + args, capture_output=True, check=True, timeout=300).stdout
+    b = subprocess.run([tg_bin] + args, capture_output=True, check=True, timeout=300, env=env).stdout
+    assert a.strip() and b"exception" not in a
+    assert a == b
+
+
 def test_store_copies_are_independent_values():
     """reuse_store.hpp:336-344: a copied store is independent of its original
     (the reference copies stores for rollback, kv_engine.hpp:146-158).  The
