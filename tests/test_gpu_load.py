@@ -586,6 +586,35 @@ def test_device_store_differential_fuzz(tg, ref, cpu, seed):
                on_step=_soak_checker(tg, cpu, seed, {}))
 
 
+@pytest.mark.parametrize("seed", range(max(1, SOAK_SEEDS // 2)))
+def test_device_store_fuzz_async(tg, ref, cpu, seed):
+    """The device fuzz with every load asynchronous (TG_LOAD_ASYNC): decisions
+    and dumps still equal the reference op by op (they are final when the
+    call returns).  After half of the ops the pending load is finished
+    explicitly (tg_pool_sync: no mismatch, nothing left suspect) and every
+    resident tensor is checked against the CPU restatement; after the other
+    half nothing is checked, so the next op — a load, an eviction, a move, a
+    KV region — has to land the previous load itself."""
+    import random
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    pick = random.Random(7000 + seed)
+    check = _soak_checker(tg, cpu, seed, {})
+
+    def sources(models, pool):
+        return HbmCache(tg, models) if seed % 2 else HostCheckpoint(models)
+
+    def on_step(pool, r):
+        if pick.random() < 0.5:
+            return
+        done = pool.sync()
+        if done is not None:
+            assert done.verify_mismatches == 0 and done.suspect_tensors == 0
+        check(pool, r)
+
+    _fuzz_once(tg, ref, 3000 + seed, n_ops=120, device=0, scale=257, sources=sources, on_step=on_step,
+               extra_flags=16)
+
+
 def _soak_checker(tg, cpu, seed, expected, peer_bytes=None):
     def on_step(pool, r):
         if r is not None and r.ok():
