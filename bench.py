@@ -473,7 +473,7 @@ def run_ours(args):
 
     traffic = None
     tf = os.path.join(ROOT, "profiles", "load_kernel_traffic.json" if policy.flags & 8 else "fp_reuse_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and not shared_gpu():  # the capture is of the 32 GiB C2 step
         try:
             traffic = json.load(open(tf)).get("traffic_bytes_per_launch")
         except Exception:
@@ -523,7 +523,8 @@ def run_ours(args):
             "e2e_sources": "missing tensors in pinned host memory, cudaMemcpyAsync H2D",
             "fingerprint": f"tgfp1 over all {len(target.tensors)} tensors ({len(miss_ids)} placed + {len(hits)} reused "
                            f"verified)",
-            "l2": "no flush: every step streams >= 20 GB, >> 126 MB L2; arena restored (D2D 32 GiB) between steps",
+            "l2": f"no flush: every step streams >= {step_bytes / 1e9:.1f} GB, >> 126 MB L2; arena restored "
+                  f"(D2D {POOL // GIB} GiB) between steps",
             "timing": "CUDA events on the pool stream around each synchronous load; snapshot restore untimed; "
                       "mean over steps, max over ranks",
             "parallelism": f"{world} independent pools (one per GPU)",
