@@ -160,6 +160,7 @@ struct TileRef {
     const std::uint8_t* base;  // tensor base
     u64 n;                   // tensor bytes
     u64 leaf0;
+    u64 seed0;               // the task's leaf_base: seed of leaf l is seed0 + l
     u32 nfull;
     u32 o;
     int task;
@@ -225,7 +226,7 @@ struct CopyTileRef {
 // K1 runs through the load kernel too: an FpTask is a fingerprint-only task.
 __device__ __forceinline__ CopyFpTask as_copy_task(const CopyFpTask& t) { return t; }
 __device__ __forceinline__ CopyFpTask as_copy_task(const FpTask& t) {
-    return CopyFpTask{t.base, nullptr, t.n, t.tile0, -1, -1};
+    return CopyFpTask{t.base, nullptr, t.n, t.tile0, -1, -1, 0};
 }
 
 // Task of tile t: the last task with tile0 <= t.  A warp takes its tiles in
@@ -255,6 +256,7 @@ __device__ __forceinline__ CopyTileRef copy_tile_ref(const Task* __restrict__ ta
     r.t.task = static_cast<int>(lo);
     r.t.base = tk.src;
     r.t.n = tk.n;
+    r.t.seed0 = tk.leaf_base & ~kRawSums;
     // A task's tiles are dispensed last-first: the tile holding the partial
     // leaf and the tail bytes (one lane hashes that leaf serially) comes
     // early, so the launch's final tiles are plain full tiles and the tail
@@ -512,7 +514,7 @@ __device__ __forceinline__ void load_tiles(const Task* __restrict__ tasks, u32 n
             }
             __syncwarp();
         }
-        const u64 my_leaf = cur.t.leaf0 + lane;
+        const u64 my_leaf = cur.t.seed0 + cur.t.leaf0 + lane;
         mm::W32 h1 = mm::w_of(my_leaf), h2 = h1;
         // The line stores of stage s also read stage s - 1 (pairs: s - 2 .. s),
         // so the ring slot refilled with stage s + kAhead is the one no store
@@ -627,7 +629,8 @@ __device__ __forceinline__ void load_tiles(const Task* __restrict__ tasks, u32 n
                 const std::uint8_t* sbytes = reinterpret_cast<const std::uint8_t*>(tb) + ga;
                 if (lane == cur.t.nfull && pl < cur.t.n) {
                     u64 d1, d2;
-                    leaf_digest_generic(sbytes + (pl - from), static_cast<u32>(cur.t.n - pl), pl / kLeafBytes, d1, d2);
+                    leaf_digest_generic(sbytes + (pl - from), static_cast<u32>(cur.t.n - pl),
+                                        cur.t.seed0 + pl / kLeafBytes, d1, d2);
                     acc_h += d1;
                     acc_l += d2;
                 }
@@ -678,6 +681,9 @@ __device__ __forceinline__ u64 globaltimer_ns() {
     return t;
 }
 
+__device__ __forceinline__ bool raw_sums(const FpTask&) { return false; }
+__device__ __forceinline__ bool raw_sums(const CopyFpTask& t) { return (t.leaf_base & kRawSums) != 0; }
+
 // The last warp's work, kept out of line: it runs once per launch and stays
 // out of the tile loop's code (A/B on one box against the inlined form and
 // against the kernel without stamps / clean-up: K1, move + fingerprint and
@@ -687,8 +693,15 @@ __device__ __noinline__ void finalize_tail(const Task* __restrict__ tasks, u32 n
                                            u64* __restrict__ digests, unsigned long long* done, u64* stamps,
                                            bool clean, unsigned long long* sync) {
     const u32 lane = threadIdx.x & 31;
-    for (u32 i = lane; i < n_tasks; i += 32)
-        digest_of(__ldcg(sums + 2 * i), __ldcg(sums + 2 * i + 1), tasks[i].n, digests + 2 * i);
+    for (u32 i = lane; i < n_tasks; i += 32) {
+        const u64 sh = __ldcg(sums + 2 * i), sl = __ldcg(sums + 2 * i + 1);
+        if (raw_sums(tasks[i])) {  // a piece of a tensor: the host adds the pieces
+            digests[2 * i] = sh;
+            digests[2 * i + 1] = sl;
+        } else {
+            digest_of(sh, sl, tasks[i].n, digests + 2 * i);
+        }
+    }
     if (clean) {       // every other warp is done with them: leave the stage zeroed for the next launch
         __syncwarp();  // (every lane has read its tasks' sums)
         u64* s = const_cast<u64*>(sums);
@@ -734,6 +747,11 @@ __global__ void copy_fp_finalize_kernel(const CopyFpTask* __restrict__ tasks, u3
                                         const u64* __restrict__ sums, u64* __restrict__ digests) {
     const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_tasks) return;
+    if (raw_sums(tasks[i])) {
+        digests[2 * i] = sums[2 * i];
+        digests[2 * i + 1] = sums[2 * i + 1];
+        return;
+    }
     u64 h1 = 0, h2 = 0;
     mm::body(h1, h2, sums[2 * i], sums[2 * i + 1]);
     mm::finish(h1, h2, tasks[i].n, 0, 8, 24);

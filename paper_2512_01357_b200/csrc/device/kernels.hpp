@@ -47,7 +47,13 @@ struct CopyFpTask {
     std::uint64_t tile0;  // tile prefix (32 leaves per tile), relative to the launch
     std::int32_t gate;    // wave that must be complete before this task writes (-1: none)
     std::int32_t wave;    // wave this task belongs to (its tiles count towards need[wave]; -1: none)
+    // Leaf index of byte 0 within its tensor (the murmur seed of leaf i is
+    // leaf_base + i): a task may be a leaf-aligned piece of a tensor.  With
+    // kRawSums set, the launch writes the task's raw (ΣH, ΣL) instead of a
+    // digest; the host adds the pieces of one tensor and takes the root.
+    std::uint64_t leaf_base = 0;
 };
+constexpr std::uint64_t kRawSums = std::uint64_t{1} << 63;
 // sync: 2 + n_waves u64 of device scratch — tile dispenser, the finished
 // tiles of each wave, finished CTAs — (zeroed by the launch unless
 // sync_zeroed); need[w] = tiles of wave w's tasks.  sums: 2 u64 per task

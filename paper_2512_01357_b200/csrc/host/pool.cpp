@@ -18,6 +18,7 @@
 #include "../device/common.cuh"
 #include "../device/kernels.hpp"
 #include "index.hpp"
+#include "murmur_mix.hpp"
 
 namespace tg {
 
@@ -685,8 +686,16 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // (re-shard pulls, kind 3, are assembled from several pieces: K1 after the last lands)
     // (bytes pulled from a peer — kinds 1 and 3 — are always fingerprinted:
     // that check is what makes a stale peer index safe)
+    // Re-shard pulls into free space (no wave gate) are assembled by the load
+    // kernel itself: each piece's leaf-aligned interior is a copy task hashed
+    // from its own read (seeds from the piece's leaf index, raw sums added on
+    // the host), and the few leaves that straddle a piece boundary are
+    // pre-copied by K3 and verified in place — two HBM passes instead of
+    // three (K3 pieces, then K1 over the assembled tensor).
+    auto fuse_reshard = [&](std::size_t i) { return fused && rep->placement_src[i] == 3 && dep[i] < 0; };
     auto k1_placement = [&](std::size_t i) {
         const std::uint8_t k = rep->placement_src[i];
+        if (k == 3 && fuse_reshard(i)) return false;
         return (fp_new || k == 1 || k == 3) && (!fused || k == 0 || k == 3);
     };
     auto tiles_of = [](u64 n) { return ((n + kLeafBytes - 1) / kLeafBytes + kLeavesPerTile - 1) / kLeavesPerTile; };
@@ -730,12 +739,46 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         ctask_of_still(hit_keys.size(), kNone);
     std::vector<u64> need(waves, 0);
     u64 ctiles = 0;
+    std::vector<std::vector<std::size_t>> ctasks_of_reshard(np);  // fused re-shard: its piece / straddle tasks
+    std::vector<MoveDesc> reshard_pre;                            // straddle fragments, K3 before the kernel
     if (fused) {
-        auto push = [&](const std::uint8_t* from, std::uint8_t* to, u64 n, int gate, int wave) {
-            ctasks.push_back(CopyFpTask{from, to, n, ctiles, gate, wave});
+        auto push = [&](const std::uint8_t* from, std::uint8_t* to, u64 n, int gate, int wave, u64 leaf_base = 0) {
+            ctasks.push_back(CopyFpTask{from, to, n, ctiles, gate, wave, leaf_base});
             ctiles += tiles_of(n);
             if (wave >= 0) need[static_cast<std::size_t>(wave)] += tiles_of(n);
         };
+        auto push_reshard = [&](std::size_t i) {
+            std::uint8_t* dst = arena_ + D.plan.placements[i].off;
+            const u64 n = D.miss_desc[D.plan.placements[i].tensor].size;
+            std::vector<u64> straddle;  // leaves touched by a fragment
+            auto fragment = [&](const std::uint8_t* from, u64 a, u64 b) {
+                if (a >= b) return;
+                reshard_pre.push_back(MoveDesc{reinterpret_cast<u64>(from), reinterpret_cast<u64>(dst + a), b - a});
+                for (u64 l = a / kLeafBytes; l * kLeafBytes < b; ++l) straddle.push_back(l);
+            };
+            for (const MoveDesc& pc : pieces[i]) {  // pc: src pointer, offset in the tensor, length
+                const auto* src = reinterpret_cast<const std::uint8_t*>(pc.src);
+                const u64 a = pc.dst, b = pc.dst + pc.len;
+                const u64 A = (a + kLeafBytes - 1) / kLeafBytes * kLeafBytes;
+                const u64 B = b == n ? n : b / kLeafBytes * kLeafBytes;
+                if (A < B) {
+                    ctasks_of_reshard[i].push_back(ctasks.size());
+                    push(src + (A - a), dst + A, B - A, -1, -1, (A / kLeafBytes) | kRawSums);
+                    fragment(src, a, A);
+                    fragment(src + (B - a), B, b);
+                } else {
+                    fragment(src, a, b);
+                }
+            }
+            std::sort(straddle.begin(), straddle.end());
+            straddle.erase(std::unique(straddle.begin(), straddle.end()), straddle.end());
+            for (u64 l : straddle) {
+                ctasks_of_reshard[i].push_back(ctasks.size());
+                push(dst + l * kLeafBytes, nullptr, std::min<u64>(kLeafBytes, n - l * kLeafBytes), -1, -1, l | kRawSums);
+            }
+        };
+        for (std::size_t i = 0; i < np; ++i)
+            if (fuse_reshard(i)) push_reshard(i);
         static const u64 rounds = [] {
             const char* e = std::getenv("TANGRAM_VERIFY_ROUNDS");  // A/B knob
             return e ? std::strtoull(e, nullptr, 10) : 8ull;
@@ -788,7 +831,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // keeps the tile loop leaner (K1 6.36-6.46 TB/s vs 6.31-6.34 for the
     // verification tasks of a writing launch, misaligned, same box).
     bool verify_only = fused && nc && waves == 0;
-    for (const CopyFpTask& t : ctasks) verify_only = verify_only && t.dst == nullptr;
+    for (const CopyFpTask& t : ctasks) verify_only = verify_only && t.dst == nullptr && t.leaf_base == 0;
     if (verify_only) {
         auto* ft = reinterpret_cast<FpTask*>(h + fdesc);
         for (std::size_t k = 0; k < nc; ++k) ft[k] = FpTask{ctasks[k].src, ctasks[k].n, ctasks[k].tile0};
@@ -815,7 +858,8 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     bool copy_used = false, peer_used = false, fp_used = false;
     for (std::size_t i = 0; i < np; ++i) {
         copy_used = copy_used || rep->placement_src[i] == 0;
-        peer_used = peer_used || rep->placement_src[i] == 3 || (rep->placement_src[i] != 0 && !fused);
+        peer_used = peer_used || (rep->placement_src[i] == 3 && !fuse_reshard(i)) ||
+                    (rep->placement_src[i] != 0 && !fused);
         fp_used = fp_used || fp_of_placement[i] != kNone;
     }
     const bool lone = fused && ctiles && !copy_used && !peer_used && !fp_used && !split;
@@ -836,6 +880,10 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // ---- device work on the main stream: the load kernel (fused) or the K3
     // relocation waves (unfused) ----------------------------------------------------
     if (!lone) TG_CUDA(cudaEventRecord(ev(1), s_main_));
+    if (fused && !reshard_pre.empty()) {  // straddle leaves of fused re-shard pulls, verified by the kernel
+        relocate_launch(reshard_pre.data(), static_cast<int>(reshard_pre.size()), sm_count_, s_main_);
+        TG_CUDA(cudaGetLastError());
+    }
     if (fused) {
         if (verify_only)
             fp_launch(reinterpret_cast<const FpTask*>(d_ctasks), static_cast<u32>(nc), ctiles, d_sums + 2 * nf,
@@ -901,7 +949,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         const auto& pl = D.plan.placements[i];
         const u64 sz = D.miss_desc[pl.tensor].size;
         if (rep->placement_src[i] == 0) continue;
-        if (rep->placement_src[i] != 3 && fused) continue;  // in the load kernel
+        if (fused && (rep->placement_src[i] != 3 || fuse_reshard(i))) continue;  // in the load kernel
         if (dep[i] > waited_peer) {
             gate(s_peer_, zeroed_peer, dep[i]);
             waited_peer = dep[i];
@@ -1065,7 +1113,8 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // ---- completion: wait for the data plane, then record / verify digests.
     // Runs now, or — with kLoadAsync — before the next operation on this pool
     // (complete_pending), so loads on different pools overlap.
-    auto finish = [this, h_dig, h_stamps, ctiles, lone, split, np, nf, fused, copy_used, peer_used, hit_base, n_still, fp_reuse, waves, nc, gate_recorded, ev_gate, ev_fp,
+    auto finish = [this, h_dig, h_stamps, ctiles, lone, split, np, nf, fused,
+                   ctasks_of_reshard = std::move(ctasks_of_reshard), copy_used, peer_used, hit_base, n_still, fp_reuse, waves, nc, gate_recorded, ev_gate, ev_fp,
                    fp_i, fp_reuse_slot, fp_reuse_launches, h0, h_issued, fp_of_placement = std::move(fp_of_placement),
                    ctask_of_placement = std::move(ctask_of_placement), has_truth = std::move(has_truth),
                    truth = std::move(truth), hit_keys = std::move(hit_keys), hit_pos = std::move(hit_pos),
@@ -1150,11 +1199,26 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         std::size_t slot = kNone;
         if (fp_of_placement[i] != kNone) slot = fp_of_placement[i];
         else if (ctask_of_placement[i] != kNone) slot = nf + ctask_of_placement[i];
-        if (slot == kNone) {  // landed (the streams are joined), not fingerprinted by request
+        const bool pieces_fused = rep->placement_src[i] == 3 && fused && ctask_of_placement[i] == kNone &&
+                                  fp_of_placement[i] == kNone;
+        if (slot == kNone && !pieces_fused) {  // landed (the streams are joined), not fingerprinted by request
             e->suspect = false;
             continue;
         }
-        const Digest g = digest_at(slot);
+        Digest g;
+        if (pieces_fused) {  // tgfp1 root of the summed raw leaf sums of the pieces and straddle leaves
+            u64 sh = 0, sl = 0;
+            for (std::size_t k : ctasks_of_reshard[i]) {
+                sh += h_dig[2 * (nf + k)];
+                sl += h_dig[2 * (nf + k) + 1];
+            }
+            u64 h1 = 0, h2 = 0;
+            mm::body(h1, h2, sh, sl);
+            mm::finish(h1, h2, t.size, 0, 8, 24);
+            g = Digest{h1, h2};
+        } else {
+            g = digest_at(slot);
+        }
         rep->digests[at] = g;
         rep->fingerprint_bytes += t.size;
         if (!has_truth[i]) {
@@ -1190,13 +1254,18 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             for (std::size_t j = 0; j < rel.size(); ++j) verified[j] |= rel[j].tensor == k;
         rep->digests[hit_pos[hix]] = g;
         rep->fingerprint_bytes += e->size;
+        // Whether the tensor was trustworthy before this load: a relocated one
+        // is marked suspect by this load until its move is verified, so its
+        // state from before the move is what counts.
+        const bool was_suspect = hit_rel[hix] != kNone ? prior_suspect[hit_rel[hix]] != 0 : e->suspect;
         if (e->has_digest && e->digest == g) {
             e->suspect = false;
-        } else if (!e->has_digest && !e->suspect) {
+        } else if (!e->has_digest && !was_suspect) {
             // Placed without a fingerprint (kLoadFingerprintNew off) by a load
             // that completed: the first verification records the truth.
             e->digest = g;
             e->has_digest = true;
+            e->suspect = false;
         } else {
             // Content drifted (the key says "reuse", the bytes disagree), or a
             // failed load left it unverifiable: re-send it in place from its

@@ -122,3 +122,48 @@ def test_reshard_from_own_pool(tg, cpu, ref):
         assert c.dump() == r_pool.dump()
         t += 1.0
     c.close()
+
+
+@pytest.mark.parametrize("src_tp,dst_tp", [(3, 2), (3, 5), (5, 3), (7, 2)])
+@pytest.mark.parametrize("fused", [False, True], ids=["K3+K1", "fused"])
+def test_reshard_piece_boundaries_inside_leaves(tg, cpu, ref, src_tp, dst_tp, fused):
+    """Layouts whose shard boundaries fall inside 4 KiB leaves of the target
+    shards (odd tensor sizes; tiny tensors whose pieces are shorter than a
+    leaf).  Fused, every piece's leaf-aligned interior is copied and hashed by
+    the load kernel with seeds from its leaf index, the straddling leaves are
+    pre-copied and verified in place, and the host adds the raw sums: the
+    digest equals the CPU restatement of the parent range, as on the K3 + K1
+    path, and the decisions equal the reference's."""
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    m = tg.make_model(f"rs-{src_tp}-{dst_tp}", 30_000_037, 2, 8192)
+    tiny = tg.make_model(f"rs-tiny-{src_tp}-{dst_tp}", 12_289, 1, 0)  # shards of a few KiB
+    srcs = [tg.shard_model(x, r, src_tp) for x in (m, tiny) for r in range(src_tp)]
+    dsts = [tg.shard_model(x, r, dst_tp) for x in (m, tiny) for r in range(dst_tp)]
+    holder = tg.ReuseStore(tg.GpuSpec("gpu0", 64_000_000), device=0)
+    with HostCheckpoint(srcs):
+        st = tg.ModelStatsTable()
+        for k, sm in enumerate(srcs):
+            st.record_request(sm.model_id, float(k))
+            holder.load_model(sm, st, float(k)).value()
+            holder.end_instance(sm.model_id)
+    c = tg.ReuseStore(tg.GpuSpec("gpu1", 64_000_000), device=0)
+    c.add_peer(holder)
+    sc = tg.ModelStatsTable()
+    r_pool, r_stats = ref.ReuseStore(64_000_000, gpu_id="gpu1"), ref.ModelStatsTable()
+    try:
+        for k, shard in enumerate(dsts):
+            sc.record_request(shard.model_id, float(k))
+            o = c.load_model(shard, sc, float(k), tg.LoadPolicy(flags=1 | 2 | 4 | (8 if fused else 0))).value()
+            assert o.peer_bytes == shard.total_size and o.pcie_bytes == 0 and o.verify_mismatches == 0
+            for i, t in enumerate(shard.tensors):
+                want = _expected(cpu, tg, t)
+                assert o.digests[i] == want, (shard.model_id, t.name)
+                assert c.fingerprint_tensor(t.id) == want, (shard.model_id, t.name)
+            c.end_instance(shard.model_id)
+            r_stats.record_request(shard.model_id, float(k))
+            r_pool.load_model(shard.to_json(), r_stats, float(k))
+            r_pool.end_instance(shard.model_id)
+            assert c.dump() == r_pool.dump()
+    finally:
+        c.close()
+        holder.close()
