@@ -466,7 +466,13 @@ struct CopyCfg {
 };
 using CfgSingle = CopyCfg<4, 6, false>;
 using CfgPair = CopyCfg<4, 6, true>;
-using CfgFpNext = CopyCfg<4, 6, false, true>;
+// K1 (fingerprint-only launches): three slots and eight warps per CTA — the
+// shared memory of four slots x six warps, 16 instead of 12 resident warps
+// per SM (A/B on one box: K1 8 GiB misaligned +1.7 %, warm reloads of
+// opt1.3B / qwen3B / opt13B 1.5-2 % faster).  TANGRAM_K1_RING=4x6 selects
+// the four-slot ring for A/B runs.
+using CfgFpNext = CopyCfg<3, 8, false, true>;
+using CfgFpNext46 = CopyCfg<4, 6, false, true>;
 
 template <class Task, class Cfg>
 __device__ __forceinline__ void load_tiles(const Task* __restrict__ tasks, u32 n_tasks, u64 total_tiles,
@@ -822,7 +828,14 @@ template <class Task>
 void load_kernel_launch(const Task* d_tasks, u32 n_tasks, u64 total_tiles, u64* d_sums, u64* d_digests, u64* d_sync,
                         const u64* d_need, u32 n_waves, int sm_count, cudaStream_t s, bool sync_zeroed,
                         bool writes, u64* stamps = nullptr, bool clean = false) {
-    if (!writes && !(std::getenv("TANGRAM_FP_NEXT") && std::strcmp(std::getenv("TANGRAM_FP_NEXT"), "0") == 0))
+    static const bool ring46 = [] {
+        const char* e = std::getenv("TANGRAM_K1_RING");
+        return e && std::strcmp(e, "4x6") == 0;
+    }();
+    if (!writes && ring46)
+        load_kernel_launch_cfg<Task, CfgFpNext46>(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, d_need, n_waves,
+                                                  sm_count, s, sync_zeroed, stamps, clean);
+    else if (!writes && !(std::getenv("TANGRAM_FP_NEXT") && std::strcmp(std::getenv("TANGRAM_FP_NEXT"), "0") == 0))
         load_kernel_launch_cfg<Task, CfgFpNext>(d_tasks, n_tasks, total_tiles, d_sums, d_digests, d_sync, d_need, n_waves,
                                                 sm_count, s, sync_zeroed, stamps, clean);
     else if (writes && pair_ring())

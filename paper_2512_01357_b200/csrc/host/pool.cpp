@@ -656,6 +656,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // launch after the waves.  hit_keys is reordered [untouched..., relocated...].
     // (tens of tensors and relocations per load: linear scans, no hashing)
     constexpr std::size_t kNone = ~std::size_t{0};
+    constexpr std::size_t kPostTask = std::size_t{1} << 62;  // provisional index of a post-kernel task
     auto reloc_index = [&](const Key& k) {
         for (std::size_t j = 0; j < rel.size(); ++j)
             if (rel[j].tensor == k) return j;
@@ -691,8 +692,12 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // from its own read (seeds from the piece's leaf index, raw sums added on
     // the host), and the few leaves that straddle a piece boundary are
     // pre-copied by K3 and verified in place — two HBM passes instead of
-    // three (K3 pieces, then K1 over the assembled tensor).
-    auto fuse_reshard = [&](std::size_t i) { return fused && rep->placement_src[i] == 3 && dep[i] < 0; };
+    // three (K3 pieces, then K1 over the assembled tensor).  A pull into bytes
+    // a relocation wave has yet to read takes the wave's gate for its piece
+    // tasks and copies its straddle fragments inside the load kernel too (a
+    // K3 pre-copy would overwrite them before the wave); its straddle leaves
+    // are then verified by a second, small launch after the load kernel.
+    auto fuse_reshard = [&](std::size_t i) { return fused && rep->placement_src[i] == 3; };
     auto k1_placement = [&](std::size_t i) {
         const std::uint8_t k = rep->placement_src[i];
         if (k == 3 && fuse_reshard(i)) return false;
@@ -741,6 +746,8 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     u64 ctiles = 0;
     std::vector<std::vector<std::size_t>> ctasks_of_reshard(np);  // fused re-shard: its piece / straddle tasks
     std::vector<MoveDesc> reshard_pre;                            // straddle fragments, K3 before the kernel
+    std::vector<CopyFpTask> post;  // straddle leaves of gated re-shard pulls: verified after the load kernel
+    u64 post_tiles = 0;
     if (fused) {
         auto push = [&](const std::uint8_t* from, std::uint8_t* to, u64 n, int gate, int wave, u64 leaf_base = 0) {
             ctasks.push_back(CopyFpTask{from, to, n, ctiles, gate, wave, leaf_base});
@@ -750,10 +757,12 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         auto push_reshard = [&](std::size_t i) {
             std::uint8_t* dst = arena_ + D.plan.placements[i].off;
             const u64 n = D.miss_desc[D.plan.placements[i].tensor].size;
+            const int gate = dep[i];  // >= 0: the wave whose reads this pull must follow
             std::vector<u64> straddle;  // leaves touched by a fragment
             auto fragment = [&](const std::uint8_t* from, u64 a, u64 b) {
                 if (a >= b) return;
-                reshard_pre.push_back(MoveDesc{reinterpret_cast<u64>(from), reinterpret_cast<u64>(dst + a), b - a});
+                if (gate < 0) reshard_pre.push_back(MoveDesc{reinterpret_cast<u64>(from), reinterpret_cast<u64>(dst + a), b - a});
+                else push(from, dst + a, b - a, gate, -1);  // copied in the kernel after the wave (sums unused)
                 for (u64 l = a / kLeafBytes; l * kLeafBytes < b; ++l) straddle.push_back(l);
             };
             for (const MoveDesc& pc : pieces[i]) {  // pc: src pointer, offset in the tensor, length
@@ -763,7 +772,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
                 const u64 B = b == n ? n : b / kLeafBytes * kLeafBytes;
                 if (A < B) {
                     ctasks_of_reshard[i].push_back(ctasks.size());
-                    push(src + (A - a), dst + A, B - A, -1, -1, (A / kLeafBytes) | kRawSums);
+                    push(src + (A - a), dst + A, B - A, gate, -1, (A / kLeafBytes) | kRawSums);
                     fragment(src, a, A);
                     fragment(src + (B - a), B, b);
                 } else {
@@ -773,12 +782,19 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             std::sort(straddle.begin(), straddle.end());
             straddle.erase(std::unique(straddle.begin(), straddle.end()), straddle.end());
             for (u64 l : straddle) {
+                const u64 len = std::min<u64>(kLeafBytes, n - l * kLeafBytes);
+                if (gate >= 0) {  // index in ctasks once `post` is appended behind the load kernel's tasks
+                    ctasks_of_reshard[i].push_back(kPostTask + post.size());
+                    post.push_back(CopyFpTask{dst + l * kLeafBytes, nullptr, len, post_tiles, -1, -1, l | kRawSums});
+                    post_tiles += tiles_of(len);
+                    continue;
+                }
                 ctasks_of_reshard[i].push_back(ctasks.size());
-                push(dst + l * kLeafBytes, nullptr, std::min<u64>(kLeafBytes, n - l * kLeafBytes), -1, -1, l | kRawSums);
+                push(dst + l * kLeafBytes, nullptr, len, -1, -1, l | kRawSums);
             }
         };
         for (std::size_t i = 0; i < np; ++i)
-            if (fuse_reshard(i)) push_reshard(i);
+            if (fuse_reshard(i) && dep[i] < 0) push_reshard(i);
         static const u64 rounds = [] {
             const char* e = std::getenv("TANGRAM_VERIFY_ROUNDS");  // A/B knob
             return e ? std::strtoull(e, nullptr, 10) : 8ull;
@@ -794,7 +810,11 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
                 push(arena_ + rel[j].from, arena_ + rel[j].to, rel[j].size, gate, static_cast<int>(g));
             }
             for (std::size_t i = 0; i < np; ++i) {
-                if (rep->placement_src[i] == 0 || rep->placement_src[i] == 3 || dep[i] != gate) continue;
+                if (rep->placement_src[i] == 0 || dep[i] != gate || (gate < 0 && rep->placement_src[i] == 3)) continue;
+                if (rep->placement_src[i] == 3) {  // gated re-shard pull: its pieces follow the wave
+                    push_reshard(i);
+                    continue;
+                }
                 ctask_of_placement[i] = ctasks.size();
                 push(peer_src[i], arena_ + D.plan.placements[i].off, D.miss_desc[D.plan.placements[i].tensor].size,
                      gate, -1);
@@ -807,8 +827,15 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             }
         }
     }
+    // the post-kernel straddle verifications go behind the load kernel's tasks
+    // (their tile numbers restart at 0: a launch of their own)
+    const std::size_t nc_main = ctasks.size();
+    for (auto& v : ctasks_of_reshard)
+        for (std::size_t& k : v)
+            if (k >= kPostTask) k = nc_main + (k - kPostTask);
+    ctasks.insert(ctasks.end(), post.begin(), post.end());
     const std::size_t nf = tasks.size(), nc = ctasks.size();
-    std::size_t n_fp_launch = 2;
+    std::size_t n_fp_launch = 2 + (post.empty() ? 0 : 1);
     for (std::size_t i = 0; i < np; ++i) n_fp_launch += fp_of_placement[i] != kNone;
     const std::size_t ev_gate = ev_fp + 2 * n_fp_launch;  // copy stream: first gated H2D may start
     ensure_events(ev_gate + 1);
@@ -862,7 +889,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
                     (rep->placement_src[i] != 0 && !fused);
         fp_used = fp_used || fp_of_placement[i] != kNone;
     }
-    const bool lone = fused && ctiles && !copy_used && !peer_used && !fp_used && !split;
+    const bool lone = fused && ctiles && !copy_used && !peer_used && !fp_used && !split && post.empty();
     // Resident descriptors: a lone load kernel leaves its sums and counters
     // zeroed (it cleans up after its digests), so a load whose descriptors
     // equal the ones already on the device (a reload of an unchanged model)
@@ -889,12 +916,18 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             fp_launch(reinterpret_cast<const FpTask*>(d_ctasks), static_cast<u32>(nc), ctiles, d_sums + 2 * nf,
                       d_dig + 2 * nf, d_sync, sm_count_, s_main_, /*sync_zeroed=*/true, d_stamps, /*clean=*/lone);
         else
-            copy_fp_launch(d_ctasks, static_cast<u32>(nc), ctiles, d_sums + 2 * nf, d_dig + 2 * nf, d_sync, d_need,
+            copy_fp_launch(d_ctasks, static_cast<u32>(nc_main), ctiles, d_sums + 2 * nf, d_dig + 2 * nf, d_sync, d_need,
                            waves, sm_count_, s_main_, /*sync_zeroed=*/true, d_stamps, /*clean=*/lone);
         TG_CUDA(cudaGetLastError());
         for (u32 w = 0; w < waves; ++w) TG_CUDA(cudaEventRecord(ev(ev_wave + w), s_main_));
         for (std::size_t i = 0; i < np; ++i)
             if (ctask_of_placement[i] != kNone) TG_CUDA(cudaEventRecord(ev(ev_land + i), s_main_));
+        if (!post.empty()) {  // straddle leaves of gated re-shard pulls, written by the load kernel above
+            copy_fp_launch(d_ctasks + nc_main, static_cast<u32>(post.size()), post_tiles, d_sums + 2 * (nf + nc_main),
+                           d_dig + 2 * (nf + nc_main), d_fp_sync + 2 * (n_fp_launch - 1), nullptr, 0, sm_count_, s_main_,
+                           /*sync_zeroed=*/true, nullptr, /*clean=*/false);
+            TG_CUDA(cudaGetLastError());
+        }
     }
     for (u32 w = 0; !fused && w < waves; ++w) {
         std::vector<MoveDesc> mv;

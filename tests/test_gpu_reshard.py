@@ -167,3 +167,89 @@ def test_reshard_piece_boundaries_inside_leaves(tg, cpu, ref, src_tp, dst_tp, fu
     finally:
         c.close()
         holder.close()
+
+
+def _gated_pulls(o):
+    """Placements of re-shard pulls (source 3) whose destination overlaps the
+    source range of one of the load's relocations: bytes a WAR wave must read
+    before the pull may write them."""
+    rel = o.plan.relocations
+    return [p for p in o.plan.placements if p.source == 3 and
+            any(p.offset < r.from_ + r.size and r.from_ < p.offset + p.size for r in rel)]
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["K3+K1", "fused"])
+def test_reshard_pulls_gated_on_relocation_waves(tg, cpu, ref, fused):
+    """Re-shard pulls into space a relocation wave of the same load vacates.
+    A pool switching among TP4 shards of one model (assembled from TP2 peers,
+    no host source) and three host-sourced models, under every merge policy,
+    with random tensor evictions: fused, a gated pull's piece tasks and
+    straddle fragments wait for the wave inside the load kernel and its
+    straddle leaves are verified by a second launch behind it.  Decisions and
+    dumps equal the reference's op by op; every resident tensor fingerprints
+    equal to the CPU restatement; the sequence provably exercises gated
+    pulls."""
+    import random
+    from paper_2512_01357_b200.checkpoint import HostCheckpoint
+    base = tg.make_model("gr", 30_000_037, 3, 8192)
+    tp2 = [tg.shard_model(base, r, 2) for r in range(2)]
+    tp4 = [tg.shard_model(base, r, 4) for r in range(4)]
+    others = [tg.make_model(f"o{i}", 9_000_000 + i * 1_000_003, 2, 4096) for i in range(3)]
+    holder = tg.ReuseStore(tg.GpuSpec("peer", 64_000_000), device=0)
+    with HostCheckpoint(tp2):
+        st = tg.ModelStatsTable()
+        for k, sm in enumerate(tp2):
+            st.record_request(sm.model_id, float(k))
+            holder.load_model(sm, st, float(k)).value()
+            holder.end_instance(sm.model_id)
+    expected = {}
+
+    def want(tid, size):
+        if tid not in expected:
+            lin = tg.lineage(tid)
+            data = cpu.synth(lin[0].hi, lin[0].lo, size, lin[1]) if lin else cpu.synth(tid.hi, tid.lo, size)
+            expected[tid] = cpu.content_fingerprint(data, threads=8)[0]
+        return expected[tid]
+
+    gated = 0
+    flags = 1 | 2 | 4 | (8 if fused else 0)
+    try:
+        with HostCheckpoint(others):
+            for seed in range(6):
+                rnd = random.Random(seed)
+                size = rnd.choice([24_000_000, 28_000_000, 32_000_000])
+                c = tg.ReuseStore(tg.GpuSpec("gpu1", size), device=0)
+                c.add_peer(holder)
+                r_pool, r_stats, sc = ref.ReuseStore(size, gpu_id="gpu1"), ref.ModelStatsTable(), tg.ModelStatsTable()
+                try:
+                    for k in range(14):
+                        t = float(k + 1)
+                        m = rnd.choice(tp4[:2] + others)
+                        merge = rnd.choice([0, 1])
+                        sc.record_request(m.model_id, t)
+                        r_stats.record_request(m.model_id, t)
+                        r = c.load_model(m, sc, t, tg.LoadPolicy(merge=tg.MergePolicy(merge), flags=flags))
+                        rr = r_pool.load_model(m.to_json(), r_stats, t, merge=merge)
+                        assert r.ok() == rr["ok"], (seed, k)
+                        if r.ok():
+                            o = r.value()
+                            assert o.verify_mismatches == 0 and o.pcie_bytes + o.peer_bytes + o.device_src_bytes \
+                                == o.bytes_transferred
+                            gated += len(_gated_pulls(o))
+                            for i, tt in enumerate(m.tensors):
+                                assert o.digests[i] == want(tt.id, tt.size), (seed, k, tt.name)
+                            c.end_instance(m.model_id)
+                            r_pool.end_instance(m.model_id)
+                        if rnd.random() < 0.4 and c.dump()["tensor_map"]:
+                            e = rnd.choice(c.dump()["tensor_map"])
+                            c.evict_tensor(tg.TensorId.from_hex(e["tensor"]))
+                            r_pool.evict_tensor(e["tensor"])
+                        assert c.dump() == r_pool.dump(), (seed, k)
+                        for e in c.dump()["tensor_map"]:
+                            tid = tg.TensorId.from_hex(e["tensor"])
+                            assert c.fingerprint_tensor(tid) == want(tid, e["size"]), (seed, k, e)
+                finally:
+                    c.close()
+    finally:
+        holder.close()
+    assert gated > 0
