@@ -259,12 +259,21 @@ void FileStager::stage(const std::string& path, u64 off, u64 size, std::uint8_t*
     end();
 }
 
-bool verify_split() {
-    static const bool on = [] {
+// A load kernel with writing tasks and at most kSplitMaxWaves relocation
+// waves leaves the in-place verification of the untouched hits to a K1
+// launch on the verify stream.  The K1 CTAs take the SM slots the load
+// kernel's CTAs release, so the verification runs on K1's own (faster) ring
+// and fills the load kernel's tail.  With more serial waves the gate waits
+// dominate, and verification tiles inside the load kernel fill them better
+// (same-box A/B: C2, 3 waves, split 1-2.6 % faster; C2 under GlobalMerge,
+// 11 waves, split 3-4 % slower).  TANGRAM_VERIFY_SPLIT=0 / =1 forces either.
+constexpr unsigned kSplitMaxWaves = 3;
+bool verify_split(unsigned waves) {
+    static const int mode = [] {
         const char* e = std::getenv("TANGRAM_VERIFY_SPLIT");
-        return e && std::strcmp(e, "1") == 0;
+        return !e ? -1 : std::strcmp(e, "0") == 0 ? 0 : 1;
     }();
-    return on;
+    return mode < 0 ? waves <= kSplitMaxWaves : mode == 1;
 }
 
 // 8 MiB chunks, a 256 MiB ring, 3/4 of the host threads reading (4..16;
@@ -725,9 +734,12 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     }
     const std::size_t hit_base = tasks.size();
     u64 still_tiles = 0, moved_tiles = 0;
-    // A/B (TANGRAM_VERIFY_SPLIT=1): a fused load verifies its untouched hits
-    // in a concurrent K1 launch instead of inside the load kernel.
-    const bool split = fused && fp_reuse && verify_split();
+    // A fused load whose load kernel writes verifies its untouched hits in a
+    // concurrent K1 launch (verify_split); a load kernel that would only
+    // verify (a warm reload) stays one lone launch.
+    bool kernel_writes = !rel.empty();
+    for (std::size_t i = 0; i < np; ++i) kernel_writes = kernel_writes || rep->placement_src[i] != 0;
+    const bool split = fused && fp_reuse && kernel_writes && n_still > 0 && verify_split(waves);
     if (fp_reuse && (!fused || split)) {
         std::vector<FpTask> still, moved_hits;
         for (std::size_t h = 0; h < (split ? n_still : hit_keys.size()); ++h) {
@@ -877,7 +889,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     const std::size_t stamp_off = desc_bytes + 2 * sums_bytes + sync_bytes;
     auto* h_stamps = reinterpret_cast<u64*>(h + stamp_off);
     auto* d_stamps = reinterpret_cast<u64*>(static_cast<std::uint8_t*>(h_stage_dev_) + stamp_off);
-    h_stamps[0] = h_stamps[1] = 0;
+    h_stamps[0] = h_stamps[1] = h_stamps[2] = h_stamps[3] = 0;  // load kernel, split K1
     // Side streams join only when they carry work: a load with neither host
     // nor peer-stream placements (a warm reload) is the load kernel alone on
     // the pool stream, with no cross-stream dependency to resolve at its end
@@ -1104,7 +1116,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             if (!count) return;
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i), s));
             fp_launch(d_tasks + first, static_cast<u32>(count), tiles, d_sums + 2 * first, d_dig + 2 * first,
-                      d_fp_sync + 2 * fp_i, sm_count_, s, /*sync_zeroed=*/true);
+                      d_fp_sync + 2 * fp_i, sm_count_, s, /*sync_zeroed=*/true, split ? d_stamps + 2 : nullptr);
             TG_CUDA(cudaGetLastError());
             TG_CUDA(cudaEventRecord(ev(ev_fp + 2 * fp_i + 1), s));
             ++fp_i;
@@ -1175,9 +1187,16 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // from its own globaltimer stamps, and a load that is that kernel alone
     // on the pool stream ends with it)
     rep->t.total_ms = ms_between(ev(0), ev(3));
-    const bool stamped = fused && ctiles && h_stamps[1] > h_stamps[0] && h_stamps[0];
-    // fused: the whole load kernel (waves, device-source placements, verification)
-    rep->t.relocate_ms = stamped ? (h_stamps[1] - h_stamps[0]) * 1e-6
+    bool stamped = fused && ctiles && h_stamps[1] > h_stamps[0] && h_stamps[0];
+    u64 t_start = h_stamps[0], t_end = h_stamps[1];
+    if (split && stamped) {  // and its concurrent verification launch (both stamped)
+        stamped = h_stamps[3] > h_stamps[2] && h_stamps[2];
+        t_start = std::min(t_start, h_stamps[2]);
+        t_end = std::max(t_end, h_stamps[3]);
+    }
+    // fused: the whole load kernel (waves, device-source placements,
+    // verification — split: up to the end of the concurrent K1)
+    rep->t.relocate_ms = stamped ? (t_end - t_start) * 1e-6
                                  : (!lone && (waves || (fused && nc))) ? ms_between(ev(1), ev(2)) : 0.0;
     rep->t.kernel_end_ms = lone ? rep->t.total_ms : ms_between(ev(0), ev(2));
     rep->t.gated_h2d_start_ms = gate_recorded ? ms_between(ev(0), ev(ev_gate)) : 0.0;

@@ -72,8 +72,9 @@ def _bytes(v):
 
 
 def traffic(rep, out_path, algo=None, source=None):
-    """DRAM traffic of the bench step's load-kernel launch against the step's
-    algorithmic bytes (printed by the same bench --profile run)."""
+    """DRAM traffic of the bench step's launches (load kernel + concurrent K1)
+    against the step's algorithmic bytes (printed by the same bench --profile
+    run)."""
     launches = summarise(rep)
     log = os.path.join(OUT, "prof_load.log")
     if algo is None and os.path.exists(log):
@@ -88,8 +89,10 @@ def traffic(rep, out_path, algo=None, source=None):
     with open(out_path, "w") as f:
         json.dump({"traffic_bytes_per_launch": t, "algorithmic_bytes": algo,
                    "ratio": t / algo if algo else None,
-                   "source": source or "ncu --set full --clock-control none of the bench step's load-kernel launch "
-                             "(bench.py --profile --steps 1 --warmup 0); dram__bytes_read.sum + dram__bytes_write.sum",
+                   "source": source or "ncu --set full --clock-control none of the bench step's launches (bench.py --profile "
+                             "--steps 1 --warmup 0): the load kernel and, since the verification split, the "
+                             "concurrent K1 launch verifying the untouched reused tensors (ncu serialises them); "
+                             "dram__bytes_read.sum + dram__bytes_write.sum summed over both",
                    "per_launch": per}, f, indent=1)
 
 

@@ -11,9 +11,11 @@ mkdir -p gpurun_out
 python tools/kernel_bench.py > gpurun_out/kernel_bench.json 2> gpurun_out/kernel_bench.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/launches_bench.log 2>&1
-# copy_fp_kernel launch order in bench --profile --steps 1 --warmup 0: one per
-# load — load #1 (0), load #2 (1), the measured step (2)
-ncu --set full --clock-control none --import-source on -k regex:copy_fp_kernel -s 2 -c 1 -o gpurun_out/prof_load -f \
+# copy_fp_kernel launch order in bench --profile --steps 1 --warmup 0: load #1
+# (0), load #2 (1) (no reused tensors: one load-kernel launch each), the
+# measured step: its load kernel (2) and the concurrent K1 launch verifying
+# the untouched reused tensors (3)
+ncu --set full --clock-control none --import-source on -k regex:copy_fp_kernel -s 2 -c 2 -o gpurun_out/prof_load -f \
     python bench.py --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/prof_load.log 2>&1
 # unfused A/B (the step only; loads #1, #2 keep the default): copy_fp_kernel
 # launches are load #1 (0), load #2 (1), the step's 13 K1 placements (2..14),
