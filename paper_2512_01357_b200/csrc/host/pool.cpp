@@ -276,6 +276,24 @@ bool verify_split(unsigned waves) {
     return mode < 0 ? waves <= kSplitMaxWaves : mode == 1;
 }
 
+bool split_candidate(bool fused, bool fp_reuse, bool kernel_writes, std::size_t n_still, unsigned waves) {
+    return fused && fp_reuse && kernel_writes && n_still > 0 && verify_split(waves);
+}
+
+// Resident-warp rounds of verification tiles behind each gate of the load
+// kernel (TANGRAM_VERIFY_ROUNDS; split loads: TANGRAM_SPLIT_ROUNDS).
+unsigned long long verify_rounds(bool split) {
+    static const unsigned long long in_kernel = [] {
+        const char* e = std::getenv("TANGRAM_VERIFY_ROUNDS");
+        return e ? std::strtoull(e, nullptr, 10) : 8ull;
+    }();
+    static const unsigned long long with_split = [] {
+        const char* e = std::getenv("TANGRAM_SPLIT_ROUNDS");
+        return e ? std::strtoull(e, nullptr, 10) : 0ull;
+    }();
+    return split ? with_split : in_kernel;
+}
+
 // 8 MiB chunks, a 256 MiB ring, 3/4 of the host threads reading (4..16;
 // TANGRAM_STAGER_THREADS overrides): page-cache preads run ~6 GB/s a thread,
 // so a dozen saturate the PCIe link.
@@ -739,10 +757,20 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // verify (a warm reload) stays one lone launch.
     bool kernel_writes = !rel.empty();
     for (std::size_t i = 0; i < np; ++i) kernel_writes = kernel_writes || rep->placement_src[i] != 0;
-    const bool split = fused && fp_reuse && kernel_writes && n_still > 0 && verify_split(waves);
+    // Verification tiles per gate inside the load kernel: `rounds` resident-
+    // warp rounds behind each wave's tasks (they fill the gate waits).  Split,
+    // the share behind the last group (the bulk) goes to the K1 launch
+    // instead: hits [0, k_in) are verified in the load kernel, [k_in, n_still)
+    // by K1.
+    const u64 share = (fused ? verify_rounds(split_candidate(fused, fp_reuse, kernel_writes, n_still, waves)) : 0) *
+                      copy_fp_resident_warps(sm_count_);
+    std::size_t k_in = 0;
+    for (u32 g = 0; g < waves && split_candidate(fused, fp_reuse, kernel_writes, n_still, waves); ++g)
+        for (u64 got = 0; k_in < n_still && got < share; ++k_in) got += tiles_of(store_.entry(hit_keys[k_in])->size);
+    const bool split = split_candidate(fused, fp_reuse, kernel_writes, n_still, waves) && k_in < n_still;
     if (fp_reuse && (!fused || split)) {
         std::vector<FpTask> still, moved_hits;
-        for (std::size_t h = 0; h < (split ? n_still : hit_keys.size()); ++h) {
+        for (std::size_t h = split ? k_in : 0; h < (split ? n_still : hit_keys.size()); ++h) {
             const Entry* e = store_.entry(hit_keys[h]);
             (h < n_still ? still : moved_hits).push_back(FpTask{arena_ + e->off, e->size, 0});
         }
@@ -807,12 +835,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
         };
         for (std::size_t i = 0; i < np; ++i)
             if (fuse_reshard(i) && dep[i] < 0) push_reshard(i);
-        static const u64 rounds = [] {
-            const char* e = std::getenv("TANGRAM_VERIFY_ROUNDS");  // A/B knob
-            return e ? std::strtoull(e, nullptr, 10) : 8ull;
-        }();
-        const u64 share = rounds * copy_fp_resident_warps(sm_count_);
-        const std::size_t n_verify = fp_reuse && !split ? n_still : 0;
+        const std::size_t n_verify = fp_reuse ? (split ? k_in : n_still) : 0;
         std::size_t next_verify = 0;
         for (u32 g = 0; g <= waves; ++g) {
             const int gate = static_cast<int>(g) - 1;
@@ -1123,7 +1146,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
             ++fp_reuse_launches;
         };
         TG_CUDA(cudaStreamWaitEvent(s_verify_, ev(1)));
-        launch(s_verify_, hit_base, n_still, still_tiles);
+        launch(s_verify_, hit_base, split ? n_still - k_in : n_still, still_tiles);
         if (!fused) launch(s_main_, hit_base + n_still, hit_keys.size() - n_still, moved_tiles);
         TG_CUDA(cudaEventRecord(ev(8), s_verify_));
         TG_CUDA(cudaStreamWaitEvent(s_main_, ev(8)));
@@ -1158,7 +1181,7 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     // ---- completion: wait for the data plane, then record / verify digests.
     // Runs now, or — with kLoadAsync — before the next operation on this pool
     // (complete_pending), so loads on different pools overlap.
-    auto finish = [this, h_dig, h_stamps, ctiles, lone, split, np, nf, fused,
+    auto finish = [this, h_dig, h_stamps, ctiles, lone, split, k_in, np, nf, fused,
                    ctasks_of_reshard = std::move(ctasks_of_reshard), copy_used, peer_used, hit_base, n_still, fp_reuse, waves, nc, gate_recorded, ev_gate, ev_fp,
                    fp_i, fp_reuse_slot, fp_reuse_launches, h0, h_issued, fp_of_placement = std::move(fp_of_placement),
                    ctask_of_placement = std::move(ctask_of_placement), has_truth = std::move(has_truth),
@@ -1297,8 +1320,9 @@ St Pool::load_model_impl(const ModelDesc& m, const StatsView& stats, double cloc
     std::vector<char> verified(rel.size(), 0);  // relocated hits settled here
     for (std::size_t hix = 0; fp_reuse && hix < hit_keys.size(); ++hix) {
         const Key& k = hit_keys[hix];
-        const std::size_t slot = !fused || (split && hix < n_still) ? hit_base + hix
-                                 : hix < n_still                       ? nf + ctask_of_still[hix]
+        const std::size_t slot = !fused                                 ? hit_base + hix
+                                 : split && hix >= k_in && hix < n_still ? hit_base + (hix - k_in)
+                                 : hix < n_still                         ? nf + ctask_of_still[hix]
                                                  : nf + ctask_of_reloc[hit_rel[hix]];
         const Digest g = digest_at(slot);
         Entry* e = store_.entry(k);
