@@ -122,6 +122,8 @@ typedef struct {
     /* data plane (device pools) */
     uint64_t pcie_bytes, peer_bytes, device_src_bytes, fingerprint_bytes, repaired_bytes;
     uint32_t verify_mismatches, expected_mismatches;
+    /* relocate_ms: fused, the load kernel's span — with the verification split (at most three waves), from the
+     * first start to the last end of the load kernel and its concurrent K1 launch; unfused, the K3 waves */
     double plan_us, total_ms, relocate_ms, h2d_ms, peer_ms, fp_kernel_ms, fp_reuse_ms, fp_reuse_max_ms;
     /* host side of the call: entry -> all device work enqueued, waiting for it, entry -> return */
     double host_issue_us, host_wait_us, host_total_us;
